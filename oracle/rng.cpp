@@ -1,0 +1,36 @@
+// TEST INFRASTRUCTURE ONLY (oracle/). Reproduces the reference's seeded inputs bit for bit by
+// running the same libstdc++ generator + distribution code the reference uses:
+//   random_start  : std::mt19937_64(seed) + std::uniform_real_distribution<double>(-1,1),
+//                   column-major fill j-outer / i-inner        (proj/include/sssvd/moments.hpp:84-94)
+//   normal_stream : one std::normal_distribution<double>(0,1) object drawn `count` times from
+//                   std::mt19937_64(seed), as build_model / the tests' random_matrix fill it
+//                   (proj/include/sssvd/problems.hpp:53-59, proj/tests/test_solver.cpp:16-23)
+// Only tests/, bench.py's cpu_baseline leg and __graft_entry__.smoke() may load this.
+#include <cstdint>
+#include <random>
+
+extern "C" {
+
+int oracle_random_start(uint64_t seed, int64_t n, int64_t block_size, double* out) {
+  if (n < block_size) return 1;
+  std::mt19937_64 gen(seed);
+  std::uniform_real_distribution<double> dist(-1.0, 1.0);
+  for (int64_t j = 0; j < block_size; ++j)
+    for (int64_t i = 0; i < n; ++i) out[j * n + i] = dist(gen);
+  return 0;
+}
+
+void oracle_normal_stream(uint64_t seed, int64_t count, double* out) {
+  std::mt19937_64 gen(seed);
+  std::normal_distribution<double> dist(0.0, 1.0);
+  for (int64_t i = 0; i < count; ++i) out[i] = dist(gen);
+}
+
+// uniform(lo,hi) and exponential(1) streams for the config spectra (documented in DESIGN.md)
+void oracle_uniform_stream(uint64_t seed, int64_t count, double lo, double hi, double* out) {
+  std::mt19937_64 gen(seed);
+  std::uniform_real_distribution<double> dist(lo, hi);
+  for (int64_t i = 0; i < count; ++i) out[i] = dist(gen);
+}
+
+}  // extern "C"
