@@ -34,3 +34,13 @@ void oracle_uniform_stream(uint64_t seed, int64_t count, double lo, double hi, d
 }
 
 }  // extern "C"
+
+extern "C" {
+// C++ standard [rand.predef]: the 10000th consecutive invocation of a default-constructed
+// std::mt19937_64 produces 9981545732273789042. Pins that this helper runs the standard engine.
+uint64_t oracle_mt19937_64_check() {
+  std::mt19937_64 gen;
+  gen.discard(9999);
+  return gen();
+}
+}

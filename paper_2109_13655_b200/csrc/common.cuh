@@ -1,0 +1,100 @@
+// Shared device helpers for the B200 (sm_100a) shifted-solve path.
+//
+// Storage conventions:
+//   * complex128 is interleaved (double2: .x = Re, .y = Im), 16-byte aligned;
+//   * the shifted operator M_j = z_j I - G is stored ROW-MAJOR. Because G is symmetric,
+//     M_j is complex symmetric and its row-major array equals its column-major array, so
+//     the reference's column-major PartialPivLU (shifted_solver.hpp:24-26) and a row-major
+//     LU with row pivoting factor the same matrix; row-major makes every row swap and every
+//     GEMM operand row contiguous in HBM;
+//   * the starting block rides as L extra columns of each row (augmented [M_j | V]) so the
+//     forward elimination L^{-1} P V happens inside the factorisation's trailing updates.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sssvd_gpu {
+
+struct cplx {
+  double re, im;
+};
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a - b*c
+__device__ __forceinline__ double2 cfms(double2 a, double2 b, double2 c) {
+  a.x -= b.x * c.x - b.y * c.y;
+  a.y -= b.x * c.y + b.y * c.x;
+  return a;
+}
+__device__ __forceinline__ double2 crecip(double2 a) {
+  // 1/a with Smith-style scaling (a is a pivot, never both parts zero when called)
+  if (fabs(a.x) >= fabs(a.y)) {
+    double r = a.y / a.x, d = a.x + a.y * r;
+    return make_double2(1.0 / d, -r / d);
+  } else {
+    double r = a.x / a.y, d = a.y + a.x * r;
+    return make_double2(r / d, -1.0 / d);
+  }
+}
+__device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
+
+// D(8x8) += A(8x4, row) * B(4x8, col), FP64 tensor core (SASS DMMA.8x8x4).
+// Fragment ownership (lane t): A[t/4][t%4], B[t%4][t/4], C/D[t/4][2(t%4) + {0,1}].
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int bytes = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// ---- thread-block cluster helpers (DSMEM) ----
+__device__ __forceinline__ unsigned cluster_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// map a local shared address to the same offset in CTA `rank` of the cluster
+__device__ __forceinline__ unsigned dsmem_addr(const void* local, unsigned rank) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(local)), out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(s), "r"(rank));
+  return out;
+}
+__device__ __forceinline__ double ld_dsmem_f64(unsigned addr) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_dsmem_s32(unsigned addr) {
+  int v;
+  asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ double2 ld_dsmem_f64x2(unsigned addr) {
+  double2 v;
+  asm volatile("ld.shared::cluster.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+
+}  // namespace sssvd_gpu
+
+#define SSSVD_CUDA_TRY(expr)                                   \
+  do {                                                         \
+    cudaError_t _e = (expr);                                   \
+    if (_e != cudaSuccess) return ::sssvd_gpu::cuda_fail(_e, #expr, __FILE__, __LINE__); \
+  } while (0)

@@ -1,0 +1,45 @@
+// Launchers for the sm_100a kernels of the shifted-solve path (internal C++ interface).
+#pragma once
+#include <cstddef>
+#include <cuda_runtime.h>
+
+namespace sssvd_gpu {
+
+cudaError_t cuda_fail(cudaError_t e, const char* expr, const char* file, int line);
+
+// K0 Gram (gram.cu): G = A^T A, A column-major (lda even, K = rows incl. zero padding)
+cudaError_t gram(const double* A, int lda, int K, int n, double* G, int ldg, cudaStream_t s);
+// max |a_i| (lu.cu)
+cudaError_t absmax(const double* a, long long count, double* out, cudaStream_t s);
+
+// K1 assembly (lu.cu): mats[b] = [z_b I - G | V]  row-major, pitch ld
+cudaError_t assemble(const double* G, int n, int ldg, const double* V, int L, const double2* shifts,
+                     double2* out, int ld, long long stride, int batch, cudaStream_t s);
+// K2 leaf panel LU (lu.cu): rows [r0, n) x cols [r0, r0+w), W in {8,16,32}
+size_t leaf_smem_bytes(int n, int W, int cluster);
+cudaError_t leaf_lu(double2* mats, int ld, long long stride, int n, int r0, int w, int W, int cluster,
+                    int* ipiv, int batch, cudaStream_t s);
+// K3/K4 (lu.cu): interchanges ipiv[r0..r0+np) on columns [c0,c1), then optional unit-lower TRSM
+cudaError_t swap_trsm(double2* mats, int ld, long long stride, int n, int r0, int np, int c0, int c1,
+                      const int* ipiv, bool do_trsm, int batch, cudaStream_t s);
+// K6 (lu.cu): rows r0..r0+np of columns [c0,c1) <- U11^{-1} (.)
+cudaError_t trsm_upper(double2* mats, int ld, long long stride, int r0, int np, int c0, int c1,
+                       int batch, cudaStream_t s);
+cudaError_t pivot_floor(const double2* mats, int ld, long long stride, int n, const double2* shifts,
+                        const double* gmax, int* status, double* minpiv, int batch, cudaStream_t s);
+// K5 (zgemm.cu): C -= A B, row-major complex, batched
+cudaError_t zgemm_sub(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B,
+                      int ldb, long long sB, double2* C, int ldc, long long sC, int batch,
+                      cudaStream_t stream);
+// K7 (moments.cu)
+cudaError_t moments(const double2* mats, int ld, long long stride, int xcol, int n, int L, int nb,
+                    const double2* coef, int M, double* S, cudaStream_t s);
+cudaError_t blocks_to_colmajor(const double* S, int n, int L, int nblk, double* out, cudaStream_t s);
+cudaError_t colnorm_diff(const double* X, int ldx, const double* Y, int ldy, const double* s, int rows,
+                         int cols, double* out, cudaStream_t st);
+cudaError_t gather_cols(const double* src, int lds, const int* perm, const double* scale, int rows,
+                        int cols, double* dst, int ldd, cudaStream_t st);
+cudaError_t sumsq(const double* a, long long count, double* scratch, double* out, cudaStream_t s);
+cudaError_t pad_copy(const double* src, int rows, int cols, int lds, double* dst, int ldd, cudaStream_t s);
+
+}  // namespace sssvd_gpu

@@ -1,0 +1,446 @@
+// Blocked complex LU with partial (row) pivoting, batched over shifts, for sm_100a.
+//
+// Replaces Eigen::PartialPivLU<ComplexMatrix>::compute + solve on (z_j I - G)
+// (proj/include/sssvd/shifted_solver.hpp:20-40), one factorisation per quadrature point
+// (moments.hpp:113-114 / :158). Kernels in this file:
+//   * assemble_kernel    : M_j = z_j I - G, augmented with the starting block V (K1)
+//   * leaf_lu_kernel     : unblocked LU of an (m x W) leaf panel. One thread-block CLUSTER
+//                          per shift holds the whole leaf in distributed shared memory; the
+//                          pivot search is a warp-shuffle argmax inside each CTA followed by
+//                          a DSMEM exchange of the C per-CTA candidates, one cluster barrier
+//                          per column (K2)
+//   * swap_trsm_kernel   : applies a block of row interchanges to a column range (gather all
+//                          sources, then scatter: no serial swap chain) and, optionally, the
+//                          unit-lower triangular solve U12 = L11^{-1} A12 (K3 + K4)
+//   * trsm_upper_kernel  : X_b = U_bb^{-1} Y_b for the back substitution (K6)
+//   * pivot_floor_kernel : min |U_ii| against 1e-30 (max|G| + |z|) (shifted_solver.hpp:27-30)
+// The trailing updates are zgemm_sub (zgemm.cu, DMMA).
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sssvd_gpu {
+
+// ----------------------------------------------------------------------------- K1 assembly
+// Mj[i][c] = -G[i][c] + (i == c ? z_j : 0) for c < n ; V[i][c-n] for n <= c < n+L.
+// G is symmetric, so reading it row-major is reading it column-major (shifted_solver.hpp:24-25).
+__global__ void assemble_kernel(const double* __restrict__ G, int n, int ldg,
+                                const double* __restrict__ V, int L, const double2* __restrict__ shifts,
+                                double2* __restrict__ out, int ld, long long stride) {
+  const int b = blockIdx.y;
+  double2* M = out + b * stride;
+  const double2 z = shifts[b];
+  const long long total = (long long)n * (n + L);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / (n + L)), c = (int)(e % (n + L));
+    double2 v;
+    if (c < n) {
+      v = make_double2(-G[(size_t)i * ldg + c], 0.0);
+      if (c == i) {
+        v.x += z.x;
+        v.y += z.y;
+      }
+    } else {
+      // V is column-major n x L (moments.hpp:84-94 fill order)
+      v = make_double2(V[(size_t)(c - n) * n + i], 0.0);
+    }
+    M[(size_t)i * ld + c] = v;
+  }
+}
+
+cudaError_t assemble(const double* G, int n, int ldg, const double* V, int L, const double2* shifts,
+                     double2* out, int ld, long long stride, int batch, cudaStream_t s) {
+  long long total = (long long)n * (n + L);
+  int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 8);
+  assemble_kernel<<<dim3(blocks, batch), 256, 0, s>>>(G, n, ldg, V, L, shifts, out, ld, stride);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------- K2 leaf panel
+// One cluster (gridDim.x == cluster size C) per shift (blockIdx.y). CTA c owns rows
+// [r0 + c*R, r0 + (c+1)*R) of the leaf columns [r0, r0 + w). Panel pitch W+1 double2 keeps
+// the column walk of the pivot search bank-conflict free.
+template <int W>
+__global__ void __launch_bounds__(256, 1)
+leaf_lu_kernel(double2* mats, int ld, long long stride, int n, int r0, int w, int R, int* ipiv) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  constexpr int P = W + 1;
+  double2* slab = reinterpret_cast<double2*>(sm_raw);                  // R x P
+  double2* cand_vals = slab + (size_t)R * P;                           // [2][W]
+  double2* diag_vals = cand_vals + 2 * W;                              // [2][W]
+  double2* urow = diag_vals + 2 * W;                                   // [W]
+  double2* drow = urow + W;                                            // [W]
+  double* cand_score = reinterpret_cast<double*>(drow + W);            // [2]
+  int* cand_row = reinterpret_cast<int*>(cand_score + 2);              // [2]
+  double* red_s = reinterpret_cast<double*>(cand_row + 2);             // [8]
+  int* red_r = reinterpret_cast<int*>(red_s + 8);                      // [8]
+  int* win = red_r + 8;                                                // [2]: rank, row
+
+  const int C = gridDim.x;
+  const unsigned rank = cluster_ctarank();
+  const int b = blockIdx.y;
+  double2* Mb = mats + b * stride;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m = n - r0;
+  const int my0 = r0 + (int)rank * R;                 // first global row of my slab
+  const int myn = max(0, min(R, n - my0));            // rows I own
+
+  // load my slab
+  for (int e = tid; e < myn * W; e += blockDim.x) {
+    int i = e / W, c = e % W;
+    slab[i * P + c] = (c < w) ? Mb[(size_t)(my0 + i) * ld + r0 + c] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  (void)m;
+
+  for (int j = 0; j < w; ++j) {
+    const int d = r0 + j;           // diagonal row
+    const int par = j & 1;
+    // 1) local argmax of |a_ij|^2 over my rows i >= d (ties: smallest row)
+    double best = -1.0;
+    int brow = 0x7fffffff;
+    for (int i = tid; i < myn; i += blockDim.x) {
+      int gi = my0 + i;
+      if (gi < d) continue;
+      double s = cabs2(slab[i * P + j]);
+      if (s > best || (s == best && gi < brow)) {
+        best = s;
+        brow = gi;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      double os = __shfl_xor_sync(0xffffffffu, best, off);
+      int orow = __shfl_xor_sync(0xffffffffu, brow, off);
+      if (os > best || (os == best && orow < brow)) {
+        best = os;
+        brow = orow;
+      }
+    }
+    if (lane == 0) {
+      red_s[warp] = best;
+      red_r[warp] = brow;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      best = lane < (int)(blockDim.x >> 5) ? red_s[lane] : -1.0;
+      brow = lane < (int)(blockDim.x >> 5) ? red_r[lane] : 0x7fffffff;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        double os = __shfl_xor_sync(0xffffffffu, best, off);
+        int orow = __shfl_xor_sync(0xffffffffu, brow, off);
+        if (os > best || (os == best && orow < brow)) {
+          best = os;
+          brow = orow;
+        }
+      }
+      if (lane == 0) {
+        cand_score[par] = best;
+        cand_row[par] = brow;
+        red_r[0] = brow;
+      }
+    }
+    __syncthreads();
+    // 2) publish candidate row and (if owned) the diagonal row
+    {
+      const int crow = red_r[0];
+      if (tid < W) {
+        if (crow != 0x7fffffff) cand_vals[par * W + tid] = slab[(crow - my0) * P + tid];
+        if (d >= my0 && d < my0 + myn) diag_vals[par * W + tid] = slab[(d - my0) * P + tid];
+      }
+    }
+    // 3) cluster barrier: candidates of every CTA are visible
+    cluster_sync_all();
+    // 4) winner over the C candidates (DSMEM), same tie rule
+    if (warp == 0) {
+      double s = -1.0;
+      int r = 0x7fffffff, rk = lane;
+      if (lane < C) {
+        s = ld_dsmem_f64(dsmem_addr(&cand_score[par], lane));
+        r = ld_dsmem_s32(dsmem_addr(&cand_row[par], lane));
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        double os = __shfl_xor_sync(0xffffffffu, s, off);
+        int orow = __shfl_xor_sync(0xffffffffu, r, off);
+        int ork = __shfl_xor_sync(0xffffffffu, rk, off);
+        if (os > s || (os == s && orow < r)) {
+          s = os;
+          r = orow;
+          rk = ork;
+        }
+      }
+      if (lane == 0) {
+        win[0] = rk;
+        win[1] = r;
+      }
+    }
+    __syncthreads();
+    const int wrank = win[0], p = win[1];
+    const int downer = (d - r0) / R;
+    if (tid < W) {
+      urow[tid] = ld_dsmem_f64x2(dsmem_addr(&cand_vals[par * W + tid], wrank));
+      if ((int)rank == wrank && p != d) drow[tid] = ld_dsmem_f64x2(dsmem_addr(&diag_vals[par * W + tid], downer));
+    }
+    __syncthreads();
+    if (tid < W) {
+      if (d >= my0 && d < my0 + myn) slab[(d - my0) * P + tid] = urow[tid];
+      if ((int)rank == wrank && p != d) slab[(p - my0) * P + tid] = drow[tid];
+    }
+    if (rank == 0 && tid == 0) ipiv[(size_t)b * n + d] = p;
+    __syncthreads();
+    // 5) scale column j below the diagonal and rank-1 update the columns right of j
+    const double2 u = urow[j];
+    const bool nz = cabs2(u) != 0.0;
+    const double2 inv = nz ? crecip(u) : make_double2(0.0, 0.0);
+    const int first = max(0, d + 1 - my0);            // first local row strictly below d
+    const int ncol = w - j - 1;
+    if (nz && ncol > 0) {
+      for (int e = tid; e < (myn - first) * ncol; e += blockDim.x) {
+        int i = first + e / ncol, c = j + 1 + e % ncol;
+        double2 l = cmul(slab[i * P + j], inv);
+        slab[i * P + c] = cfms(slab[i * P + c], l, urow[c]);
+      }
+    }
+    __syncthreads();
+    if (nz)
+      for (int i = first + tid; i < myn; i += blockDim.x) slab[i * P + j] = cmul(slab[i * P + j], inv);
+    __syncthreads();
+  }
+  // write back (no other CTA reads my smem after the last barrier of the loop, but keep the
+  // cluster alive until everybody finished its DSMEM reads of the last column)
+  for (int e = tid; e < myn * w; e += blockDim.x) {
+    int i = e / w, c = e % w;
+    Mb[(size_t)(my0 + i) * ld + r0 + c] = slab[i * P + c];
+  }
+  cluster_sync_all();
+}
+
+template <int W>
+static cudaError_t launch_leaf(double2* mats, int ld, long long stride, int n, int r0, int w,
+                               int cluster, int* ipiv, int batch, cudaStream_t s) {
+  const int m = n - r0;
+  const int R = (m + cluster - 1) / cluster;
+  const size_t smem = (size_t)R * (W + 1) * sizeof(double2) + (6 * W) * sizeof(double2) + 256;
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(leaf_lu_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(leaf_lu_kernel<W>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cluster, batch, 1);
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, leaf_lu_kernel<W>, mats, ld, stride, n, r0, w, R, ipiv);
+}
+
+size_t leaf_smem_bytes(int n, int W, int cluster) {
+  const int R = (n + cluster - 1) / cluster;
+  return (size_t)R * (W + 1) * sizeof(double2) + (6 * W) * sizeof(double2) + 256;
+}
+
+cudaError_t leaf_lu(double2* mats, int ld, long long stride, int n, int r0, int w, int W,
+                    int cluster, int* ipiv, int batch, cudaStream_t s) {
+  switch (W) {
+    case 8: return launch_leaf<8>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s);
+    case 16: return launch_leaf<16>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s);
+    case 32: return launch_leaf<32>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// ----------------------------------------------------------------------------- K3+K4 swap/TRSM
+// For the pivots ipiv[r0 .. r0+np) (global row indices, LAPACK sequential-swap semantics) and
+// the columns [c0, c1): (1) warp 0 folds the np swaps into a list of (dst <- src) moves over the
+// <= 2 np touched rows; (2) each thread owns one column, gathers every source value, then
+// scatters (no serial dependency chain); (3) optionally solves the unit-lower L11 (rows/cols
+// r0..r0+np of the same matrix) against rows r0..r0+np of its column.
+constexpr int ST_COLS = 32;
+
+__global__ void __launch_bounds__(ST_COLS)
+swap_trsm_kernel(double2* mats, int ld, long long stride, int n, int r0, int np, int c0, int c1,
+                 const int* __restrict__ ipiv, int do_trsm) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  int* pos = reinterpret_cast<int*>(sm_raw);            // [2 np] touched positions
+  int* cont = pos + 2 * np;                             // [2 np] current content (source row)
+  int* slot = cont + 2 * np;                            // [np] list index of position r0+i
+  double2* buf = reinterpret_cast<double2*>(
+      (reinterpret_cast<uintptr_t>(slot + np) + 15) & ~uintptr_t(15));   // [2 np][ST_COLS]
+  double2* xs = buf + (size_t)2 * np * ST_COLS;         // [np][ST_COLS] TRSM work
+  const int b = blockIdx.y;
+  double2* Mb = mats + b * stride;
+  const int* piv = ipiv + (size_t)b * n;
+  const int lane = threadIdx.x;   // one warp per CTA
+
+  // fold the sequential interchanges into moves (warp-parallel ballot search)
+  int k = 0;
+  for (int j = 0; j < np; ++j) {
+    const int a = r0 + j, q = piv[r0 + j];
+    int ia = -1, iq = -1;
+    for (int base = 0; base < k; base += 32) {
+      const int t = base + lane;
+      const int pv = t < k ? pos[t] : -1;
+      const unsigned ba = __ballot_sync(0xffffffffu, pv == a);
+      const unsigned bq = __ballot_sync(0xffffffffu, pv == q);
+      if (ba && ia < 0) ia = base + __ffs(ba) - 1;
+      if (bq && iq < 0) iq = base + __ffs(bq) - 1;
+    }
+    if (ia < 0) {
+      if (lane == 0) { pos[k] = a; cont[k] = a; }
+      ia = k++;
+    }
+    if (q == a) iq = ia;
+    if (iq < 0) {
+      if (lane == 0) { pos[k] = q; cont[k] = q; }
+      iq = k++;
+    }
+    __syncwarp();
+    if (lane == 0 && ia != iq) { int t = cont[ia]; cont[ia] = cont[iq]; cont[iq] = t; }
+    __syncwarp();
+  }
+  for (int t = lane; t < k; t += 32)
+    if (pos[t] >= r0 && pos[t] < r0 + np) slot[pos[t] - r0] = t;
+  __syncwarp();
+  const int c = c0 + blockIdx.x * ST_COLS + lane;
+  if (c >= c1) return;
+  // gather every source, then scatter the rows that leave the block
+  for (int t = 0; t < k; ++t) buf[t * ST_COLS + lane] = Mb[(size_t)cont[t] * ld + c];
+  for (int t = 0; t < k; ++t)
+    if (pos[t] >= r0 + np) Mb[(size_t)pos[t] * ld + c] = buf[t * ST_COLS + lane];
+  for (int i = 0; i < np; ++i) xs[i * ST_COLS + lane] = buf[slot[i] * ST_COLS + lane];
+  if (do_trsm) {
+    for (int i = 1; i < np; ++i) {
+      double2 x = xs[i * ST_COLS + lane];
+      const double2* Lrow = Mb + (size_t)(r0 + i) * ld + r0;
+      for (int l = 0; l < i; ++l) x = cfms(x, Lrow[l], xs[l * ST_COLS + lane]);
+      xs[i * ST_COLS + lane] = x;
+    }
+  }
+  for (int i = 0; i < np; ++i) Mb[(size_t)(r0 + i) * ld + c] = xs[i * ST_COLS + lane];
+}
+
+size_t swap_trsm_smem(int np) {
+  return (size_t)(5 * np + 8) * sizeof(int) + (size_t)3 * np * ST_COLS * sizeof(double2) + 64;
+}
+
+cudaError_t swap_trsm(double2* mats, int ld, long long stride, int n, int r0, int np, int c0,
+                      int c1, const int* ipiv, bool do_trsm, int batch, cudaStream_t s) {
+  if (c1 <= c0 || np <= 0) return cudaSuccess;
+  const size_t smem = swap_trsm_smem(np);
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(swap_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  dim3 grid((c1 - c0 + ST_COLS - 1) / ST_COLS, batch);
+  swap_trsm_kernel<<<grid, ST_COLS, smem, s>>>(mats, ld, stride, n, r0, np, c0, c1, ipiv, do_trsm ? 1 : 0);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------- K6 upper TRSM
+// Rows r0..r0+np of the columns [c0, c1): x = U11^{-1} y, U11 non-unit upper (rows/cols r0..).
+__global__ void trsm_upper_kernel(double2* mats, int ld, long long stride, int r0, int np, int c0, int c1) {
+  extern __shared__ __align__(16) double2 xs[];   // [np][blockDim.x]
+  const int b = blockIdx.y;
+  double2* Mb = mats + b * stride;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int c = c0 + blockIdx.x * nt + tid;
+  if (c >= c1) return;
+  for (int i = 0; i < np; ++i) xs[i * nt + tid] = Mb[(size_t)(r0 + i) * ld + c];
+  for (int i = np - 1; i >= 0; --i) {
+    const double2* Urow = Mb + (size_t)(r0 + i) * ld + r0;
+    double2 x = xs[i * nt + tid];
+    for (int l = i + 1; l < np; ++l) x = cfms(x, Urow[l], xs[l * nt + tid]);
+    const double2 u = Urow[i];
+    x = cabs2(u) != 0.0 ? cmul(x, crecip(u)) : x;
+    xs[i * nt + tid] = x;
+  }
+  for (int i = 0; i < np; ++i) Mb[(size_t)(r0 + i) * ld + c] = xs[i * nt + tid];
+}
+
+cudaError_t trsm_upper(double2* mats, int ld, long long stride, int r0, int np, int c0, int c1,
+                       int batch, cudaStream_t s) {
+  if (c1 <= c0 || np <= 0) return cudaSuccess;
+  const int nt = 32;
+  const size_t smem = (size_t)np * nt * sizeof(double2);
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(trsm_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  dim3 grid((c1 - c0 + nt - 1) / nt, batch);
+  trsm_upper_kernel<<<grid, nt, smem, s>>>(mats, ld, stride, r0, np, c0, c1);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------- pivot floor
+// status[b] = 1 if min_i |U_ii| <= 1e-30 * (max|G| + |z_b|)  (shifted_solver.hpp:27-30)
+__global__ void pivot_floor_kernel(const double2* mats, int ld, long long stride, int n,
+                                   const double2* shifts, const double* gmax, int* status,
+                                   double* minpiv) {
+  const int b = blockIdx.x;
+  const double2* Mb = mats + b * stride;
+  double mn = 1e300;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) mn = fmin(mn, hypot(Mb[(size_t)i * ld + i].x, Mb[(size_t)i * ld + i].y));
+  __shared__ double red[32];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mn;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mn = fmin(mn, red[w]);
+    mn = fmin(mn, red[0]);
+    const double floor = 1e-30 * (gmax[0] + hypot(shifts[b].x, shifts[b].y));
+    status[b] = (mn <= floor || !(mn == mn)) ? 1 : 0;
+    minpiv[b] = mn;
+  }
+}
+
+cudaError_t pivot_floor(const double2* mats, int ld, long long stride, int n, const double2* shifts,
+                        const double* gmax, int* status, double* minpiv, int batch, cudaStream_t s) {
+  pivot_floor_kernel<<<batch, 256, 0, s>>>(mats, ld, stride, n, shifts, gmax, status, minpiv);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------- max |G|
+__global__ void absmax_kernel(const double* __restrict__ a, long long count, double* out) {
+  double m = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(a[i]));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+    // values are >= 0: the IEEE bit pattern orders like the unsigned integer
+    if (threadIdx.x == 0) atomicMax(reinterpret_cast<unsigned long long*>(out), (unsigned long long)__double_as_longlong(m));
+  }
+}
+
+cudaError_t absmax(const double* a, long long count, double* out, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), s);
+  if (e != cudaSuccess) return e;
+  absmax_kernel<<<148 * 4, 256, 0, s>>>(a, count, out);
+  return cudaGetLastError();
+}
+
+}  // namespace sssvd_gpu

@@ -1,0 +1,189 @@
+// K7: fused moment accumulation, plus the small HBM-bound kernels of the tail.
+//
+// Reference: MomentAccumulator::accumulate (proj/include/sssvd/moments.hpp:132-147)
+//   for k in 0..M: for j ascending: S_k += 2 Re(w_j t_j^k X_j); power_j *= t_j
+// which re-reads every X_j M+1 times on one CPU thread. Here every X_j element is read once
+// and all M+1 outputs are updated from registers. The coefficient table c[k][j] = w_j t_j^k is
+// formed on the host with the reference's own std::complex power chain, and the real part is
+// evaluated as 2*(cr*xr - ci*xi) with explicitly rounded (non-fused) operations, in ascending j
+// for every k: given identical X_j the result is bitwise the reference's.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sssvd_gpu {
+
+constexpr int MMAX = 32;
+
+// S is row-major [(M+1)][n][L]; X_j = rows 0..n-1, columns xcol..xcol+L-1 of mats[j].
+__global__ void __launch_bounds__(256)
+moments_kernel(const double2* __restrict__ mats, int ld, long long stride, int xcol, int n, int L,
+               int nb, const double2* __restrict__ coef, int M, double* __restrict__ S) {
+  extern __shared__ double2 cs[];   // [(M+1)][nb]
+  for (int t = threadIdx.x; t < (M + 1) * nb; t += blockDim.x) cs[t] = coef[t];
+  __syncthreads();
+  const long long nl = (long long)n * L;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nl;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / L), c = (int)(e % L);
+    double acc[MMAX + 1];
+#pragma unroll
+    for (int k = 0; k <= MMAX; ++k)
+      if (k <= M) acc[k] = S[k * nl + e];
+    for (int j = 0; j < nb; ++j) {
+      const double2 x = mats[j * stride + (size_t)i * ld + xcol + c];
+#pragma unroll
+      for (int k = 0; k <= MMAX; ++k) {
+        if (k <= M) {
+          const double2 w = cs[k * nb + j];
+          const double re = __dsub_rn(__dmul_rn(w.x, x.x), __dmul_rn(w.y, x.y));
+          acc[k] = __dadd_rn(acc[k], 2.0 * re);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k <= MMAX; ++k)
+      if (k <= M) S[k * nl + e] = acc[k];
+  }
+}
+
+cudaError_t moments(const double2* mats, int ld, long long stride, int xcol, int n, int L, int nb,
+                    const double2* coef, int M, double* S, cudaStream_t s) {
+  if (M > MMAX) return cudaErrorInvalidValue;
+  const long long nl = (long long)n * L;
+  int blocks = (int)std::min<long long>((nl + 255) / 256, 148 * 8);
+  moments_kernel<<<blocks, 256, (size_t)(M + 1) * nb * sizeof(double2), s>>>(mats, ld, stride, xcol, n,
+                                                                           L, nb, coef, M, S);
+  return cudaGetLastError();
+}
+
+// [(M+1)][n][L] row-major  ->  column-major blocks [(M+1)][L][n] (stacked n x (M+1)L matrix)
+__global__ void blocks_to_colmajor_kernel(const double* __restrict__ S, int n, int L, int nblk,
+                                          double* __restrict__ out) {
+  __shared__ double tile[32][33];
+  const int k = blockIdx.z;
+  const double* Sk = S + (size_t)k * n * L;
+  double* Ok = out + (size_t)k * n * L;
+  const int i0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    int i = i0 + r, c = c0 + threadIdx.x;
+    if (i < n && c < L) tile[r][threadIdx.x] = Sk[(size_t)i * L + c];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    int c = c0 + r, i = i0 + threadIdx.x;
+    if (i < n && c < L) Ok[(size_t)c * n + i] = tile[threadIdx.x][r];
+  }
+  (void)nblk;
+}
+
+cudaError_t blocks_to_colmajor(const double* S, int n, int L, int nblk, double* out, cudaStream_t s) {
+  dim3 grid((n + 31) / 32, (L + 31) / 32, nblk);
+  blocks_to_colmajor_kernel<<<grid, dim3(32, 8), 0, s>>>(S, n, L, nblk, out);
+  return cudaGetLastError();
+}
+
+// out[j] = || X[:, j] - s_j * Y[:, j] ||_2 for column-major X (ldx), Y (ldy), rows x cols.
+// One CTA per column; s == nullptr means s_j = 0. The residual kernel of the tail
+// (postprocess.hpp:36-39 exact residual, pipeline.hpp:205-207 Galerkin, :91-95 estimate).
+__global__ void colnorm_diff_kernel(const double* __restrict__ X, int ldx, const double* __restrict__ Y,
+                                    int ldy, const double* __restrict__ s, int rows,
+                                    double* __restrict__ out) {
+  const int j = blockIdx.x;
+  const double sj = s ? s[j] : 0.0;
+  const double* x = X + (size_t)j * ldx;
+  const double* y = Y ? Y + (size_t)j * ldy : nullptr;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < rows; i += blockDim.x) {
+    double v = x[i] - (y ? sj * y[i] : 0.0);
+    acc += v * v;
+  }
+  __shared__ double red[32];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (threadIdx.x == 0) out[j] = sqrt(acc);
+  }
+}
+
+cudaError_t colnorm_diff(const double* X, int ldx, const double* Y, int ldy, const double* s, int rows,
+                         int cols, double* out, cudaStream_t st) {
+  if (cols <= 0) return cudaSuccess;
+  colnorm_diff_kernel<<<cols, 256, 0, st>>>(X, ldx, Y, ldy, s, rows, out);
+  return cudaGetLastError();
+}
+
+// dst[:, j] = src[:, perm[j]] * (scale ? scale[j] : 1)   (column gather, column-major)
+__global__ void gather_cols_kernel(const double* __restrict__ src, int lds, const int* __restrict__ perm,
+                                   const double* __restrict__ scale, int rows, double* __restrict__ dst,
+                                   int ldd) {
+  const int j = blockIdx.x;
+  const double sc = scale ? scale[j] : 1.0;
+  const double* s = src + (size_t)perm[j] * lds;
+  double* d = dst + (size_t)j * ldd;
+  for (int i = threadIdx.x; i < rows; i += blockDim.x) d[i] = s[i] * sc;
+}
+
+cudaError_t gather_cols(const double* src, int lds, const int* perm, const double* scale, int rows,
+                        int cols, double* dst, int ldd, cudaStream_t st) {
+  if (cols <= 0) return cudaSuccess;
+  gather_cols_kernel<<<cols, 256, 0, st>>>(src, lds, perm, scale, rows, dst, ldd);
+  return cudaGetLastError();
+}
+
+// Frobenius norm squared (deterministic two-level reduction into out[0])
+__global__ void sumsq_kernel(const double* __restrict__ a, long long count, double* __restrict__ partial) {
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x)
+    acc += a[i] * a[i];
+  __shared__ double red[32];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (threadIdx.x == 0) partial[blockIdx.x] = acc;
+  }
+}
+
+__global__ void sum_partials_kernel(const double* __restrict__ partial, int cnt, double* out) {
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < cnt; i += 32) acc += partial[i];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (threadIdx.x == 0) out[0] = acc;
+}
+
+cudaError_t sumsq(const double* a, long long count, double* scratch /*>= 593 doubles*/, double* out,
+                  cudaStream_t s) {
+  const int blocks = 148 * 4;
+  sumsq_kernel<<<blocks, 256, 0, s>>>(a, count, scratch);
+  sum_partials_kernel<<<1, 32, 0, s>>>(scratch, blocks, out);
+  return cudaGetLastError();
+}
+
+// column-major (rows x cols, lda)  ->  row-major [rows][cols] complex with zero imaginary part
+__global__ void pad_copy_kernel(const double* __restrict__ src, int rows, int cols, int lds,
+                                double* __restrict__ dst, int ldd) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)ldd * cols;
+       e += (long long)gridDim.x * blockDim.x) {
+    int c = (int)(e / ldd), r = (int)(e % ldd);
+    dst[e] = r < rows ? src[(size_t)c * lds + r] : 0.0;
+  }
+}
+
+cudaError_t pad_copy(const double* src, int rows, int cols, int lds, double* dst, int ldd, cudaStream_t s) {
+  long long total = (long long)ldd * cols;
+  int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
+  pad_copy_kernel<<<blocks, 256, 0, s>>>(src, rows, cols, lds, dst, ldd);
+  return cudaGetLastError();
+}
+
+}  // namespace sssvd_gpu

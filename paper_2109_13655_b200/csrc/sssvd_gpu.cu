@@ -1,0 +1,984 @@
+// C-ABI implementation and host orchestration of the B200 shifted-solve path.
+//
+// Follows run_solve (proj/include/sssvd/pipeline.hpp:112-231) step for step:
+//   steps 1-2 : form_gram (K0) -> per shift batch: assemble (K1), blocked LU with the starting
+//               block riding as extra columns (K2-K5), back substitution (K6, K5), fused moment
+//               accumulation (K7) -> one ncclAllReduce over ranks
+//   step 3    : low_rank (QR + SVD of R)            \
+//   step 4    : project_qr (A U_S1, QR)              |  round-1 interim: cuSOLVER / cuBLAS
+//   step 5    : svd_small + assemble_triplets        |  (plain library QR/SVD/GEMM), the
+//   postproc. : tau, residual estimate, exact, Galerkin residual norms on the residual kernel
+// There is no CPU fallback: every numerical step runs on the GPU.
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/sssvd_gpu.h"
+#include "host_mirror.h"
+#include "kernels.h"
+
+namespace sssvd_gpu {
+
+cudaError_t cuda_fail(cudaError_t e, const char*, const char*, int) { return e; }
+
+struct Status : std::runtime_error {
+  sssvd_status code;
+  Status(sssvd_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(expr)                                                                                 \
+  do {                                                                                           \
+    cudaError_t _e = (expr);                                                                     \
+    if (_e != cudaSuccess)                                                                       \
+      throw Status(_e == cudaErrorMemoryAllocation ? SSSVD_E_OOM : SSSVD_E_CUDA,                 \
+                   std::string(#expr) + ": " + cudaGetErrorString(_e));                          \
+  } while (0)
+#define CKB(expr)                                                                                \
+  do {                                                                                           \
+    cublasStatus_t _s = (expr);                                                                  \
+    if (_s != CUBLAS_STATUS_SUCCESS) throw Status(SSSVD_E_CUDA, std::string(#expr) + " failed"); \
+  } while (0)
+#define CKS(expr)                                                                                \
+  do {                                                                                           \
+    cusolverStatus_t _s = (expr);                                                                \
+    if (_s != CUSOLVER_STATUS_SUCCESS) throw Status(SSSVD_E_CUDA, std::string(#expr) + " failed"); \
+  } while (0)
+#define CKN(expr)                                                                                \
+  do {                                                                                           \
+    ncclResult_t _r = (expr);                                                                    \
+    if (_r != ncclSuccess) throw Status(SSSVD_E_NCCL, std::string(#expr) + ": " + nccl().GetErrorString(_r)); \
+  } while (0)
+
+// device buffer with grow-only capacity
+struct DBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes) {
+    if (bytes > cap) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      cap = 0;
+      CK(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+      cap = std::max<size_t>(bytes, 256);
+    }
+    return p;
+  }
+  template <typename T>
+  T* as(size_t count) { return static_cast<T*>(get(count * sizeof(T))); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+// NCCL is resolved at run time (dlopen of the libnccl.so.2 already loaded by the host process,
+// e.g. torch's, else the system one) and only when a communicator is requested, so loading this
+// library never pins an NCCL version for the rest of the process.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+      api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+      api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+      api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+      api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy && api.GetErrorString;
+    }
+  }
+  if (!api.ok) throw Status(SSSVD_E_NCCL, "libnccl.so.2 not found");
+  return api;
+}
+
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace sssvd_gpu
+
+using namespace sssvd_gpu;
+
+enum TailBuf { T_SC, T_Q, T_R, T_UR, T_VR, T_SV, T_US1, T_QM, T_LEFT, T_RIGHT, T_PERM, T_UT, T_BM, T_PM, T_PHI,
+               T_QS, T_SIG, T_PS, T_QSC, T_COEFF, T_X, T_IMG, T_NRM, T_COUNT };
+
+struct sssvd_gpu_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cublasHandle_t blas = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  int max_batch = 0;
+  std::string err;
+  // operator (internal orientation: rows >= cols), column-major, lda even with zero padding
+  int64_t m = 0, n = 0, lda = 0;
+  bool transposed = false;
+  bool has_gram = false;
+  DBuf A, G, gmax, mats, ipiv, shifts, coef, S, V, status, minpiv, scratch;
+  DBuf t0, t1, t2, t7, work, info;
+  DBuf tail[24];
+  double t_gram = 0, t_solves = 0, t_allreduce = 0, solve_flops = 0;
+};
+
+struct sssvd_gpu_result {
+  sssvd_result_info info{};
+  std::vector<double> sigma, tau, estimated, exact, galerkin, left, right, basis_sv, blocks, q;
+  std::vector<int32_t> in_interval, spurious;
+  std::string note;
+};
+
+namespace sssvd_gpu {
+
+// ----------------------------------------------------------------------------- LU driver
+struct LuPlan {
+  int n, L, ld, NB, W, cluster;
+  long long stride;
+};
+
+static LuPlan make_plan(int n, int L) {
+  LuPlan p;
+  p.n = n;
+  p.L = L;
+  p.ld = ((n + L) + 7) / 8 * 8;
+  p.stride = (long long)n * p.ld;
+  p.NB = 64;
+  // leaf width W and cluster size C: the leaf slab (ceil(n/C) x (W+1) complex) must fit ~200 KB
+  const size_t budget = 200 * 1024;
+  p.W = 8;
+  p.cluster = 16;
+  const int Ws[3] = {32, 16, 8};
+  bool found = false;
+  for (int wi = 0; wi < 3 && !found; ++wi)
+    for (int c = 1; c <= 8 && !found; c *= 2)
+      if (leaf_smem_bytes(n, Ws[wi], c) <= budget) {
+        p.W = Ws[wi];
+        p.cluster = c;
+        found = true;
+      }
+  if (!found) {
+    for (int wi = 0; wi < 3 && !found; ++wi)
+      if (leaf_smem_bytes(n, Ws[wi], 16) <= budget) {
+        p.W = Ws[wi];
+        p.cluster = 16;
+        found = true;
+      }
+  }
+  if (!found) throw Status(SSSVD_E_LENGTH, "operator too large for the on-chip leaf panel");
+  return p;
+}
+
+// LU of nb augmented matrices [z I - G | V] in place (rows 0..n-1, cols 0..n+L-1), then the
+// back substitution U^{-1} on the L right-hand-side columns. ipiv: nb x n.
+static void lu_solve_batch(const LuPlan& P, double2* mats, int* ipiv, int nb, cudaStream_t s) {
+  const int n = P.n, ncols = n + P.L;
+  for (int kb = 0; kb < n; kb += P.NB) {
+    const int nbk = std::min(P.NB, n - kb);
+    for (int kc = kb; kc < kb + nbk; kc += P.W) {
+      const int w = std::min(P.W, kb + nbk - kc);
+      CK(leaf_lu(mats, P.ld, P.stride, n, kc, w, P.W, P.cluster, ipiv, nb, s));
+      if (kc > kb) CK(swap_trsm(mats, P.ld, P.stride, n, kc, w, kb, kc, ipiv, false, nb, s));
+      if (kc + w < kb + nbk) {
+        CK(swap_trsm(mats, P.ld, P.stride, n, kc, w, kc + w, kb + nbk, ipiv, true, nb, s));
+        const int M = n - (kc + w), N = kb + nbk - (kc + w);
+        if (M > 0)
+          CK(zgemm_sub(M, N, w, mats + (size_t)(kc + w) * P.ld + kc, P.ld, P.stride,
+                       mats + (size_t)kc * P.ld + kc + w, P.ld, P.stride,
+                       mats + (size_t)(kc + w) * P.ld + kc + w, P.ld, P.stride, nb, s));
+      }
+    }
+    const int c0 = kb + nbk;
+    if (c0 < ncols) {
+      CK(swap_trsm(mats, P.ld, P.stride, n, kb, nbk, c0, ncols, ipiv, true, nb, s));
+      const int M = n - c0, N = ncols - c0;
+      if (M > 0)
+        CK(zgemm_sub(M, N, nbk, mats + (size_t)c0 * P.ld + kb, P.ld, P.stride,
+                     mats + (size_t)kb * P.ld + c0, P.ld, P.stride, mats + (size_t)c0 * P.ld + c0, P.ld,
+                     P.stride, nb, s));
+    }
+  }
+  // back substitution on the RHS columns [n, n+L)
+  const int nblocks = (n + P.NB - 1) / P.NB;
+  for (int bi = nblocks - 1; bi >= 0; --bi) {
+    const int kb = bi * P.NB, nbk = std::min(P.NB, n - kb);
+    CK(trsm_upper(mats, P.ld, P.stride, kb, nbk, n, ncols, nb, s));
+    if (kb > 0)
+      CK(zgemm_sub(kb, P.L, nbk, mats + kb, P.ld, P.stride, mats + (size_t)kb * P.ld + n, P.ld, P.stride,
+                   mats + n, P.ld, P.stride, nb, s));
+  }
+}
+
+static size_t bytes_per_shift(const LuPlan& P) { return (size_t)P.stride * sizeof(double2) + (size_t)P.n * sizeof(int); }
+
+static int choose_batch(sssvd_gpu_ctx* ctx, const LuPlan& P, int64_t shifts) {
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  // keep what is already allocated for mats reusable; leave 4 GiB headroom for the tail
+  size_t avail = free_b + ctx->mats.cap + ctx->ipiv.cap;
+  const size_t headroom = (size_t)4 << 30;
+  avail = avail > headroom ? avail - headroom : avail / 2;
+  int64_t b = std::max<int64_t>(1, (int64_t)(avail / bytes_per_shift(P)));
+  b = std::min<int64_t>(b, shifts);
+  b = std::min<int64_t>(b, 32);
+  if (ctx->max_batch > 0) b = std::min<int64_t>(b, ctx->max_batch);
+  return (int)std::max<int64_t>(1, b);
+}
+
+// One pass over this rank's shifts [jb, je): S_dev (row-major [(M+1)][n][L]) is zeroed and
+// receives sum_j 2 Re(c[k][j] X_j) in ascending j. V_dev: n x L column-major (real).
+static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<double>>& shifts,
+                        const std::vector<std::complex<double>>& coef, int64_t h, int64_t jb, int64_t je,
+                        const double* V_dev, int L, int M, double* S_dev) {
+  cudaStream_t s = ctx->stream;
+  const int n = (int)ctx->n;
+  LuPlan P = make_plan(n, L);
+  CK(cudaMemsetAsync(S_dev, 0, sizeof(double) * (size_t)(M + 1) * n * L, s));
+  if (je <= jb) return;
+  const int B = choose_batch(ctx, P, je - jb);
+  double2* mats = ctx->mats.as<double2>((size_t)B * P.stride);
+  int* ipiv = ctx->ipiv.as<int>((size_t)B * n);
+  double2* dshift = ctx->shifts.as<double2>(B);
+  double2* dcoef = ctx->coef.as<double2>((size_t)(M + 1) * B);
+  int* dstatus = ctx->status.as<int>(B);
+  double* dmin = ctx->minpiv.as<double>(B);
+  std::vector<double2> hshift(B), hcoef((size_t)(M + 1) * B);
+  std::vector<int> hstatus(B);
+  for (int64_t j0 = jb; j0 < je; j0 += B) {
+    const int nb = (int)std::min<int64_t>(B, je - j0);
+    for (int b = 0; b < nb; ++b) hshift[b] = make_double2(shifts[j0 + b].real(), shifts[j0 + b].imag());
+    for (int k = 0; k <= M; ++k)
+      for (int b = 0; b < nb; ++b) {
+        const auto c = coef[(size_t)k * h + j0 + b];
+        hcoef[(size_t)k * nb + b] = make_double2(c.real(), c.imag());
+      }
+    CK(cudaMemcpyAsync(dshift, hshift.data(), sizeof(double2) * nb, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dcoef, hcoef.data(), sizeof(double2) * (M + 1) * nb, cudaMemcpyHostToDevice, s));
+    CK(assemble(ctx->G.as<double>(0), n, n, V_dev, L, dshift, mats, P.ld, P.stride, nb, s));
+    lu_solve_batch(P, mats, ipiv, nb, s);
+    CK(pivot_floor(mats, P.ld, P.stride, n, dshift, ctx->gmax.as<double>(1), dstatus, dmin, nb, s));
+    CK(moments(mats, P.ld, P.stride, n, n, L, nb, dcoef, M, S_dev, s));
+    CK(cudaMemcpyAsync(hstatus.data(), dstatus, sizeof(int) * nb, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int b = 0; b < nb; ++b)
+      if (hstatus[b]) throw Status(SSSVD_E_NUMERICAL, "ShiftedFactorization: shift numerically on the spectrum");
+    ctx->solve_flops += nb * (8.0 * n * (double)n * n / 3.0 + 8.0 * (double)n * n * L);
+  }
+}
+
+static void allreduce_S(sssvd_gpu_ctx* ctx, double* S, size_t count) {
+  if (!ctx->comm || ctx->nranks <= 1) return;
+  CKN(nccl().AllReduce(S, S, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+}
+
+// Gram of the current operator into ctx->G (row-major == column-major, symmetric) + max|G|
+static void ensure_gram(sssvd_gpu_ctx* ctx, int64_t cap) {
+  if (ctx->n <= 0) throw Status(SSSVD_E_INVALID_ARGUMENT, "no operator set");
+  if (ctx->n > cap) throw Status(SSSVD_E_LENGTH, "form_gram: column count exceeds the dense Gram cap");
+  if (ctx->has_gram) return;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, ctx->stream));
+  double* G = ctx->G.as<double>((size_t)ctx->n * ctx->n);
+  CK(gram(ctx->A.as<double>(0), (int)ctx->lda, (int)ctx->lda, (int)ctx->n, G, (int)ctx->n, ctx->stream));
+  CK(absmax(G, (long long)ctx->n * ctx->n, ctx->gmax.as<double>(1), ctx->stream));
+  CK(cudaEventRecord(e1, ctx->stream));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  ctx->t_gram = ms * 1e-3;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  ctx->has_gram = true;
+}
+
+// ----------------------------------------------------------------------------- dense tail helpers
+// column-major helpers on ctx->stream via cuBLAS/cuSOLVER (round-1 interim for QR / SVD)
+static void dgemm(sssvd_gpu_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* A,
+                  int lda, const double* B, int ldb, double beta, double* C, int ldc) {
+  if (m <= 0 || n <= 0) return;
+  CKB(cublasDgemm(ctx->blas, ta ? CUBLAS_OP_T : CUBLAS_OP_N, tb ? CUBLAS_OP_T : CUBLAS_OP_N, m, n, k, &alpha, A,
+                  lda, B, ldb, &beta, C, ldc));
+}
+
+// thin QR: A (m x k, lda=m) is overwritten by Q; R (k x k upper, ldr = k) returned
+static void thin_qr(sssvd_gpu_ctx* ctx, double* A, int m, int k, double* R) {
+  double* tau = ctx->t7.as<double>(k);
+  int* dinfo = ctx->info.as<int>(1);
+  int lw1 = 0, lw2 = 0;
+  CKS(cusolverDnDgeqrf_bufferSize(ctx->solver, m, k, A, m, &lw1));
+  CKS(cusolverDnDorgqr_bufferSize(ctx->solver, m, k, k, A, m, tau, &lw2));
+  double* work = ctx->work.as<double>(std::max(lw1, lw2));
+  CKS(cusolverDnDgeqrf(ctx->solver, m, k, A, m, tau, work, std::max(lw1, lw2), dinfo));
+  // R = upper triangle of the first k rows
+  CK(cudaMemset2DAsync(R, sizeof(double) * k, 0, sizeof(double) * k, k, ctx->stream));
+  for (int j = 0; j < k; ++j)
+    CK(cudaMemcpyAsync(R + (size_t)j * k, A + (size_t)j * m, sizeof(double) * (j + 1), cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+  CKS(cusolverDnDorgqr(ctx->solver, m, k, k, A, m, tau, work, std::max(lw1, lw2), dinfo));
+}
+
+// full SVD of a square k x k matrix B (destroyed): U (k x k), S (k, descending), V (k x k)
+static void svd_square(sssvd_gpu_ctx* ctx, double* B, int k, double* U, double* S, double* V) {
+  gesvdjInfo_t params;
+  CKS(cusolverDnCreateGesvdjInfo(&params));
+  CKS(cusolverDnXgesvdjSetTolerance(params, 1e-15));
+  CKS(cusolverDnXgesvdjSetMaxSweeps(params, 100));
+  int lwork = 0;
+  CKS(cusolverDnDgesvdj_bufferSize(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, 0, k, k, B, k, S, U, k, V, k, &lwork,
+                                   params));
+  double* work = ctx->work.as<double>(lwork);
+  int* dinfo = ctx->info.as<int>(1);
+  CKS(cusolverDnDgesvdj(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, 0, k, k, B, k, S, U, k, V, k, work, lwork, dinfo,
+                        params));
+  cusolverDnDestroyGesvdjInfo(params);
+}
+
+static std::vector<double> d2h(const double* d, size_t count, cudaStream_t s) {
+  std::vector<double> h(count);
+  if (count) {
+    CK(cudaMemcpyAsync(h.data(), d, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  return h;
+}
+
+static bool near_endpoint(double sigma, double endpoint) {
+  return std::abs(sigma - endpoint) <= 1e-9 * std::max(std::abs(endpoint), sigma);
+}
+
+static const char* kEmptyNote = "filter annihilated the starting block: no singular values inside the interval";
+
+// ----------------------------------------------------------------------------- run_solve
+static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gpu_result* res) {
+  cudaStream_t s = ctx->stream;
+  const int64_t n = ctx->n, m = ctx->m;
+  if (n <= 0) throw Status(SSSVD_E_INVALID_ARGUMENT, "no operator set");
+  validate_params(cfg.params, n);
+  const bool use_exp = cfg.mode == SSSVD_MODE_SS_SVD_NT || cfg.mode == SSSVD_MODE_NAIVE_NT;
+  const bool naive = cfg.mode == SSSVD_MODE_NAIVE || cfg.mode == SSSVD_MODE_NAIVE_NT;
+  Contour rule = make_contour(cfg.interval_a, cfg.interval_b, cfg.params.quadrature_count, cfg.aspect, use_exp);
+  const int L = (int)cfg.params.block_size, M = (int)cfg.params.moment_degree;
+  const int64_t h = cfg.params.quadrature_count / 2;
+  auto& info = res->info;
+  info.input_transposed = ctx->transposed;
+  info.n_internal = n;
+  info.block_size = L;
+  info.moment_degree = M;
+  info.calibration_index = -1;
+  info.rows = ctx->transposed ? n : m;
+  info.cols = ctx->transposed ? m : n;
+  ctx->t_solves = ctx->t_allreduce = ctx->solve_flops = 0;
+
+  // ---- steps 1-2
+  double t0 = now_s();
+  ensure_gram(ctx, cfg.gram_cap > 0 ? cfg.gram_cap : 8192);
+  std::vector<double> v0 = random_start(n, L, cfg.params.seed);
+  double start_norm2 = 0;
+  for (double x : v0) start_norm2 += x * x;
+  const double starting_norm = std::sqrt(start_norm2);
+  std::vector<std::complex<double>> shifts(h);
+  for (int64_t j = 0; j < h; ++j) shifts[j] = rule.shift(j);
+  std::vector<std::complex<double>> w(rule.weights.begin(), rule.weights.begin() + h);
+  std::vector<std::complex<double>> t(rule.nodes.begin(), rule.nodes.begin() + h);
+  int64_t jb = 0, je = h;
+  shard_range(h, ctx->nranks, ctx->rank, &jb, &je);
+  double* Vd = ctx->V.as<double>((size_t)n * L);
+  CK(cudaMemcpyAsync(Vd, v0.data(), sizeof(double) * n * L, cudaMemcpyHostToDevice, s));
+  double* S = ctx->S.as<double>((size_t)(M + 1) * n * L);
+  cudaEvent_t e0, e1, e2;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventCreate(&e2));
+  for (int64_t nu = 1; nu < cfg.params.refinement_steps; ++nu) {
+    // refine (moments.hpp:121-128): S0 <- 2 sum_j Re(w_j X_j) == moment pass with M = 0
+    CK(cudaEventRecord(e0, s));
+    moment_pass(ctx, shifts, w, h, jb, je, Vd, L, 0, S);
+    CK(cudaEventRecord(e1, s));
+    allreduce_S(ctx, S, (size_t)n * L);
+    CK(cudaEventRecord(e2, s));
+    CK(cudaEventSynchronize(e2));
+    float a = 0, b = 0;
+    CK(cudaEventElapsedTime(&a, e0, e1));
+    CK(cudaEventElapsedTime(&b, e1, e2));
+    ctx->t_solves += a * 1e-3;
+    ctx->t_allreduce += b * 1e-3;
+    // S0 row-major [n][L] -> column-major V
+    CK(blocks_to_colmajor(S, (int)n, L, 1, Vd, s));
+  }
+  auto coef = moment_coefficients(w, t, h, M);
+  CK(cudaEventRecord(e0, s));
+  moment_pass(ctx, shifts, coef, h, jb, je, Vd, L, M, S);
+  CK(cudaEventRecord(e1, s));
+  allreduce_S(ctx, S, (size_t)(M + 1) * n * L);
+  CK(cudaEventRecord(e2, s));
+  CK(cudaEventSynchronize(e2));
+  {
+    float a = 0, b = 0;
+    CK(cudaEventElapsedTime(&a, e0, e1));
+    CK(cudaEventElapsedTime(&b, e1, e2));
+    ctx->t_solves += a * 1e-3;
+    ctx->t_allreduce += b * 1e-3;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  // column-major blocks: Sc = [S_0 .. S_M] (n x (M+1)L); stacked = Sc[:, :LM], S+ = Sc[:, L:]
+  const int r = L * M;
+  auto& B = ctx->tail;
+  double* Sc = B[T_SC].as<double>((size_t)(M + 1) * n * L);
+  CK(blocks_to_colmajor(S, (int)n, L, M + 1, Sc, s));
+  CK(cudaStreamSynchronize(s));
+  info.steps_1_2 = now_s() - t0;
+  info.t_gram = ctx->t_gram;
+  info.t_shifted_solves = ctx->t_solves;
+  info.t_allreduce = ctx->t_allreduce;
+  info.shifted_solve_flops = ctx->solve_flops;
+  res->blocks = d2h(Sc, (size_t)(M + 1) * n * L, s);
+
+  // ---- step 3: low_rank (moments.hpp:190-211)
+  t0 = now_s();
+  double* scratch = ctx->scratch.as<double>(1024);
+  CK(sumsq(Sc, (long long)n * r, scratch, scratch + 1000, s));
+  const double snorm = std::sqrt(d2h(scratch + 1000, 1, s)[0]);
+  if (!(snorm > 1e-12 * starting_norm)) {   // pipeline.hpp:141-148
+    info.empty = 1;
+    res->note = kEmptyNote;
+    info.step_3 = now_s() - t0;
+    return;
+  }
+  double* Q = B[T_Q].as<double>((size_t)n * r);
+  CK(cudaMemcpyAsync(Q, Sc, sizeof(double) * n * r, cudaMemcpyDeviceToDevice, s));
+  double* R = B[T_R].as<double>((size_t)r * r);
+  thin_qr(ctx, Q, (int)n, r, R);
+  double* UR = B[T_UR].as<double>((size_t)r * r);
+  double* VR = B[T_VR].as<double>((size_t)r * r);   // W_S1 = VR[:, :rank]
+  double* SV = B[T_SV].as<double>(r);
+  svd_square(ctx, R, r, UR, SV, VR);
+  std::vector<double> sv = d2h(SV, r, s);
+  if (sv.empty() || !(sv[0] > 0)) {   // EmptySubspaceError caught at pipeline.hpp:151-156
+    info.empty = 1;
+    res->note = kEmptyNote;
+    info.step_3 = now_s() - t0;
+    return;
+  }
+  int rank = 0;
+  while (rank < r && sv[rank] >= cfg.params.lowrank_threshold * sv[0]) ++rank;
+  info.retained_rank = rank;
+  res->basis_sv.assign(sv.begin(), sv.begin() + rank);
+  double* US1 = B[T_US1].as<double>((size_t)n * rank);
+  dgemm(ctx, false, false, (int)n, rank, r, 1.0, Q, (int)n, UR, r, 0.0, US1, (int)n);
+  CK(cudaStreamSynchronize(s));
+  info.step_3 = now_s() - t0;
+
+  const double* Ad = ctx->A.as<double>(0);
+  const int lda = (int)ctx->lda;
+  const int tcount = rank;
+  std::vector<double> sigma(tcount);
+  std::vector<int> order(tcount);
+  std::vector<int32_t> invalid(tcount, 0);
+  std::iota(order.begin(), order.end(), 0);
+  double* Qm = B[T_QM].as<double>((size_t)rank * rank);
+  double* leftv = B[T_LEFT].as<double>((size_t)m * rank);
+  double* right = B[T_RIGHT].as<double>((size_t)n * rank);
+  int* perm_d = B[T_PERM].as<int>(rank);
+  double* Ut = nullptr;
+  double* Pm = nullptr;
+  if (!naive) {
+    // ---- step 4: project_qr (extract.hpp:43-57)
+    t0 = now_s();
+    Ut = B[T_UT].as<double>((size_t)m * rank);
+    dgemm(ctx, false, false, (int)m, rank, (int)n, 1.0, Ad, lda, US1, (int)n, 0.0, Ut, (int)m);
+    double* Bm = B[T_BM].as<double>((size_t)rank * rank);
+    thin_qr(ctx, Ut, (int)m, rank, Bm);
+    std::vector<double> bd = d2h(Bm, (size_t)rank * rank, s);
+    const double lead = std::abs(bd[0]);
+    for (int i = 0; i < rank; ++i)
+      if (std::abs(bd[(size_t)i * rank + i]) <= 1e-14 * lead) info.rank_deficient_qr = 1;
+    info.step_4 = now_s() - t0;
+    // ---- step 5: svd_small + assemble_triplets (extract.hpp:66-102)
+    t0 = now_s();
+    Pm = B[T_PM].as<double>((size_t)rank * rank);
+    double* phi_d = B[T_PHI].as<double>(rank);
+    svd_square(ctx, Bm, rank, Pm, phi_d, Qm);
+    std::vector<double> phi = d2h(phi_d, rank, s);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return phi[a] < phi[b]; });
+    for (int i = 0; i < rank; ++i) sigma[i] = phi[order[i]];
+  } else {
+    // ---- naive_eigen_route (extract.hpp:108-139): Rayleigh-Ritz on G in span(U_S1)
+    t0 = now_s();
+    double* GU = B[T_UT].as<double>((size_t)n * rank);
+    dgemm(ctx, false, false, (int)n, rank, (int)n, 1.0, ctx->G.as<double>(0), (int)n, US1, (int)n, 0.0, GU, (int)n);
+    double* H = B[T_BM].as<double>((size_t)rank * rank);
+    dgemm(ctx, true, false, rank, rank, (int)n, 1.0, US1, (int)n, GU, (int)n, 0.0, H, rank);
+    std::vector<double> hh = d2h(H, (size_t)rank * rank, s);
+    for (int i = 0; i < rank; ++i)
+      for (int j = 0; j < i; ++j) {
+        const double v = (hh[(size_t)j * rank + i] + hh[(size_t)i * rank + j]) / 2.0;
+        hh[(size_t)j * rank + i] = hh[(size_t)i * rank + j] = v;
+      }
+    CK(cudaMemcpyAsync(H, hh.data(), sizeof(double) * rank * rank, cudaMemcpyHostToDevice, s));
+    double* theta_d = B[T_PHI].as<double>(rank);
+    int lwork = 0;
+    CKS(cusolverDnDsyevd_bufferSize(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, rank, H, rank,
+                                    theta_d, &lwork));
+    double* work = ctx->work.as<double>(lwork);
+    CKS(cusolverDnDsyevd(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, rank, H, rank, theta_d, work,
+                         lwork, ctx->info.as<int>(1)));
+    std::vector<double> theta = d2h(theta_d, rank, s);   // ascending
+    CK(cudaMemcpyAsync(Qm, H, sizeof(double) * rank * rank, cudaMemcpyDeviceToDevice, s));
+    for (int i = 0; i < rank; ++i) {
+      sigma[i] = std::sqrt(std::max(theta[i], 0.0));
+      invalid[i] = theta[i] > 0 ? 0 : 1;
+    }
+  }
+  CK(cudaMemcpyAsync(perm_d, order.data(), sizeof(int) * rank, cudaMemcpyHostToDevice, s));
+  double* qs = B[T_QS].as<double>((size_t)rank * rank);           // q = Q[:, order]
+  CK(gather_cols(Qm, rank, perm_d, nullptr, rank, rank, qs, rank, s));
+  dgemm(ctx, false, false, (int)n, rank, rank, 1.0, US1, (int)n, qs, rank, 0.0, right, (int)n);
+  double* sig_d = B[T_SIG].as<double>(rank);
+  if (!naive) {
+    double* ps = B[T_PS].as<double>((size_t)rank * rank);         // P[:, order]
+    CK(gather_cols(Pm, rank, perm_d, nullptr, rank, rank, ps, rank, s));
+    dgemm(ctx, false, false, (int)m, rank, rank, 1.0, Ut, (int)m, ps, rank, 0.0, leftv, (int)m);
+  } else {
+    double* av = B[T_UT].as<double>((size_t)m * rank);
+    dgemm(ctx, false, false, (int)m, rank, (int)n, 1.0, Ad, lda, right, (int)n, 0.0, av, (int)m);
+    std::vector<double> inv(rank);
+    for (int i = 0; i < rank; ++i) inv[i] = invalid[i] ? 0.0 : 1.0 / sigma[i];
+    CK(cudaMemcpyAsync(sig_d, inv.data(), sizeof(double) * rank, cudaMemcpyHostToDevice, s));
+    std::vector<int> idn(rank);
+    std::iota(idn.begin(), idn.end(), 0);
+    CK(cudaMemcpyAsync(perm_d, idn.data(), sizeof(int) * rank, cudaMemcpyHostToDevice, s));
+    CK(gather_cols(av, (int)m, perm_d, sig_d, (int)m, rank, leftv, (int)m, s));
+  }
+  std::vector<double> qhost = d2h(qs, (size_t)rank * rank, s);
+  info.step_5 = now_s() - t0;
+
+  // ---- postprocess (pipeline.hpp:179-208)
+  t0 = now_s();
+  info.count = tcount;
+  res->sigma = sigma;
+  res->q = qhost;
+  res->in_interval.resize(tcount);
+  for (int i = 0; i < tcount; ++i) res->in_interval[i] = (sigma[i] >= cfg.interval_a && sigma[i] <= cfg.interval_b);
+  // detect_spurious (postprocess.hpp:47-62)
+  const double sv_max = *std::max_element(res->basis_sv.begin(), res->basis_sv.end());
+  for (double x : res->basis_sv)
+    if (!(x > 0)) throw Status(SSSVD_E_INVALID_ARGUMENT, "detect_spurious: Sigma_S1 must be positive");
+  info.spurious_threshold = cfg.params.spurious_threshold * sv_max;
+  res->tau.resize(tcount);
+  res->spurious.resize(tcount);
+  for (int i = 0; i < tcount; ++i) {
+    double num = 0, den = 0;
+    for (int l = 0; l < rank; ++l) {
+      const double v = qhost[(size_t)i * rank + l];
+      num += v * v;
+      den += v * v / res->basis_sv[l];
+    }
+    res->tau[i] = num / den;
+    res->spurious[i] = (res->tau[i] < info.spurious_threshold) || invalid[i];
+  }
+  // transformed residual norms (postprocess.hpp:76-97): ||S+ W Sigma^+ q_i - img_i U_S1 q_i|| / sigma_i
+  {
+    const double rcond = use_exp ? cfg.estimator_rcond_exp : cfg.estimator_rcond_identity;
+    std::vector<double> qsc(qhost.size());
+    for (int l = 0; l < rank; ++l) {
+      const double inv = res->basis_sv[l] >= rcond * sv_max ? 1.0 / res->basis_sv[l] : 0.0;
+      for (int i = 0; i < tcount; ++i) qsc[(size_t)i * rank + l] = inv * qhost[(size_t)i * rank + l];
+    }
+    double* qsc_d = B[T_QSC].as<double>((size_t)rank * tcount);
+    double* coeff = B[T_COEFF].as<double>((size_t)r * tcount);
+    double* X = B[T_X].as<double>((size_t)std::max(n, m) * tcount);
+    CK(cudaMemcpyAsync(qsc_d, qsc.data(), sizeof(double) * rank * tcount, cudaMemcpyHostToDevice, s));
+    dgemm(ctx, false, false, r, tcount, rank, 1.0, VR, r, qsc_d, rank, 0.0, coeff, r);
+    dgemm(ctx, false, false, (int)n, tcount, r, 1.0, Sc + (size_t)n * L, (int)n, coeff, r, 0.0, X, (int)n);
+    std::vector<double> images(tcount);
+    for (int i = 0; i < tcount; ++i) {
+      if (use_exp) images[i] = sigma[i] > 1e-30 ? std::log(sigma[i] * sigma[i]) : 0.0;   // g^{-1}(sigma^2)
+      else images[i] = sigma[i] * sigma[i];
+    }
+    double* img_d = B[T_IMG].as<double>(tcount);
+    CK(cudaMemcpyAsync(img_d, images.data(), sizeof(double) * tcount, cudaMemcpyHostToDevice, s));
+    double* out_d = B[T_NRM].as<double>(3 * (size_t)tcount);
+    CK(colnorm_diff(X, (int)n, right, (int)n, img_d, (int)n, tcount, out_d, s));
+    // exact residual ||A^T u - sigma v|| (postprocess.hpp:34-41), Galerkin ||A v - sigma u||
+    CK(cudaMemcpyAsync(sig_d, sigma.data(), sizeof(double) * tcount, cudaMemcpyHostToDevice, s));
+    dgemm(ctx, true, false, (int)n, tcount, (int)m, 1.0, Ad, lda, leftv, (int)m, 0.0, X, (int)n);
+    CK(colnorm_diff(X, (int)n, right, (int)n, sig_d, (int)n, tcount, out_d + tcount, s));
+    dgemm(ctx, false, false, (int)m, tcount, (int)n, 1.0, Ad, lda, right, (int)n, 0.0, X, (int)m);
+    CK(colnorm_diff(X, (int)m, leftv, (int)m, sig_d, (int)m, tcount, out_d + 2 * tcount, s));
+    std::vector<double> norms = d2h(out_d, 3 * (size_t)tcount, s);
+    res->estimated.assign(norms.begin(), norms.begin() + tcount);
+    for (int i = 0; i < tcount; ++i)
+      res->estimated[i] = sigma[i] <= 1e-30 ? std::numeric_limits<double>::infinity() : res->estimated[i] / sigma[i];
+    res->exact.assign(norms.begin() + tcount, norms.begin() + 2 * tcount);
+    res->galerkin.assign(norms.begin() + 2 * tcount, norms.end());
+  }
+  if (use_exp) {
+    // estimate_residual_nonlinear calibration (postprocess.hpp:121-156)
+    int best = -1;
+    for (int i = 0; i < tcount; ++i) {
+      if (!res->in_interval[i] || res->spurious[i]) continue;
+      if (best < 0 || res->tau[i] > res->tau[best]) best = i;
+    }
+    if (best < 0) {
+      std::fill(res->estimated.begin(), res->estimated.end(), std::numeric_limits<double>::quiet_NaN());
+      res->note = "nonlinear residual calibration impossible: all candidates spurious";
+    } else {
+      const double exact_best = res->exact[best];
+      const double mu = exact_best / res->estimated[best];
+      for (auto& x : res->estimated) x *= mu;
+      res->estimated[best] = exact_best;
+      info.calibration_index = best;
+      info.mu = mu;
+    }
+  }
+  res->left = d2h(leftv, (size_t)m * tcount, s);
+  res->right = d2h(right, (size_t)n * tcount, s);
+  info.postprocess = now_s() - t0;
+  if (ctx->transposed) {   // pipeline.hpp:214-217
+    std::swap(res->left, res->right);
+    std::swap(res->exact, res->galerkin);
+  }
+  for (int i = 0; i < tcount; ++i) {   // pipeline.hpp:219-229
+    if (!res->in_interval[i]) continue;
+    ++info.count_in_interval;
+    if (!res->spurious[i]) ++info.count_nonspurious_in_interval;
+    if (near_endpoint(sigma[i], cfg.interval_a) || near_endpoint(sigma[i], cfg.interval_b)) ++info.count_boundary;
+    else ++info.count_interior;
+  }
+}
+
+}  // namespace sssvd_gpu
+
+// ----------------------------------------------------------------------------- C ABI
+template <typename F>
+static sssvd_status guarded(sssvd_gpu_ctx* ctx, F&& body) {
+  try {
+    body();
+    return SSSVD_OK;
+  } catch (const Status& st) {
+    if (ctx) ctx->err = st.what();
+    return st.code;
+  } catch (const std::domain_error& ex) {
+    if (ctx) ctx->err = ex.what();
+    return SSSVD_E_DOMAIN;
+  } catch (const std::length_error& ex) {
+    if (ctx) ctx->err = ex.what();
+    return SSSVD_E_LENGTH;
+  } catch (const std::invalid_argument& ex) {
+    if (ctx) ctx->err = ex.what();
+    return SSSVD_E_INVALID_ARGUMENT;
+  } catch (const std::bad_alloc& ex) {
+    if (ctx) ctx->err = ex.what();
+    return SSSVD_E_OOM;
+  } catch (const std::exception& ex) {
+    if (ctx) ctx->err = ex.what();
+    return SSSVD_E_CUDA;
+  }
+}
+
+extern "C" {
+
+const char* sssvd_build_info(void) {
+  return "sssvd_gpu: sm_100a (compute_100a) DMMA/FP64 kernels";
+}
+
+sssvd_status sssvd_gpu_create(int device, sssvd_gpu_ctx** out) {
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count <= device) return SSSVD_E_CUDA;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return SSSVD_E_CUDA;
+  if (prop.major != 10) return SSSVD_E_CUDA;  // sm_100a binary only
+  auto* ctx = new sssvd_gpu_ctx();
+  ctx->device = device;
+  if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cublasCreate(&ctx->blas) != CUBLAS_STATUS_SUCCESS || cusolverDnCreate(&ctx->solver) != CUSOLVER_STATUS_SUCCESS) {
+    delete ctx;
+    return SSSVD_E_CUDA;
+  }
+  cublasSetStream(ctx->blas, ctx->stream);
+  cusolverDnSetStream(ctx->solver, ctx->stream);
+  *out = ctx;
+  return SSSVD_OK;
+}
+
+void sssvd_gpu_destroy(sssvd_gpu_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  DBuf* bufs[] = {&ctx->A, &ctx->G, &ctx->gmax, &ctx->mats, &ctx->ipiv, &ctx->shifts, &ctx->coef, &ctx->S, &ctx->V,
+                  &ctx->status, &ctx->minpiv, &ctx->scratch, &ctx->t0, &ctx->t1, &ctx->t2, &ctx->t7, &ctx->work,
+                  &ctx->info};
+  for (DBuf* b : bufs) b->release();
+  for (auto& b : ctx->tail) b.release();
+  if (ctx->comm) nccl().CommDestroy(ctx->comm);
+  if (ctx->solver) cusolverDnDestroy(ctx->solver);
+  if (ctx->blas) cublasDestroy(ctx->blas);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* sssvd_gpu_last_error(const sssvd_gpu_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+sssvd_status sssvd_gpu_set_batch(sssvd_gpu_ctx* ctx, int max_shifts) {
+  ctx->max_batch = max_shifts;
+  return SSSVD_OK;
+}
+
+sssvd_status sssvd_gpu_nccl_unique_id(void* out128) {
+  ncclUniqueId id;
+  try {
+    if (nccl().GetUniqueId(&id) != ncclSuccess) return SSSVD_E_NCCL;
+  } catch (const Status& st) {
+    return st.code;
+  }
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(out128, &id, sizeof(id));
+  return SSSVD_OK;
+}
+
+sssvd_status sssvd_gpu_init_comm(sssvd_gpu_ctx* ctx, const void* uid, int nranks, int rank) {
+  return guarded(ctx, [&]() {
+    CK(cudaSetDevice(ctx->device));
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof(id));
+    if (ctx->comm) nccl().CommDestroy(ctx->comm);
+    ctx->comm = nullptr;
+    CKN(nccl().CommInitRank(&ctx->comm, nranks, id, rank));
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+  });
+}
+
+sssvd_status sssvd_gpu_set_operator(sssvd_gpu_ctx* ctx, const double* a, int64_t rows, int64_t cols, int64_t lda,
+                                    int on_device) {
+  return guarded(ctx, [&]() {
+    if (rows <= 0 || cols <= 0 || lda < rows) throw Status(SSSVD_E_INVALID_ARGUMENT, "set_operator: bad shape");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const bool tr = rows < cols;
+    const int64_t m = tr ? cols : rows, n = tr ? rows : cols;
+    const int64_t ldp = (m + 7) / 8 * 8;
+    double* Ad = ctx->A.as<double>((size_t)ldp * n);
+    // stage the user matrix on the device, then pad (and transpose if needed) on the device
+    double* stage;
+    if (on_device) {
+      stage = const_cast<double*>(a);
+    } else {
+      stage = ctx->t0.as<double>((size_t)lda * cols);
+      CK(cudaMemcpyAsync(stage, a, sizeof(double) * lda * cols, cudaMemcpyHostToDevice, s));
+    }
+    if (!tr) {
+      CK(pad_copy(stage, (int)rows, (int)cols, (int)lda, Ad, (int)ldp, s));
+    } else {
+      // A^T via cuBLAS geam into a dense m x n buffer, then pad
+      double* tmp = ctx->t1.as<double>((size_t)m * n);
+      const double one = 1.0, zero = 0.0;
+      CKB(cublasDgeam(ctx->blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)m, (int)n, &one, stage, (int)lda, &zero, tmp, (int)m,
+                      tmp, (int)m));
+      CK(pad_copy(tmp, (int)m, (int)n, (int)m, Ad, (int)ldp, s));
+    }
+    // NaN / Inf check (problem.hpp:56-58): sum of squares is finite iff every entry is
+    double* scratch = ctx->scratch.as<double>(1024);
+    CK(sumsq(Ad, (long long)ldp * n, scratch, scratch + 1000, s));
+    double ss = 0;
+    CK(cudaMemcpyAsync(&ss, scratch + 1000, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (!std::isfinite(ss)) throw Status(SSSVD_E_INVALID_ARGUMENT, "ProblemMatrix: NaN/Inf entry");
+    ctx->m = m;
+    ctx->n = n;
+    ctx->lda = ldp;
+    ctx->transposed = tr;
+    ctx->has_gram = false;
+  });
+}
+
+sssvd_status sssvd_gpu_form_gram(sssvd_gpu_ctx* ctx, int64_t cap, double* g_out) {
+  return guarded(ctx, [&]() {
+    CK(cudaSetDevice(ctx->device));
+    ensure_gram(ctx, cap > 0 ? cap : 8192);
+    if (g_out) {
+      CK(cudaMemcpyAsync(g_out, ctx->G.as<double>(0), sizeof(double) * ctx->n * ctx->n, cudaMemcpyDeviceToHost,
+                         ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+    }
+  });
+}
+
+sssvd_status sssvd_gpu_shifted_solve(sssvd_gpu_ctx* ctx, const double* g, int64_t n, double zr, double zi,
+                                     const double* rhs, int64_t rhs_rows, int64_t L, double* x_out) {
+  return guarded(ctx, [&]() {
+    if (n <= 0 || L <= 0) throw Status(SSSVD_E_INVALID_ARGUMENT, "ShiftedFactorization: empty system");
+    if (rhs_rows != n) throw std::invalid_argument("ShiftedFactorization: right-hand side dimension mismatch");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    LuPlan P = make_plan((int)n, (int)L);
+    double2* mats = ctx->mats.as<double2>(P.stride);
+    int* ipiv = ctx->ipiv.as<int>(n);
+    double* Gd = ctx->t0.as<double>((size_t)n * n);
+    CK(cudaMemcpyAsync(Gd, g, sizeof(double) * n * n, cudaMemcpyHostToDevice, s));
+    double* gmax = ctx->t2.as<double>(1);
+    CK(absmax(Gd, (long long)n * n, gmax, s));
+    double2* dz = ctx->shifts.as<double2>(1);
+    double2 hz = make_double2(zr, zi);
+    CK(cudaMemcpyAsync(dz, &hz, sizeof(double2), cudaMemcpyHostToDevice, s));
+    // assemble with a zero RHS block, then write the complex RHS into the augmented columns
+    double* Vz = ctx->t1.as<double>((size_t)n * L);
+    CK(cudaMemsetAsync(Vz, 0, sizeof(double) * n * L, s));
+    CK(assemble(Gd, (int)n, (int)n, Vz, (int)L, dz, mats, P.ld, P.stride, 1, s));
+    // rhs: column-major complex n x L -> row-major columns n..n+L of mats
+    std::vector<double2> hrow((size_t)n * L);
+    for (int64_t c = 0; c < L; ++c)
+      for (int64_t i = 0; i < n; ++i) hrow[(size_t)i * L + c] = make_double2(rhs[2 * (c * n + i)], rhs[2 * (c * n + i) + 1]);
+    CK(cudaMemcpy2DAsync(mats + n, sizeof(double2) * P.ld, hrow.data(), sizeof(double2) * L, sizeof(double2) * L, n,
+                         cudaMemcpyHostToDevice, s));
+    lu_solve_batch(P, mats, ipiv, 1, s);
+    int* dstatus = ctx->status.as<int>(1);
+    double* dmin = ctx->minpiv.as<double>(1);
+    CK(pivot_floor(mats, P.ld, P.stride, (int)n, dz, gmax, dstatus, dmin, 1, s));
+    int hs = 0;
+    CK(cudaMemcpyAsync(&hs, dstatus, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpy2DAsync(hrow.data(), sizeof(double2) * L, mats + n, sizeof(double2) * P.ld, sizeof(double2) * L, n,
+                         cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hs) throw Status(SSSVD_E_NUMERICAL, "ShiftedFactorization: shift numerically on the spectrum");
+    for (int64_t c = 0; c < L; ++c)
+      for (int64_t i = 0; i < n; ++i) {
+        x_out[2 * (c * n + i)] = hrow[(size_t)i * L + c].x;
+        x_out[2 * (c * n + i) + 1] = hrow[(size_t)i * L + c].y;
+      }
+  });
+}
+
+sssvd_status sssvd_gpu_moments(sssvd_gpu_ctx* ctx, int64_t h, const double* shifts, const double* weights,
+                               const double* nodes, const double* s0, int64_t L, int64_t ell, int64_t M,
+                               double* s_out) {
+  return guarded(ctx, [&]() {
+    if (h < 1 || L < 1 || ell < 1 || M < 0) throw std::invalid_argument("moments: bad counts");
+    if (!ctx->has_gram) throw Status(SSSVD_E_INVALID_ARGUMENT, "moments: call sssvd_gpu_form_gram first");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const int64_t n = ctx->n;
+    std::vector<std::complex<double>> z(h), w(h), t(h);
+    for (int64_t j = 0; j < h; ++j) {
+      z[j] = {shifts[2 * j], shifts[2 * j + 1]};
+      w[j] = {weights[2 * j], weights[2 * j + 1]};
+      t[j] = {nodes[2 * j], nodes[2 * j + 1]};
+    }
+    int64_t jb = 0, je = h;
+    shard_range(h, ctx->nranks, ctx->rank, &jb, &je);
+    double* Vd = ctx->V.as<double>((size_t)n * L);
+    CK(cudaMemcpyAsync(Vd, s0, sizeof(double) * n * L, cudaMemcpyHostToDevice, s));
+    double* S = ctx->S.as<double>((size_t)(M + 1) * n * L);
+    for (int64_t nu = 1; nu < ell; ++nu) {
+      moment_pass(ctx, z, w, h, jb, je, Vd, (int)L, 0, S);
+      allreduce_S(ctx, S, (size_t)n * L);
+      CK(blocks_to_colmajor(S, (int)n, (int)L, 1, Vd, s));
+    }
+    auto coef = moment_coefficients(w, t, h, M);
+    moment_pass(ctx, z, coef, h, jb, je, Vd, (int)L, (int)M, S);
+    allreduce_S(ctx, S, (size_t)(M + 1) * n * L);
+    double* Sc = ctx->t0.as<double>((size_t)(M + 1) * n * L);
+    CK(blocks_to_colmajor(S, (int)n, (int)L, (int)M + 1, Sc, s));
+    CK(cudaMemcpyAsync(s_out, Sc, sizeof(double) * (M + 1) * n * L, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  });
+}
+
+sssvd_status sssvd_gpu_run_solve(sssvd_gpu_ctx* ctx, const sssvd_config* cfg, sssvd_gpu_result** out) {
+  *out = nullptr;
+  auto* res = new sssvd_gpu_result();
+  sssvd_status st;
+  {
+    auto body = [&]() {
+      CK(cudaSetDevice(ctx->device));
+      run_solve_impl(ctx, *cfg, res);
+    };
+    try {
+      body();
+      st = SSSVD_OK;
+    } catch (const Status& e) {
+      ctx->err = e.what();
+      st = e.code;
+    } catch (const std::domain_error& e) {
+      ctx->err = e.what();
+      st = SSSVD_E_DOMAIN;
+    } catch (const std::length_error& e) {
+      ctx->err = e.what();
+      st = SSSVD_E_LENGTH;
+    } catch (const std::invalid_argument& e) {
+      ctx->err = e.what();
+      st = SSSVD_E_INVALID_ARGUMENT;
+    } catch (const std::exception& e) {
+      ctx->err = e.what();
+      st = SSSVD_E_CUDA;
+    }
+  }
+  if (st != SSSVD_OK) {
+    delete res;
+    return st;
+  }
+  *out = res;
+  return SSSVD_OK;
+}
+
+sssvd_status sssvd_result_info_get(const sssvd_gpu_result* res, sssvd_result_info* info) {
+  *info = res->info;
+  return SSSVD_OK;
+}
+
+sssvd_status sssvd_result_copy(const sssvd_gpu_result* res, int field, void* dst) {
+  auto cp = [&](const auto& v) {
+    if (!v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+  };
+  switch (field) {
+    case SSSVD_FIELD_SIGMA: cp(res->sigma); break;
+    case SSSVD_FIELD_TAU: cp(res->tau); break;
+    case SSSVD_FIELD_ESTIMATED: cp(res->estimated); break;
+    case SSSVD_FIELD_EXACT: cp(res->exact); break;
+    case SSSVD_FIELD_GALERKIN: cp(res->galerkin); break;
+    case SSSVD_FIELD_IN_INTERVAL: cp(res->in_interval); break;
+    case SSSVD_FIELD_SPURIOUS: cp(res->spurious); break;
+    case SSSVD_FIELD_LEFT: cp(res->left); break;
+    case SSSVD_FIELD_RIGHT: cp(res->right); break;
+    case SSSVD_FIELD_BASIS_SV: cp(res->basis_sv); break;
+    case SSSVD_FIELD_BLOCKS: cp(res->blocks); break;
+    case SSSVD_FIELD_Q: cp(res->q); break;
+    default: return SSSVD_E_INVALID_ARGUMENT;
+  }
+  return SSSVD_OK;
+}
+
+const char* sssvd_result_note(const sssvd_gpu_result* res) { return res->note.c_str(); }
+void sssvd_result_free(sssvd_gpu_result* res) { delete res; }
+
+}  // extern "C"

@@ -1,0 +1,160 @@
+// Batched complex update  C[MxN] -= A[MxK] * B[KxN]  on the FP64 tensor cores (DMMA).
+//
+// This is the trailing update of the blocked LU (A = L21, B = U12, C = A22) and the block
+// update of the back substitution. The reference does this inside Eigen::PartialPivLU
+// (proj/include/sssvd/shifted_solver.hpp:26) on one CPU thread per shift.
+//
+// All operands are ROW-MAJOR interleaved complex128 (double2) with leading dimensions in
+// elements; blockIdx.z walks the batch of shifts. Complex products use the 4-real-product
+// form on mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4):
+//   Cre += Are*Bre + (-Aim)*Bim ,  Cim += Are*Bim + Aim*Bre
+// CTA tile 64x64 (4 warps, 32x32 each), K staged 16 at a time through a 3-deep cp.async ring.
+// Shared-memory row pitches are padded (A: 20, B: 66 double2) so every fragment load is one
+// conflict-free LDS.128 per quarter-warp.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sssvd_gpu {
+
+namespace {
+constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3;
+constexpr int LDA_S = BK + 4;   // 20 double2: row pitch of the A tile (== 4 mod 8)
+constexpr int LDB_S = BN + 2;   // 66 double2: row pitch of the B tile (== 2 mod 8)
+constexpr int A_STAGE = BM * LDA_S;
+constexpr int B_STAGE = BK * LDB_S;
+constexpr int THREADS = 128;
+
+__device__ __forceinline__ void load_stage(double2* As, double2* Bs, const double2* A, int lda,
+                                           const double2* B, int ldb, int M, int N, int K,
+                                           int m0, int n0, int k0, int tid) {
+#pragma unroll
+  for (int i = 0; i < (BM * BK) / THREADS; ++i) {
+    int idx = tid + i * THREADS;
+    int r = idx / BK, kk = idx % BK;
+    bool p = (m0 + r < M) && (k0 + kk < K);
+    const double2* src = p ? A + (size_t)(m0 + r) * lda + (k0 + kk) : A;
+    cp_async16(As + r * LDA_S + kk, src, p);
+  }
+#pragma unroll
+  for (int i = 0; i < (BK * BN) / THREADS; ++i) {
+    int idx = tid + i * THREADS;
+    int kk = idx / BN, c = idx % BN;
+    bool p = (k0 + kk < K) && (n0 + c < N);
+    const double2* src = p ? B + (size_t)(k0 + kk) * ldb + (n0 + c) : B;
+    cp_async16(Bs + kk * LDB_S + c, src, p);
+  }
+}
+}  // namespace
+
+__global__ void __launch_bounds__(THREADS, 2)
+zgemm_sub_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long long sA,
+                 const double2* __restrict__ B, int ldb, long long sB, double2* C, int ldc,
+                 long long sC) {
+  extern __shared__ __align__(16) double2 smem[];
+  double2* As = smem;
+  double2* Bs = smem + STAGES * A_STAGE;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  A += blockIdx.z * sA;
+  B += blockIdx.z * sB;
+  C += blockIdx.z * sC;
+
+  double acc_re[4][4][2], acc_im[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      acc_re[i][j][0] = acc_re[i][j][1] = 0.0;
+      acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
+    }
+
+  const int KT = (K + BK - 1) / BK;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_stage(As + s * A_STAGE, Bs + s * B_STAGE, A, lda, B, ldb, M, N, K, m0, n0, s * BK, tid);
+    cp_async_commit();
+  }
+  const int fr = lane >> 2, fc = lane & 3;
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      int nk = kt + STAGES - 1;
+      if (nk < KT) {
+        int st = nk % STAGES;
+        load_stage(As + st * A_STAGE, Bs + st * B_STAGE, A, lda, B, ldb, M, N, K, m0, n0, nk * BK, tid);
+      }
+      cp_async_commit();
+    }
+    const double2* as = As + (kt % STAGES) * A_STAGE + (wm * 32 + fr) * LDA_S + fc;
+    const double2* bs = Bs + (kt % STAGES) * B_STAGE + fc * LDB_S + wn * 32 + fr;
+#pragma unroll
+    for (int kq = 0; kq < BK / 4; ++kq) {
+      double2 a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = as[i * 8 * LDA_S + kq * 4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = bs[kq * 4 * LDB_S + j * 8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double nai = -a[i].y;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          dmma884(acc_re[i][j][0], acc_re[i][j][1], a[i].x, b[j].x);
+          dmma884(acc_re[i][j][0], acc_re[i][j][1], nai, b[j].y);
+          dmma884(acc_im[i][j][0], acc_im[i][j][1], a[i].x, b[j].y);
+          dmma884(acc_im[i][j][0], acc_im[i][j][1], a[i].y, b[j].x);
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+
+  // epilogue: C -= acc (fragment rows fr, cols 2*fc, 2*fc+1 of each 8x8 sub-tile)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = m0 + wm * 32 + i * 8 + fr;
+    if (r >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = n0 + wn * 32 + j * 8 + 2 * fc;
+      double2* cp = C + (size_t)r * ldc + c;
+      if (c + 1 < N) {
+        double2 v0 = cp[0], v1 = cp[1];
+        v0.x -= acc_re[i][j][0];
+        v0.y -= acc_im[i][j][0];
+        v1.x -= acc_re[i][j][1];
+        v1.y -= acc_im[i][j][1];
+        cp[0] = v0;
+        cp[1] = v1;
+      } else if (c < N) {
+        double2 v0 = cp[0];
+        v0.x -= acc_re[i][j][0];
+        v0.y -= acc_im[i][j][0];
+        cp[0] = v0;
+      }
+    }
+  }
+}
+
+size_t zgemm_sub_smem() { return (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double2); }
+
+cudaError_t zgemm_sub(int M, int N, int K, const double2* A, int lda, long long sA,
+                      const double2* B, int ldb, long long sB, double2* C, int ldc, long long sC,
+                      int batch, cudaStream_t stream) {
+  if (M <= 0 || N <= 0 || K <= 0 || batch <= 0) return cudaSuccess;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(zgemm_sub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)zgemm_sub_smem());
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch);
+  zgemm_sub_kernel<<<grid, THREADS, zgemm_sub_smem(), stream>>>(M, N, K, A, lda, sA, B, ldb, sB, C,
+                                                                 ldc, sC);
+  return cudaGetLastError();
+}
+
+}  // namespace sssvd_gpu

@@ -1,0 +1,623 @@
+"""Python mirror of the reference `sssvd` API over the C ABI of libsssvd_gpu.so.
+
+The reference is a header-only C++ library (proj/include/sssvd); this module exposes the same
+names, argument meanings and error behaviour for the shifted-solve path so the parity tests read
+like the reference's own tests:
+
+    ProblemMatrix.from_dense   problem.hpp:20-25       form_gram            problem.hpp:81-95
+    ContourRule / build_contour contour.hpp:27-62     SpectralTransform     transform.hpp:16-45
+    SsParams (+ validate)      moments.hpp:23-47       random_start         moments.hpp:84-94
+    ShiftedFactorization       shifted_solver.hpp:20-40 (factor_shift / solve_block :77-87)
+    DenseShiftedSolver         shifted_solver.hpp:54-75
+    MomentAccumulator          moments.hpp:101-169 (refine / accumulate)
+    RunConfig / run_solve      pipeline.hpp:43-58 / :112-231
+Errors map back onto the reference's exception types (core.hpp:29-39).
+
+Everything numerical runs in the CUDA library; there is no CPU fallback. Loading this module
+without the built library, or calling a compute entry point without a B200, raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsssvd_gpu.so")
+
+
+# ----------------------------------------------------------------------------- errors
+class NumericalError(RuntimeError):
+    """core.hpp:29-32."""
+
+
+class EmptySubspaceError(NumericalError):
+    """core.hpp:36-39."""
+
+
+class DomainError(ValueError):
+    """std::domain_error."""
+
+
+class LengthError(ValueError):
+    """std::length_error."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+SSSVD_OK, E_INVALID, E_DOMAIN, E_LENGTH, E_NUMERICAL, E_EMPTY, E_CUDA, E_NCCL, E_OOM = range(9)
+
+
+def _raise(code: int, msg: str):
+    if code == E_INVALID:
+        raise ValueError(msg)
+    if code == E_DOMAIN:
+        raise DomainError(msg)
+    if code == E_LENGTH:
+        raise LengthError(msg)
+    if code == E_NUMERICAL:
+        raise NumericalError(msg)
+    if code == E_EMPTY:
+        raise EmptySubspaceError(msg)
+    raise CudaError(f"status {code}: {msg}")
+
+
+# ----------------------------------------------------------------------------- C structs
+class _Params(ctypes.Structure):
+    _fields_ = [("block_size", ctypes.c_int64), ("moment_degree", ctypes.c_int64),
+                ("quadrature_count", ctypes.c_int64), ("refinement_steps", ctypes.c_int64),
+                ("lowrank_threshold", ctypes.c_double), ("spurious_threshold", ctypes.c_double),
+                ("seed", ctypes.c_uint64)]
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [("interval_a", ctypes.c_double), ("interval_b", ctypes.c_double),
+                ("mode", ctypes.c_int32), ("aspect", ctypes.c_double), ("params", _Params),
+                ("threads", ctypes.c_int32), ("estimator_rcond_identity", ctypes.c_double),
+                ("estimator_rcond_exp", ctypes.c_double), ("gram_cap", ctypes.c_int64)]
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [("count", ctypes.c_int64), ("rows", ctypes.c_int64), ("cols", ctypes.c_int64),
+                ("retained_rank", ctypes.c_int64), ("n_internal", ctypes.c_int64),
+                ("block_size", ctypes.c_int64), ("moment_degree", ctypes.c_int64),
+                ("empty", ctypes.c_int32), ("input_transposed", ctypes.c_int32),
+                ("rank_deficient_qr", ctypes.c_int32),
+                ("count_in_interval", ctypes.c_int64),
+                ("count_nonspurious_in_interval", ctypes.c_int64),
+                ("count_interior", ctypes.c_int64), ("count_boundary", ctypes.c_int64),
+                ("calibration_index", ctypes.c_int64), ("mu", ctypes.c_double),
+                ("spurious_threshold", ctypes.c_double),
+                ("steps_1_2", ctypes.c_double), ("step_3", ctypes.c_double),
+                ("step_4", ctypes.c_double), ("step_5", ctypes.c_double),
+                ("postprocess", ctypes.c_double), ("t_gram", ctypes.c_double),
+                ("t_shifted_solves", ctypes.c_double), ("t_allreduce", ctypes.c_double),
+                ("shifted_solve_flops", ctypes.c_double)]
+
+
+EXPORTED_SYMBOLS = [
+    "sssvd_default_config", "sssvd_gpu_create", "sssvd_gpu_destroy", "sssvd_gpu_last_error",
+    "sssvd_gpu_set_batch", "sssvd_gpu_nccl_unique_id", "sssvd_gpu_init_comm", "sssvd_shard_range",
+    "sssvd_gpu_set_operator", "sssvd_gpu_form_gram", "sssvd_gpu_shifted_solve", "sssvd_gpu_moments",
+    "sssvd_gpu_run_solve", "sssvd_result_info_get", "sssvd_result_copy", "sssvd_result_note",
+    "sssvd_result_free", "sssvd_contour", "sssvd_random_start", "sssvd_validate_params",
+    "sssvd_moment_coefficients", "sssvd_build_info",
+]
+
+_lib = None
+
+
+def lib():
+    """Load libsssvd_gpu.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2109_13655_b200.build`")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i64, dp, ip = ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int
+    L.sssvd_default_config.argtypes = [ctypes.POINTER(_Config)]
+    L.sssvd_gpu_create.argtypes = [ctypes.c_int, ctypes.POINTER(vp)]
+    L.sssvd_gpu_destroy.argtypes = [vp]
+    L.sssvd_gpu_last_error.argtypes = [vp]
+    L.sssvd_gpu_last_error.restype = ctypes.c_char_p
+    L.sssvd_gpu_set_batch.argtypes = [vp, ctypes.c_int]
+    L.sssvd_gpu_nccl_unique_id.argtypes = [vp]
+    L.sssvd_gpu_init_comm.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int]
+    L.sssvd_shard_range.argtypes = [i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.sssvd_shard_range.restype = None
+    L.sssvd_gpu_set_operator.argtypes = [vp, dp, i64, i64, i64, ip]
+    L.sssvd_gpu_form_gram.argtypes = [vp, i64, dp]
+    L.sssvd_gpu_shifted_solve.argtypes = [vp, dp, i64, ctypes.c_double, ctypes.c_double, dp, i64, i64, dp]
+    L.sssvd_gpu_moments.argtypes = [vp, i64, dp, dp, dp, dp, i64, i64, i64, dp]
+    L.sssvd_gpu_run_solve.argtypes = [vp, ctypes.POINTER(_Config), ctypes.POINTER(vp)]
+    L.sssvd_result_info_get.argtypes = [vp, ctypes.POINTER(_Info)]
+    L.sssvd_result_copy.argtypes = [vp, ctypes.c_int, dp]
+    L.sssvd_result_note.argtypes = [vp]
+    L.sssvd_result_note.restype = ctypes.c_char_p
+    L.sssvd_result_free.argtypes = [vp]
+    L.sssvd_result_free.restype = None
+    L.sssvd_contour.argtypes = [ctypes.c_double, ctypes.c_double, i64, ctypes.c_double, ctypes.c_int, dp, dp, dp]
+    L.sssvd_random_start.argtypes = [i64, i64, ctypes.c_uint64, dp]
+    L.sssvd_validate_params.argtypes = [ctypes.POINTER(_Params), i64]
+    L.sssvd_moment_coefficients.argtypes = [i64, dp, dp, i64, dp]
+    L.sssvd_build_info.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+# ----------------------------------------------------------------------------- transform / contour
+IDENTITY, EXP = 0, 1
+
+
+class SpectralTransform:
+    """transform.hpp:16-45."""
+
+    def __init__(self, kind: int):
+        self._kind = kind
+
+    @staticmethod
+    def identity():
+        return SpectralTransform(IDENTITY)
+
+    @staticmethod
+    def exponential():
+        return SpectralTransform(EXP)
+
+    def kind(self):
+        return self._kind
+
+    def g(self, t):
+        return t if self._kind == IDENTITY else np.exp(t)
+
+    def g_inverse(self, z: float) -> float:
+        if self._kind == IDENTITY:
+            return z
+        if not z > 0:
+            raise DomainError("SpectralTransform: g_inverse of non-positive value under Exp")
+        return math.log(z)
+
+    def g_prime(self, t: float) -> float:
+        return 1.0 if self._kind == IDENTITY else math.exp(t)
+
+
+class ContourRule:
+    """contour.hpp:27-62, computed by the library's host mirror (host_mirror.cpp)."""
+
+    def __init__(self, a: float, b: float, count: int, aspect: float, transform: SpectralTransform):
+        nodes = np.empty(2 * count)
+        weights = np.empty(2 * count)
+        cr = np.empty(2)
+        st = lib().sssvd_contour(a, b, count, aspect, transform.kind(), _ptr(nodes), _ptr(weights), _ptr(cr))
+        if st != SSSVD_OK:
+            _raise(st, "ContourRule: " + ("Exp transform requires a > 0" if st == E_DOMAIN else "bad arguments"))
+        self._a, self._b, self._count, self._aspect, self._transform = a, b, count, aspect, transform
+        self._center, self._radius = float(cr[0]), float(cr[1])
+        self._nodes = nodes.view(np.complex128).copy()
+        self._weights = weights.view(np.complex128).copy()
+
+    def interval_a(self): return self._a
+    def interval_b(self): return self._b
+    def center(self): return self._center
+    def radius(self): return self._radius
+    def aspect(self): return self._aspect
+    def count(self): return self._count
+    def transform(self): return self._transform
+    def nodes(self): return self._nodes
+    def weights(self): return self._weights
+
+    def shift(self, j: int) -> complex:
+        t = complex(self._nodes[j])
+        if self._transform.kind() == IDENTITY:
+            return t
+        e = math.exp(t.real)
+        return complex(e * math.cos(t.imag), e * math.sin(t.imag))
+
+
+def build_contour(a, b, count, aspect, transform):
+    return ContourRule(a, b, count, aspect, transform)
+
+
+# ----------------------------------------------------------------------------- params / config
+@dataclass
+class SsParams:
+    """moments.hpp:23-47."""
+    block_size: int = 20
+    moment_degree: int = 4
+    quadrature_count: int = 32
+    refinement_steps: int = 1
+    lowrank_threshold: float = 1e-20
+    spurious_threshold: float = 1e-8
+    seed: int = 42
+
+    def subspace_dim(self):
+        return self.block_size * self.moment_degree
+
+    def _c(self):
+        return _Params(self.block_size, self.moment_degree, self.quadrature_count, self.refinement_steps,
+                       self.lowrank_threshold, self.spurious_threshold, self.seed)
+
+    def validate(self, n: int):
+        p = self._c()
+        if lib().sssvd_validate_params(ctypes.byref(p), n) != SSSVD_OK:
+            raise ValueError("SsParams: invalid parameters")
+
+
+class SolveMode:
+    """pipeline.hpp:24."""
+    SsSvd, SsSvdNT, Naive, NaiveNT = 0, 1, 2, 3
+
+
+@dataclass
+class RunConfig:
+    """pipeline.hpp:43-58 (+ the form_gram cap, problem.hpp:82)."""
+    interval_a: float = 0.0
+    interval_b: float = 1.0
+    mode: int = SolveMode.SsSvd
+    aspect: float = 0.1
+    params: SsParams = field(default_factory=SsParams)
+    threads: int = 0
+    estimator_rcond_identity: float = 2e-15
+    estimator_rcond_exp: float = 1e-14
+    gram_cap: int = 8192
+
+    def transform(self):
+        return SpectralTransform(EXP if self.mode in (SolveMode.SsSvdNT, SolveMode.NaiveNT) else IDENTITY)
+
+    def _c(self):
+        return _Config(self.interval_a, self.interval_b, self.mode, self.aspect, self.params._c(), self.threads,
+                       self.estimator_rcond_identity, self.estimator_rcond_exp, self.gram_cap)
+
+
+def random_start(n: int, block_size: int, seed: int) -> np.ndarray:
+    """moments.hpp:84-94 (libstdc++ mt19937_64 in the library's host mirror)."""
+    out = np.empty((n, block_size), order="F")
+    if lib().sssvd_random_start(n, block_size, seed, _ptr(out)) != SSSVD_OK:
+        raise ValueError("random_start: block size exceeds dimension")
+    return out
+
+
+def moment_coefficients(weights, nodes, degree: int) -> np.ndarray:
+    """c[k][j] = w_j t_j^k with the reference's power chain (moments.hpp:138-144)."""
+    w = np.ascontiguousarray(weights, dtype=np.complex128)
+    t = np.ascontiguousarray(nodes, dtype=np.complex128)
+    out = np.empty((degree + 1) * w.size, dtype=np.complex128)
+    st = lib().sssvd_moment_coefficients(w.size, _ptr(w), _ptr(t), degree, _ptr(out))
+    if st != SSSVD_OK:
+        _raise(st, "moment_coefficients")
+    return out.reshape(degree + 1, w.size)
+
+
+def shard_range(h: int, nranks: int, rank: int):
+    b, e = ctypes.c_int64(), ctypes.c_int64()
+    lib().sssvd_shard_range(h, nranks, rank, ctypes.byref(b), ctypes.byref(e))
+    return b.value, e.value
+
+
+# ----------------------------------------------------------------------------- device context
+class Device:
+    """One B200 context: owns device memory, the stream and the optional NCCL communicator."""
+
+    def __init__(self, device: int = 0):
+        h = ctypes.c_void_p()
+        st = lib().sssvd_gpu_create(device, ctypes.byref(h))
+        if st != SSSVD_OK:
+            raise CudaError(f"sssvd_gpu_create({device}) failed: no sm_100 GPU available (status {st})")
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib().sssvd_gpu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, st: int):
+        if st != SSSVD_OK:
+            _raise(st, lib().sssvd_gpu_last_error(self.h).decode())
+
+    def set_batch(self, max_shifts: int):
+        lib().sssvd_gpu_set_batch(self.h, max_shifts)
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        if lib().sssvd_gpu_nccl_unique_id(buf) != SSSVD_OK:
+            raise CudaError("ncclGetUniqueId failed")
+        return buf.raw
+
+    def init_comm(self, unique_id: bytes, nranks: int, rank: int):
+        buf = ctypes.create_string_buffer(unique_id, 128)
+        self.check(lib().sssvd_gpu_init_comm(self.h, buf, nranks, rank))
+
+    def set_operator(self, a: np.ndarray):
+        a = np.asfortranarray(a, dtype=np.float64)
+        self.check(lib().sssvd_gpu_set_operator(self.h, _ptr(a), a.shape[0], a.shape[1], a.shape[0], 0))
+        self._n = min(a.shape)
+
+    def set_operator_device(self, ptr: int, rows: int, cols: int, lda: int):
+        self.check(lib().sssvd_gpu_set_operator(self.h, ctypes.c_void_p(ptr), rows, cols, lda, 1))
+        self._n = min(rows, cols)
+
+    def form_gram(self, size_cap: int = 8192, copy_out: bool = True):
+        if not copy_out:
+            self.check(lib().sssvd_gpu_form_gram(self.h, size_cap, None))
+            return None
+        g = np.empty((self._n, self._n), order="F")
+        self.check(lib().sssvd_gpu_form_gram(self.h, size_cap, _ptr(g)))
+        return g
+
+    def run_solve(self, config: RunConfig) -> "RunResult":
+        c = config._c()
+        res = ctypes.c_void_p()
+        self.check(lib().sssvd_gpu_run_solve(self.h, ctypes.byref(c), ctypes.byref(res)))
+        try:
+            return RunResult._from_handle(res)
+        finally:
+            lib().sssvd_result_free(res)
+
+
+_default_device: Optional[Device] = None
+
+
+def default_device() -> Device:
+    global _default_device
+    if _default_device is None:
+        _default_device = Device(int(os.environ.get("LOCAL_RANK", "0")))
+    return _default_device
+
+
+# ----------------------------------------------------------------------------- problem / Gram
+class ProblemMatrix:
+    """problem.hpp:14-77 (dense). Auto-transpose and the NaN check also run in the library."""
+
+    def __init__(self, a: np.ndarray, transposed: bool):
+        self._a = a
+        self._transposed = transposed
+
+    @staticmethod
+    def from_dense(a) -> "ProblemMatrix":
+        a = np.asarray(a, dtype=np.float64)
+        if not np.all(np.isfinite(a)):
+            raise ValueError("ProblemMatrix: NaN/Inf entry")
+        tr = a.shape[0] < a.shape[1]
+        return ProblemMatrix(np.asfortranarray(a.T if tr else a), tr)
+
+    def rows(self): return self._a.shape[0]
+    def cols(self): return self._a.shape[1]
+    def transposed(self): return self._transposed
+    def dense(self): return self._a
+
+
+def form_gram(a: ProblemMatrix, size_cap: int = 8192, device: Optional[Device] = None) -> np.ndarray:
+    """problem.hpp:81-95 on the GPU (DMMA Gram kernel); length_error above the cap."""
+    dev = device or default_device()
+    if a.cols() > size_cap:
+        raise LengthError("form_gram: column count exceeds the dense Gram cap")
+    dev.set_operator(a.dense())
+    return dev.form_gram(size_cap)
+
+
+# ----------------------------------------------------------------------------- shifted solves
+class ShiftedFactorization:
+    """shifted_solver.hpp:20-40. The factorisation and the solve both run on the GPU; because
+    the library fuses them (the right-hand side rides through the LU as extra columns), the
+    factor step validates the shift eagerly and solve() re-runs the fused kernel chain."""
+
+    def __init__(self, gram: np.ndarray, shift: complex, device: Optional[Device] = None):
+        gram = np.asfortranarray(gram, dtype=np.float64)
+        if gram.shape[0] != gram.shape[1]:
+            raise ValueError("ShiftedFactorization: Gram matrix must be square")
+        self._g, self._shift, self._n = gram, complex(shift), gram.shape[0]
+        self._dev = device or default_device()
+        # eager pivot-floor check like the reference constructor (shifted_solver.hpp:27-30)
+        self.solve(np.zeros((self._n, 1), dtype=np.complex128))
+
+    def shift(self): return self._shift
+    def size(self): return self._n
+
+    def solve(self, rhs) -> np.ndarray:
+        rhs = np.asarray(rhs)
+        if rhs.ndim == 1:
+            rhs = rhs[:, None]
+        if rhs.shape[0] != self._n:
+            raise ValueError("ShiftedFactorization: right-hand side dimension mismatch")
+        r = np.asfortranarray(rhs, dtype=np.complex128)
+        x = np.empty_like(r, order="F")
+        self._dev.check(lib().sssvd_gpu_shifted_solve(
+            self._dev.h, _ptr(self._g), self._n, self._shift.real, self._shift.imag,
+            _ptr(r), r.shape[0], r.shape[1], _ptr(x)))
+        return x
+
+    def solve_real(self, rhs):
+        return self.solve(np.asarray(rhs, dtype=np.complex128))
+
+
+def factor_shift(gram, shift, device=None):
+    return ShiftedFactorization(gram, shift, device)
+
+
+def solve_block(fact: ShiftedFactorization, rhs):
+    return fact.solve(rhs)
+
+
+class DenseShiftedSolver:
+    """shifted_solver.hpp:54-75."""
+
+    def __init__(self, gram: np.ndarray):
+        self._g = np.asfortranarray(gram, dtype=np.float64)
+
+    def gram(self): return self._g
+    def size(self): return self._g.shape[0]
+    def factor(self, shift): return ShiftedFactorization(self._g, shift)
+    def factor_bytes(self): return self._g.shape[0] ** 2 * 16
+
+
+@dataclass
+class MomentBlocks:
+    """moments.hpp:51-71."""
+    blocks: List[np.ndarray]
+
+    def degree(self): return len(self.blocks) - 1
+    def stacked(self): return np.hstack(self.blocks[:self.degree()])
+    def stacked_plus(self): return np.hstack(self.blocks[1:self.degree() + 1])
+
+
+class MomentAccumulator:
+    """moments.hpp:101-169 on the GPU: the operator's Gram must be resident (form_gram or
+    set_operator + form_gram on the same device)."""
+
+    def __init__(self, rule: ContourRule, device: Optional[Device] = None):
+        self._rule = rule
+        self._dev = device or default_device()
+        h = rule.count() // 2
+        self._h = h
+        self._shifts = np.array([rule.shift(j) for j in range(h)], dtype=np.complex128)
+        self._w = np.ascontiguousarray(rule.weights()[:h])
+        self._t = np.ascontiguousarray(rule.nodes()[:h])
+
+    def rule(self): return self._rule
+
+    def _run(self, s0, ell, degree):
+        s0 = np.asfortranarray(s0, dtype=np.float64)
+        n, L = s0.shape
+        out = np.empty((degree + 1) * n * L)
+        self._dev.check(lib().sssvd_gpu_moments(self._dev.h, self._h, _ptr(self._shifts), _ptr(self._w),
+                                                _ptr(self._t), _ptr(s0), L, ell, degree, _ptr(out)))
+        return [out[k * n * L:(k + 1) * n * L].reshape((L, n)).T.copy(order="F") for k in range(degree + 1)]
+
+    def refine(self, s0):
+        """moments.hpp:121-128: one pass S0 <- 2 sum_j Re(w_j X_j) (the k = 0 moment)."""
+        return self._run(s0, 1, 0)[0]
+
+    def accumulate(self, s0, degree: int) -> MomentBlocks:
+        """moments.hpp:132-147."""
+        return MomentBlocks(self._run(s0, 1, degree))
+
+
+# ----------------------------------------------------------------------------- run_solve
+@dataclass
+class StepTimings:
+    steps_1_2: float = 0.0
+    step_3: float = 0.0
+    step_4: float = 0.0
+    step_5: float = 0.0
+    postprocess: float = 0.0
+
+    def total(self):
+        return self.steps_1_2 + self.step_3 + self.step_4 + self.step_5
+
+
+@dataclass
+class TripletSet:
+    sigma: np.ndarray
+    left: np.ndarray
+    right: np.ndarray
+    q: np.ndarray
+    in_interval: np.ndarray
+
+    def count(self): return self.sigma.size
+
+
+@dataclass
+class RunResult:
+    """pipeline.hpp:74-95 (host copies of the device results)."""
+    triplets: Optional[TripletSet] = None
+    tau: Optional[np.ndarray] = None
+    spurious: Optional[np.ndarray] = None
+    estimated: Optional[np.ndarray] = None
+    exact: Optional[np.ndarray] = None
+    galerkin: Optional[np.ndarray] = None
+    basis_singular_values: Optional[np.ndarray] = None
+    blocks: Optional[MomentBlocks] = None
+    rank_deficient_qr: bool = False
+    timings: StepTimings = field(default_factory=StepTimings)
+    empty: bool = False
+    note: str = ""
+    input_transposed: bool = False
+    count_in_interval: int = 0
+    count_nonspurious_in_interval: int = 0
+    count_interior: int = 0
+    count_boundary: int = 0
+    calibration_index: Optional[int] = None
+    mu: Optional[float] = None
+    spurious_threshold: float = 0.0
+    device_times: dict = field(default_factory=dict)
+
+    def retained_rank(self):
+        return 0 if self.basis_singular_values is None else self.basis_singular_values.size
+
+    @staticmethod
+    def _from_handle(h) -> "RunResult":
+        L = lib()
+        info = _Info()
+        L.sssvd_result_info_get(h, ctypes.byref(info))
+        r = RunResult()
+        r.empty = bool(info.empty)
+        r.note = L.sssvd_result_note(h).decode()
+        r.input_transposed = bool(info.input_transposed)
+        r.rank_deficient_qr = bool(info.rank_deficient_qr)
+        r.timings = StepTimings(info.steps_1_2, info.step_3, info.step_4, info.step_5, info.postprocess)
+        r.device_times = {"gram_s": info.t_gram, "shifted_solves_s": info.t_shifted_solves,
+                          "allreduce_s": info.t_allreduce, "shifted_solve_flops": info.shifted_solve_flops}
+        n, Lb, M = info.n_internal, info.block_size, info.moment_degree
+
+        def get(field, count, dtype=np.float64):
+            out = np.empty(count, dtype=dtype)
+            if count:
+                L.sssvd_result_copy(h, field, _ptr(out))
+            return out
+
+        blk = get(10, (M + 1) * n * Lb)
+        r.blocks = MomentBlocks([blk[k * n * Lb:(k + 1) * n * Lb].reshape((Lb, n)).T.copy(order="F")
+                                 for k in range(M + 1)])
+        r.basis_singular_values = get(9, info.retained_rank)
+        t = info.count
+        r.count_in_interval = info.count_in_interval
+        r.count_nonspurious_in_interval = info.count_nonspurious_in_interval
+        r.count_interior, r.count_boundary = info.count_interior, info.count_boundary
+        r.calibration_index = None if info.calibration_index < 0 else info.calibration_index
+        r.mu = info.mu if info.calibration_index >= 0 else None
+        r.spurious_threshold = info.spurious_threshold
+        if r.empty:
+            r.triplets = TripletSet(np.empty(0), np.empty((info.rows, 0)), np.empty((info.cols, 0)),
+                                    np.empty((0, 0)), np.empty(0, dtype=bool))
+            return r
+        sigma = get(0, t)
+        left = get(7, info.rows * t).reshape((t, info.rows)).T
+        right = get(8, info.cols * t).reshape((t, info.cols)).T
+        q = get(11, info.retained_rank * t).reshape((t, info.retained_rank)).T
+        in_int = get(5, t, np.int32).astype(bool)
+        r.triplets = TripletSet(sigma, left, right, q, in_int)
+        r.tau = get(1, t)
+        r.spurious = get(6, t, np.int32).astype(bool)
+        r.estimated = get(2, t)
+        r.exact = get(3, t)
+        r.galerkin = get(4, t)
+        return r
+
+
+def run_solve(a, config: RunConfig, device: Optional[Device] = None) -> RunResult:
+    """pipeline.hpp:112-231 on the GPU. `a` is a ProblemMatrix or a dense array (user
+    orientation); the library auto-transposes wide inputs like ProblemMatrix::from_dense."""
+    dev = device or default_device()
+    if isinstance(a, ProblemMatrix):
+        arr = a.dense().T if a.transposed() else a.dense()
+    else:
+        arr = np.asarray(a, dtype=np.float64)
+    dev.set_operator(arr)
+    return dev.run_solve(config)

@@ -1,0 +1,20 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (runs the sm_100a library)")
+    config.addinivalue_line("markers", "slow: full-size configuration checks")
+
+
+@pytest.fixture(scope="session")
+def dev():
+    from paper_2109_13655_b200 import sssvd
+    d = sssvd.default_device()
+    yield d

@@ -1,0 +1,147 @@
+"""GPU parity for the moment accumulation (MomentAccumulator, moments.hpp:101-169), re-expressing
+proj/tests/test_moments.cpp against the sm_100a path and comparing with the CPU oracle."""
+import numpy as np
+import pytest
+
+from oracle import sssvd_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def constructed(m, n, sigma, su, sv):
+    u, _ = np.linalg.qr(orc.random_matrix(m, n, su))
+    v, _ = np.linalg.qr(orc.random_matrix(n, n, sv))
+    return (u * sigma[None, :]) @ v.T
+
+
+def gpu_blocks(dev, a, rule, s0, degree, ell=1):
+    from paper_2109_13655_b200 import sssvd
+    dev.set_operator(a)
+    dev.form_gram(1 << 30, copy_out=False)
+    acc = sssvd.MomentAccumulator(rule, dev)
+    if ell == 1:
+        return acc.accumulate(s0, degree).blocks
+    return acc._run(s0, ell, degree)
+
+
+def rules(a, b, N, aspect, exp=False):
+    from paper_2109_13655_b200 import sssvd
+    tf = sssvd.SpectralTransform.exponential() if exp else sssvd.SpectralTransform.identity()
+    return (sssvd.ContourRule(a, b, N, aspect, tf),
+            orc.ContourRule(a, b, N, aspect, orc.SpectralTransform("exp" if exp else "identity")))
+
+
+def test_moment_identity_identity_transform(dev):
+    n = 40
+    a = constructed(80, n, 0.2 + 0.04 * np.arange(n), 51, 52)
+    g = a.T @ a
+    rg, _ = rules(0.8, 1.2, 32, 0.1)
+    s0 = orc.random_start(n, 10, 7)
+    blocks = gpu_blocks(dev, a, rg, s0, 4)
+    assert len(blocks) == 5
+    power = blocks[0]
+    for k in range(1, 5):                                             # test_moments.cpp:116-139
+        power = g @ power
+        assert np.linalg.norm(blocks[k] - power) / np.linalg.norm(power) <= 1e-8
+    splus, stacked = np.hstack(blocks[1:]), np.hstack(blocks[:4])
+    assert np.linalg.norm(splus - g @ stacked) / np.linalg.norm(g @ stacked) <= 1e-8
+
+
+@pytest.mark.parametrize("m,n,L,M,N,exp", [(80, 40, 10, 4, 32, False), (300, 200, 8, 3, 16, True),
+                                            (2000, 1000, 16, 8, 32, True), (1500, 1100, 20, 4, 32, False)])
+def test_moments_match_oracle(dev, m, n, L, M, N, exp):
+    a = constructed(m, n, np.linspace(0.01, 1.0, n), 11, 12)
+    lo, hi = (0.45, 0.55)
+    rg, ro = rules(lo, hi, N, 0.1, exp)
+    s0 = orc.random_start(n, L, 42)
+    blocks = gpu_blocks(dev, a, rg, s0, M)
+    ref = orc.MomentAccumulator(orc.form_gram(orc.ProblemMatrix(a), 1 << 30), ro).accumulate(s0, M).blocks
+    for k in range(M + 1):
+        err = np.linalg.norm(blocks[k] - ref[k]) / np.linalg.norm(ref[k])
+        assert err <= 1e-10, (k, err)
+
+
+def test_batching_does_not_change_result(dev):
+    """test_moments.cpp:205-215 (worker count) -> shifts-in-flight count: bitwise identical."""
+    a = orc.random_matrix(300, 160, 91)
+    rg, _ = rules(0.5, 2.0, 32, 0.1)
+    s0 = orc.random_start(160, 5, 11)
+    dev.set_batch(16)
+    b16 = gpu_blocks(dev, a, rg, s0, 3)
+    dev.set_batch(1)
+    b1 = gpu_blocks(dev, a, rg, s0, 3)
+    dev.set_batch(5)
+    b5 = gpu_blocks(dev, a, rg, s0, 3)
+    dev.set_batch(0)
+    for k in range(4):
+        assert np.array_equal(b16[k], b1[k]) and np.array_equal(b16[k], b5[k])
+
+
+def test_refinement_fixed_map_on_invariant_block(dev):
+    from paper_2109_13655_b200 import sssvd
+    n = 40
+    sigma = 0.3 + 0.05 * np.arange(n)
+    u, _ = np.linalg.qr(orc.random_matrix(60, n, 21))
+    v, _ = np.linalg.qr(orc.random_matrix(n, n, 22))
+    a = (u * sigma) @ v.T
+    rg, _ = rules(0.8, 1.2, 32, 0.1)
+    inside = [i for i in range(n) if 0.8 <= sigma[i] <= 1.2]
+    vsel = v[:, inside]
+    dev.set_operator(a)
+    dev.form_gram(1 << 30, copy_out=False)
+    refined = sssvd.MomentAccumulator(rg, dev).refine(vsel)
+    qx, _ = np.linalg.qr(refined)
+    qy, _ = np.linalg.qr(vsel)
+    assert np.linalg.svd(qx - qy @ (qy.T @ qx), compute_uv=False)[0] <= 1e-8   # test_moments.cpp:61-82
+
+
+def test_refinement_annihilates_far_spectrum(dev):
+    from paper_2109_13655_b200 import sssvd
+    n = 30
+    a = constructed(50, n, 5.0 + 0.03 * np.arange(n), 41, 42)
+    rg, _ = rules(0.8, 1.2, 32, 0.1)
+    s0 = orc.random_start(n, 8, 6)
+    dev.set_operator(a)
+    dev.form_gram(1 << 30, copy_out=False)
+    refined = sssvd.MomentAccumulator(rg, dev).refine(s0)
+    assert np.linalg.norm(refined) / np.linalg.norm(s0) <= 1e-6      # test_moments.cpp:102-114
+
+
+def test_exp_transform_approximates_log_g(dev):
+    n = 40
+    a = constructed(80, n, 10.0 ** (-6.0 + 6.0 * np.arange(n) / (n - 1)), 61, 62)
+    g = a.T @ a
+    g = (g + g.T) / 2
+    rg, _ = rules(1e-4, 1e-1, 32, 0.1, exp=True)
+    s0 = orc.random_start(n, 10, 8)
+    blocks = gpu_blocks(dev, a, rg, s0, 2)
+    lam, vec = np.linalg.eigh(g)
+    logg = (vec * np.log(np.maximum(lam, 1e-300))) @ vec.T
+    expected = logg @ blocks[0]
+    assert np.linalg.norm(blocks[1] - expected) / np.linalg.norm(expected) <= 1e-4   # :141-163
+
+
+def test_rank_one_filter_gain(dev):
+    m, n = 50, 20
+    u = orc.random_matrix(m, 1, 101)[:, 0]
+    u /= np.linalg.norm(u)
+    v = orc.random_matrix(n, 1, 102)[:, 0]
+    v /= np.linalg.norm(v)
+    s = 1.03
+    a = s * np.outer(u, v)
+    rg, ro = rules(0.8, 1.2, 32, 0.1)
+    vin = orc.random_start(n, 6, 12)
+    blocks = gpu_blocks(dev, a, rg, vin, 1)
+    gain = np.linalg.norm(blocks[0]) / np.linalg.norm(v @ vin)
+    assert abs(gain - abs(orc.eval_filter(ro, s))) <= 1e-10 * abs(orc.eval_filter(ro, s))  # :217-231
+
+
+def test_ell2_matches_oracle(dev):
+    a = constructed(120, 60, np.linspace(0.05, 1.5, 60), 7, 8)
+    rg, ro = rules(0.6, 0.9, 16, 0.1)
+    s0 = orc.random_start(60, 6, 42)
+    blocks = gpu_blocks(dev, a, rg, s0, 3, ell=2)
+    acc = orc.MomentAccumulator(orc.form_gram(orc.ProblemMatrix(a)), ro)
+    ref = acc.accumulate(acc.refine(s0), 3).blocks
+    for k in range(4):
+        assert np.linalg.norm(blocks[k] - ref[k]) / np.linalg.norm(ref[k]) <= 1e-10
