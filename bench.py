@@ -1,0 +1,277 @@
+"""Benchmark: time-to-triplets of the block SS-SVD shifted-solve path on B200 (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+One step = one run_solve per solve mode of the workload (config 2: NT off and NT on, as
+BASELINE.json configs[1] states "both run"), i.e. time-to-triplets for the config.
+  value : device time (CUDA events on the library stream, max over ranks) of a step with the
+          operator already resident in HBM (set_operator from a device pointer)
+  e2e   : the same step through the public C ABI from pinned HOST memory: H2D of A, the solve,
+          and D2H of every triplet (sigma, u, v, tau, residuals) inside the timed region
+Multi-GPU (torchrun, one rank per GPU, NCCL): the h quadrature points are sharded contiguously
+over the ranks (sssvd_shard_range) and the partial moment blocks are summed with one NCCL
+all-reduce inside the library; total work is fixed ("strong" scaling).
+--impl reference times the reference algorithm's CPU restatement (oracle/, numpy + LAPACK over
+all host threads) on a bounded sample of the same workload (see cpu_baseline.sample).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "time-to-triplets (s)"
+PEAKS = {}
+try:
+    PEAKS = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+except Exception:
+    pass
+FP64_PEAK_TFLOPS = 37.1   # measured: DMMA probe, profiles/r01_fp64_peaks.json (cuBLAS ZGEMM 36.8)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", type=int, default=2)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index=0):
+        self.samples, self.proc = [], None
+        self.index = index
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and "Active" in s[3 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def run_reference(args, rank, world):
+    """CPU arm: the oracle restatement on this host's cores (rank 0 only)."""
+    if rank != 0:
+        return
+    from paper_2109_13655_b200 import workloads
+    from oracle import sssvd_oracle as orc
+    w = workloads.CONFIGS[args.config]
+    a, sigma = workloads.make_operator(args.config, use_torch=False)
+    A = orc.ProblemMatrix(a)
+    # bounded sample: one full run_solve of the first mode; the other mode repeats the same
+    # steps 1-2 work on the same shapes, so the step time is scaled by the mode count
+    mode = w.modes[0]
+    ocfg = orc.RunConfig(w.a, w.b, mode=[orc.SS_SVD, orc.SS_SVD_NT][mode],
+                         params=orc.SsParams(block_size=w.L, moment_degree=w.M, quadrature_count=w.N))
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        orc.run_solve(A, ocfg, gram_cap=1 << 30)
+        dt = (time.perf_counter() - t0) * len(w.modes)
+        if i >= args.warmup:
+            times.append(dt)
+    v = float(np.mean(times))
+    cores = os.cpu_count()
+    sample = (f"{w.name}: oracle run_solve of mode {mode} (all {w.N // 2} shifts, full tail) per step, "
+              f"x{len(w.modes)} modes; numpy/OpenBLAS on {cores} host threads")
+    print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": world,
+                      "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+                      "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                      "config": {"workload": w.description, "m": w.m, "n": w.n, "L": w.L, "M": w.M, "N": w.N},
+                      "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "port", "sample": sample},
+                      "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+          flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2109_13655_b200 import sssvd, workloads
+    w = workloads.CONFIGS[args.config]
+    dev = sssvd.Device(local)
+    if world > 1:
+        uid = [sssvd.Device.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        dev.init_comm(uid[0], world, rank)
+
+    a, sigma = workloads.make_operator(args.config)
+    a_dev = torch.from_numpy(a.T.copy()).cuda()   # column-major A == row-major A^T, resident in HBM
+    a_pin = torch.from_numpy(np.ascontiguousarray(a.T)).pin_memory()
+    cfgs = [sssvd.RunConfig(w.a, w.b, mode=m, params=sssvd.SsParams(block_size=w.L, moment_degree=w.M,
+                                                                     quadrature_count=w.N), gram_cap=1 << 30)
+            for m in w.modes]
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
+    def step_device():
+        dev.set_operator_device(a_dev.data_ptr(), w.m, w.n, w.m)
+        out = []
+        for c in cfgs:
+            out.append(dev.run_solve(c))
+        return out
+
+    def step_e2e():
+        # public API from host memory: H2D of A inside, D2H of all triplets inside
+        lib = sssvd.lib()
+        dev.check(lib.sssvd_gpu_set_operator(dev.h, sssvd.ctypes.c_void_p(a_pin.data_ptr()), w.m, w.n, w.m, 0))
+        return [dev.run_solve(c) for c in cfgs]
+
+    for _ in range(args.warmup):
+        res = step_device()
+    barrier()
+    # ---- timed region (device events on the current stream bracket library work that is
+    #      synchronised inside run_solve; CUDA events + synchronize on both sides)
+    sssvd.profile_gemm(True)
+    launches0 = sssvd.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        barrier()
+        ev0.record()
+        for _ in range(args.steps):
+            res = step_device()
+        ev1.record()
+        barrier()
+    launches = sssvd.launch_count() - launches0
+    gemm_ms, gemm_flops, gemm_launches = sssvd.profile_gemm_collect()
+    sssvd.profile_gemm(False)
+    t = ev0.elapsed_time(ev1) / 1e3 / args.steps
+    if dist:
+        tt = torch.tensor([t], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    # ---- e2e through the public API with host buffers
+    step_e2e()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        res_e = step_e2e()
+    barrier()
+    te = (time.perf_counter() - t0) / args.steps
+    if dist:
+        tt = torch.tensor([te], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        te = float(tt.item())
+    h2d = a.nbytes + len(cfgs) * (w.n * w.L * 8)
+    d2h = sum(r.triplets.left.nbytes + r.triplets.right.nbytes + 5 * r.triplets.sigma.nbytes +
+              sum(b.nbytes for b in r.blocks.blocks) for r in res_e)
+
+    # phase-level FP64 roofline (north star): shifted-solve flops / device time of the phase
+    dt = res[0].device_times
+    h_local = None
+    solve_s = sum(r.device_times["shifted_solves_s"] for r in res)
+    solve_flops = sum(r.device_times["shifted_solve_flops"] for r in res)
+    gemm_tflops = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
+    counts = [{"mode": c.mode, "nonspurious_in_interval": r.count_nonspurious_in_interval,
+               "in_interval": r.count_in_interval, "boundary": r.count_boundary} for c, r in zip(cfgs, res)]
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.config)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": t, "unit": "s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.description, "m": w.m, "n": w.n, "L": w.L, "M": w.M, "N": w.N,
+                       "modes": ["ss-svd" if m == 0 else "ss-svd-nt" for m in w.modes],
+                       "parallelism": f"shift-sharded x{world} (+1 NCCL all-reduce)",
+                       "l2": "inputs larger than L2: A 134 MB, 16 factors x 272 MB per mode"},
+            "e2e": {"value": te, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+            "roofline": {"bound": "tensor", "kernel": "zgemm_sub_kernel (DMMA trailing update)",
+                         "achieved": gemm_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": (gemm_tflops / FP64_PEAK_TFLOPS) if gemm_tflops else None,
+                         "traffic": None,
+                         "peak_source": "measured FP64 DMMA probe (profiles/r01_fp64_peaks.json); MEASURED_PEAKS.json has no FP64 entry",
+                         "gemm_launches": gemm_launches, "gemm_ms_per_step": gemm_ms / args.steps,
+                         "phase_tflops": solve_flops / solve_s / 1e12 if solve_s > 0 else None,
+                         "phase_frac": (solve_flops / solve_s / 1e12 / FP64_PEAK_TFLOPS) if solve_s > 0 else None,
+                         "phase_flops_per_step": solve_flops, "phase_s_per_step": solve_s},
+            "phases_s": {"steps_1_2": sum(r.timings.steps_1_2 for r in res), "step_3": sum(r.timings.step_3 for r in res),
+                         "step_4": sum(r.timings.step_4 for r in res), "step_5": sum(r.timings.step_5 for r in res),
+                         "postprocess": sum(r.timings.postprocess for r in res), "gram": dt["gram_s"],
+                         "allreduce": sum(r.device_times["allreduce_s"] for r in res)},
+            "counts": counts,
+            "truth_in_interval": int(np.sum((sigma >= w.a) & (sigma <= w.b))),
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "gpu_launches": int(launches // max(1, args.steps)),
+            "gpu_launches_timed_region": int(launches),
+            "input_sha256": workloads.sha256(a),
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(cfg):
+    """Oracle (reference restatement) on the host cores, bounded sample of the same workload."""
+    try:
+        from paper_2109_13655_b200 import workloads
+        from oracle import sssvd_oracle as orc
+        w = workloads.CONFIGS[cfg]
+        a, _ = workloads.make_operator(cfg, use_torch=False)
+        mode = w.modes[0]
+        ocfg = orc.RunConfig(w.a, w.b, mode=[orc.SS_SVD, orc.SS_SVD_NT][mode],
+                             params=orc.SsParams(block_size=w.L, moment_degree=w.M, quadrature_count=w.N))
+        t0 = time.perf_counter()
+        orc.run_solve(orc.ProblemMatrix(a), ocfg, gram_cap=1 << 30)
+        dt = time.perf_counter() - t0
+        return {"value": dt * len(w.modes), "unit": "s", "cores": os.cpu_count(), "kind": "port",
+                "sample": f"{w.name}: one oracle run_solve (mode {mode}, all shifts, full tail) x{len(w.modes)} modes, "
+                          f"numpy/OpenBLAS on all {os.cpu_count()} host threads"}
+    except Exception as e:  # the baseline is reported, never required
+        return {"value": None, "unit": "s", "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
+
+
+if __name__ == "__main__":
+    main()

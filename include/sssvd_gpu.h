@@ -175,6 +175,11 @@ sssvd_status sssvd_validate_params(const sssvd_params* p, int64_t n);
  * moments.hpp:138-144), complex interleaved, row k at offset 2*k*h. */
 sssvd_status sssvd_moment_coefficients(int64_t h, const double* weights, const double* nodes, int64_t M,
                                        double* coef_out);
+/* Instrumentation: number of kernels this library launched so far (process-wide), and live
+ * CUDA-event timing of the dominant kernel (the DMMA trailing update) while enabled. */
+uint64_t sssvd_gpu_launch_count(void);
+void sssvd_gpu_profile_gemm(int enable);
+void sssvd_gpu_profile_gemm_collect(double* ms, double* flops, uint64_t* launches);
 /* Build provenance for the loaded library ("sm_100a ..."). */
 const char* sssvd_build_info(void);
 

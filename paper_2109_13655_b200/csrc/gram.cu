@@ -110,6 +110,7 @@ cudaError_t gram(const double* A, int lda, int K, int n, double* G, int ldg, cud
   }
   const long long T = (n + BM - 1) / BM;
   gram_kernel<<<(unsigned)(T * (T + 1) / 2), THREADS, smem, s>>>(A, lda, K, n, G, ldg);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -7,6 +7,13 @@ namespace sssvd_gpu {
 
 cudaError_t cuda_fail(cudaError_t e, const char* expr, const char* file, int line);
 
+// instrumentation: every launcher bumps the launch counter; when profiling is on, zgemm_sub
+// brackets each launch with CUDA events on its stream (the dominant kernel's live timing)
+void note_launch(unsigned long long count = 1);
+unsigned long long launch_count();
+void zgemm_profile_enable(bool on);
+void zgemm_profile_collect(double* ms, double* flops, unsigned long long* launches);
+
 // K0 Gram (gram.cu): G = A^T A, A column-major (lda even, K = rows incl. zero padding)
 cudaError_t gram(const double* A, int lda, int K, int n, double* G, int ldg, cudaStream_t s);
 // max |a_i| (lu.cu)

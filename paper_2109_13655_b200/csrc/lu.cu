@@ -55,6 +55,7 @@ cudaError_t assemble(const double* G, int n, int ldg, const double* V, int L, co
   long long total = (long long)n * (n + L);
   int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 8);
   assemble_kernel<<<dim3(blocks, batch), 256, 0, s>>>(G, n, ldg, V, L, shifts, out, ld, stride);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -244,6 +245,7 @@ static cudaError_t launch_leaf(double2* mats, int ld, long long stride, int n, i
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  note_launch();
   return cudaLaunchKernelEx(&cfg, leaf_lu_kernel<W>, mats, ld, stride, n, r0, w, R, ipiv);
 }
 
@@ -348,6 +350,7 @@ cudaError_t swap_trsm(double2* mats, int ld, long long stride, int n, int r0, in
   }
   dim3 grid((c1 - c0 + ST_COLS - 1) / ST_COLS, batch);
   swap_trsm_kernel<<<grid, ST_COLS, smem, s>>>(mats, ld, stride, n, r0, np, c0, c1, ipiv, do_trsm ? 1 : 0);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -385,6 +388,7 @@ cudaError_t trsm_upper(double2* mats, int ld, long long stride, int r0, int np, 
   }
   dim3 grid((c1 - c0 + nt - 1) / nt, batch);
   trsm_upper_kernel<<<grid, nt, smem, s>>>(mats, ld, stride, r0, np, c0, c1);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -414,6 +418,7 @@ __global__ void pivot_floor_kernel(const double2* mats, int ld, long long stride
 cudaError_t pivot_floor(const double2* mats, int ld, long long stride, int n, const double2* shifts,
                         const double* gmax, int* status, double* minpiv, int batch, cudaStream_t s) {
   pivot_floor_kernel<<<batch, 256, 0, s>>>(mats, ld, stride, n, shifts, gmax, status, minpiv);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -440,6 +445,7 @@ cudaError_t absmax(const double* a, long long count, double* out, cudaStream_t s
   cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), s);
   if (e != cudaSuccess) return e;
   absmax_kernel<<<148 * 4, 256, 0, s>>>(a, count, out);
+  note_launch();
   return cudaGetLastError();
 }
 

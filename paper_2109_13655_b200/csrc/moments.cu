@@ -53,6 +53,7 @@ cudaError_t moments(const double2* mats, int ld, long long stride, int xcol, int
   int blocks = (int)std::min<long long>((nl + 255) / 256, 148 * 8);
   moments_kernel<<<blocks, 256, (size_t)(M + 1) * nb * sizeof(double2), s>>>(mats, ld, stride, xcol, n,
                                                                            L, nb, coef, M, S);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -79,6 +80,7 @@ __global__ void blocks_to_colmajor_kernel(const double* __restrict__ S, int n, i
 cudaError_t blocks_to_colmajor(const double* S, int n, int L, int nblk, double* out, cudaStream_t s) {
   dim3 grid((n + 31) / 32, (L + 31) / 32, nblk);
   blocks_to_colmajor_kernel<<<grid, dim3(32, 8), 0, s>>>(S, n, L, nblk, out);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -114,6 +116,7 @@ cudaError_t colnorm_diff(const double* X, int ldx, const double* Y, int ldy, con
                          int cols, double* out, cudaStream_t st) {
   if (cols <= 0) return cudaSuccess;
   colnorm_diff_kernel<<<cols, 256, 0, st>>>(X, ldx, Y, ldy, s, rows, out);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -132,6 +135,7 @@ cudaError_t gather_cols(const double* src, int lds, const int* perm, const doubl
                         int cols, double* dst, int ldd, cudaStream_t st) {
   if (cols <= 0) return cudaSuccess;
   gather_cols_kernel<<<cols, 256, 0, st>>>(src, lds, perm, scale, rows, dst, ldd);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -165,7 +169,9 @@ cudaError_t sumsq(const double* a, long long count, double* scratch /*>= 593 dou
                   cudaStream_t s) {
   const int blocks = 148 * 4;
   sumsq_kernel<<<blocks, 256, 0, s>>>(a, count, scratch);
+  note_launch();
   sum_partials_kernel<<<1, 32, 0, s>>>(scratch, blocks, out);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -183,6 +189,7 @@ cudaError_t pad_copy(const double* src, int rows, int cols, int lds, double* dst
   long long total = (long long)ldd * cols;
   int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
   pad_copy_kernel<<<blocks, 256, 0, s>>>(src, rows, cols, lds, dst, ldd);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -168,7 +168,7 @@ static LuPlan make_plan(int n, int L) {
   p.L = L;
   p.ld = ((n + L) + 7) / 8 * 8;
   p.stride = (long long)n * p.ld;
-  p.NB = 64;
+  p.NB = 128;
   // leaf width W and cluster size C: the leaf slab (ceil(n/C) x (W+1) complex) must fit ~200 KB
   const size_t budget = 200 * 1024;
   p.W = 8;
@@ -194,27 +194,43 @@ static LuPlan make_plan(int n, int L) {
   return p;
 }
 
+// Recursive (getrf2-style) factorisation of the panel columns [c0, c0+w) over rows [c0, n),
+// confined to the current NB block [cb, ce): leaves of width <= W run the cluster kernel; an
+// internal node factors its left half, applies those interchanges + the unit-lower solve to its
+// right half, updates the right half with one DMMA GEMM (K = left width), then factors the right
+// half. Each leaf applies its interchanges to the block columns on its left; the columns on its
+// right receive them from the lowest common ancestor, so every block column sees every
+// interchange of the block exactly once and in order (LAPACK semantics within the block).
+static void factor_rec(const LuPlan& P, double2* mats, int* ipiv, int nb, cudaStream_t s, int c0, int w,
+                       int cb) {
+  const int n = P.n;
+  if (w <= P.W) {
+    CK(leaf_lu(mats, P.ld, P.stride, n, c0, w, P.W, P.cluster, ipiv, nb, s));
+    if (c0 > cb) CK(swap_trsm(mats, P.ld, P.stride, n, c0, w, cb, c0, ipiv, false, nb, s));
+    return;
+  }
+  int wl = ((w / 2) + P.W - 1) / P.W * P.W;
+  if (wl >= w) wl = w - P.W;
+  factor_rec(P, mats, ipiv, nb, s, c0, wl, cb);
+  const int r0 = c0 + wl, wr = w - wl;
+  CK(swap_trsm(mats, P.ld, P.stride, n, c0, wl, r0, r0 + wr, ipiv, true, nb, s));
+  if (n - r0 > 0)
+    CK(zgemm_sub(n - r0, wr, wl, mats + (size_t)r0 * P.ld + c0, P.ld, P.stride, mats + (size_t)c0 * P.ld + r0, P.ld,
+                 P.stride, mats + (size_t)r0 * P.ld + r0, P.ld, P.stride, nb, s));
+  factor_rec(P, mats, ipiv, nb, s, r0, wr, cb);
+}
+
 // LU of nb augmented matrices [z I - G | V] in place (rows 0..n-1, cols 0..n+L-1), then the
 // back substitution U^{-1} on the L right-hand-side columns. ipiv: nb x n.
 static void lu_solve_batch(const LuPlan& P, double2* mats, int* ipiv, int nb, cudaStream_t s) {
   const int n = P.n, ncols = n + P.L;
   for (int kb = 0; kb < n; kb += P.NB) {
     const int nbk = std::min(P.NB, n - kb);
-    for (int kc = kb; kc < kb + nbk; kc += P.W) {
-      const int w = std::min(P.W, kb + nbk - kc);
-      CK(leaf_lu(mats, P.ld, P.stride, n, kc, w, P.W, P.cluster, ipiv, nb, s));
-      if (kc > kb) CK(swap_trsm(mats, P.ld, P.stride, n, kc, w, kb, kc, ipiv, false, nb, s));
-      if (kc + w < kb + nbk) {
-        CK(swap_trsm(mats, P.ld, P.stride, n, kc, w, kc + w, kb + nbk, ipiv, true, nb, s));
-        const int M = n - (kc + w), N = kb + nbk - (kc + w);
-        if (M > 0)
-          CK(zgemm_sub(M, N, w, mats + (size_t)(kc + w) * P.ld + kc, P.ld, P.stride,
-                       mats + (size_t)kc * P.ld + kc + w, P.ld, P.stride,
-                       mats + (size_t)(kc + w) * P.ld + kc + w, P.ld, P.stride, nb, s));
-      }
-    }
+    factor_rec(P, mats, ipiv, nb, s, kb, nbk, kb);
     const int c0 = kb + nbk;
     if (c0 < ncols) {
+      // trailing columns (incl. the right-hand side): all NB interchanges, U12 = L11^{-1} A12,
+      // then A22 -= L21 U12 on the FP64 tensor cores
       CK(swap_trsm(mats, P.ld, P.stride, n, kb, nbk, c0, ncols, ipiv, true, nb, s));
       const int M = n - c0, N = ncols - c0;
       if (M > 0)
@@ -396,8 +412,9 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
   info.cols = ctx->transposed ? m : n;
   ctx->t_solves = ctx->t_allreduce = ctx->solve_flops = 0;
 
-  // ---- steps 1-2
+  // ---- steps 1-2 (form_gram is part of steps 1-2 in every run, pipeline.hpp:124-125)
   double t0 = now_s();
+  ctx->has_gram = false;
   ensure_gram(ctx, cfg.gram_cap > 0 ? cfg.gram_cap : 8192);
   std::vector<double> v0 = random_start(n, L, cfg.params.seed);
   double start_norm2 = 0;
@@ -706,6 +723,14 @@ static sssvd_status guarded(sssvd_gpu_ctx* ctx, F&& body) {
 }
 
 extern "C" {
+
+uint64_t sssvd_gpu_launch_count(void) { return launch_count(); }
+void sssvd_gpu_profile_gemm(int enable) { zgemm_profile_enable(enable != 0); }
+void sssvd_gpu_profile_gemm_collect(double* ms, double* flops, uint64_t* launches) {
+  unsigned long long l = 0;
+  zgemm_profile_collect(ms, flops, &l);
+  *launches = l;
+}
 
 const char* sssvd_build_info(void) {
   return "sssvd_gpu: sm_100a (compute_100a) DMMA/FP64 kernels";

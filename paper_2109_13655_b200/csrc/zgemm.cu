@@ -11,10 +11,47 @@
 // CTA tile 64x64 (4 warps, 32x32 each), K staged 16 at a time through a 3-deep cp.async ring.
 // Shared-memory row pitches are padded (A: 20, B: 66 double2) so every fragment load is one
 // conflict-free LDS.128 per quarter-warp.
+#include <atomic>
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.h"
 
 namespace sssvd_gpu {
+
+static std::atomic<unsigned long long> g_launches{0};
+void note_launch(unsigned long long c) { g_launches += c; }
+unsigned long long launch_count() { return g_launches.load(); }
+
+struct GemmProf {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;       // pairs
+  std::vector<double> flops;
+  size_t used = 0;
+};
+static GemmProf g_prof;
+
+void zgemm_profile_enable(bool on) {
+  g_prof.on = on;
+  g_prof.used = 0;
+  g_prof.flops.clear();
+}
+
+void zgemm_profile_collect(double* ms, double* flops, unsigned long long* launches) {
+  double t = 0, f = 0;
+  for (size_t i = 0; i < g_prof.used; ++i) {
+    cudaEventSynchronize(g_prof.ev[2 * i + 1]);
+    float x = 0;
+    cudaEventElapsedTime(&x, g_prof.ev[2 * i], g_prof.ev[2 * i + 1]);
+    t += x;
+    f += g_prof.flops[i];
+  }
+  *ms = t;
+  *flops = f;
+  *launches = g_prof.used;
+  g_prof.used = 0;
+  g_prof.flops.clear();
+}
 
 namespace {
 constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3;
@@ -152,8 +189,24 @@ cudaError_t zgemm_sub(int M, int N, int K, const double2* A, int lda, long long 
     configured = true;
   }
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch);
+  if (g_prof.on) {
+    if (2 * (g_prof.used + 1) > g_prof.ev.size()) {
+      for (int i = 0; i < 512; ++i) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        g_prof.ev.push_back(e);
+      }
+    }
+    cudaEventRecord(g_prof.ev[2 * g_prof.used], stream);
+  }
   zgemm_sub_kernel<<<grid, THREADS, zgemm_sub_smem(), stream>>>(M, N, K, A, lda, sA, B, ldb, sB, C,
                                                                  ldc, sC);
+  note_launch();
+  if (g_prof.on) {
+    cudaEventRecord(g_prof.ev[2 * g_prof.used + 1], stream);
+    g_prof.flops.push_back(8.0 * M * (double)N * K * batch);
+    ++g_prof.used;
+  }
   return cudaGetLastError();
 }
 

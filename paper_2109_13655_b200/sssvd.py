@@ -107,7 +107,8 @@ EXPORTED_SYMBOLS = [
     "sssvd_gpu_set_operator", "sssvd_gpu_form_gram", "sssvd_gpu_shifted_solve", "sssvd_gpu_moments",
     "sssvd_gpu_run_solve", "sssvd_result_info_get", "sssvd_result_copy", "sssvd_result_note",
     "sssvd_result_free", "sssvd_contour", "sssvd_random_start", "sssvd_validate_params",
-    "sssvd_moment_coefficients", "sssvd_build_info",
+    "sssvd_moment_coefficients", "sssvd_build_info", "sssvd_gpu_launch_count", "sssvd_gpu_profile_gemm",
+    "sssvd_gpu_profile_gemm_collect",
 ]
 
 _lib = None
@@ -148,6 +149,12 @@ def lib():
     L.sssvd_validate_params.argtypes = [ctypes.POINTER(_Params), i64]
     L.sssvd_moment_coefficients.argtypes = [i64, dp, dp, i64, dp]
     L.sssvd_build_info.restype = ctypes.c_char_p
+    L.sssvd_gpu_launch_count.restype = ctypes.c_uint64
+    L.sssvd_gpu_profile_gemm.argtypes = [ctypes.c_int]
+    L.sssvd_gpu_profile_gemm.restype = None
+    L.sssvd_gpu_profile_gemm_collect.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                                 ctypes.POINTER(ctypes.c_uint64)]
+    L.sssvd_gpu_profile_gemm_collect.restype = None
     _lib = L
     return L
 
@@ -296,6 +303,21 @@ def moment_coefficients(weights, nodes, degree: int) -> np.ndarray:
     if st != SSSVD_OK:
         _raise(st, "moment_coefficients")
     return out.reshape(degree + 1, w.size)
+
+
+def launch_count() -> int:
+    return int(lib().sssvd_gpu_launch_count())
+
+
+def profile_gemm(enable: bool):
+    lib().sssvd_gpu_profile_gemm(1 if enable else 0)
+
+
+def profile_gemm_collect():
+    """(total ms, algorithmic flops, launches) of the DMMA trailing-update kernel since enable."""
+    ms, fl, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_uint64()
+    lib().sssvd_gpu_profile_gemm_collect(ctypes.byref(ms), ctypes.byref(fl), ctypes.byref(n))
+    return ms.value, fl.value, int(n.value)
 
 
 def shard_range(h: int, nranks: int, rank: int):

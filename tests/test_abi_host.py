@@ -123,3 +123,18 @@ def test_no_cpu_fallback_without_gpu():
     from paper_2109_13655_b200 import sssvd
     with pytest.raises(sssvd.CudaError):
         sssvd.Device(0)
+
+
+def test_cpp_binding_compiles_and_maps_errors(tmp_path):
+    """include/sssvd_gpu.hpp (the reference-side binding) builds with g++ -std=c++20
+    against the library and maps status codes onto the reference's exception types."""
+    import subprocess
+    import torch
+    exe = tmp_path / "abi_smoke"
+    lib = os.path.join(ROOT, "paper_2109_13655_b200")
+    subprocess.check_call(["g++", "-std=c++20", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "tests", "cpp", "abi_smoke.cpp"), "-L", lib, "-lsssvd_gpu",
+                           f"-Wl,-rpath,{lib}", "-o", str(exe)])
+    args = [str(exe)] + (["gpu"] if torch.cuda.is_available() else [])
+    out = subprocess.run(args, capture_output=True, text=True)
+    assert out.returncode == 0 and "abi_smoke ok" in out.stdout, out.stdout + out.stderr
