@@ -38,6 +38,19 @@ cudaError_t pivot_floor(const double2* mats, int ld, long long stride, int n, co
 cudaError_t zgemm_sub(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B,
                       int ldb, long long sB, double2* C, int ldc, long long sC, int batch,
                       cudaStream_t stream);
+// C = A B[brow[k], :] (row-gathered B), row-major complex, batched (zgemm.cu)
+cudaError_t zgemm_set_gather(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B,
+                             int ldb, long long sB, const int* brow, int sR, double2* C, int ldc, long long sC,
+                             int batch, cudaStream_t stream);
+// interchange map, L11^{-1}, scatter+copy, warp back substitution (lu.cu)
+cudaError_t build_moves(const int* ipiv, int n, int r0, int np, int* src, int* disp, int stride, int batch,
+                        cudaStream_t s);
+cudaError_t trinv_lower(const double2* mats, int ld, long long stride, int r0, int np, double2* linv,
+                        long long lstride, int batch, cudaStream_t s);
+cudaError_t scatter_copy(double2* mats, int ld, long long stride, int r0, int np, int c0, int c1, const int* disp,
+                         int dstride, const double2* T, int ldt, long long tstride, int batch, cudaStream_t s);
+cudaError_t trsm_upper_warp(double2* mats, int ld, long long stride, int r0, int np, int c0, int c1, int batch,
+                            cudaStream_t s);
 // K7 (moments.cu)
 cudaError_t moments(const double2* mats, int ld, long long stride, int xcol, int n, int L, int nb,
                     const double2* coef, int M, double* S, cudaStream_t s);

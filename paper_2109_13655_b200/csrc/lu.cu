@@ -450,3 +450,218 @@ cudaError_t absmax(const double* a, long long count, double* out, cudaStream_t s
 }
 
 }  // namespace sssvd_gpu
+
+namespace sssvd_gpu {
+
+// ----------------------------------------------------------------------------- interchange map
+// One warp per shift folds the np sequential interchanges (r0+j <-> ipiv[r0+j]) into
+//   src[q]  (q < np): the ORIGINAL row whose content ends at position r0+q, and
+//   disp    : the moves (dst >= r0+np <- src) of rows displaced below the panel.
+// Every displaced row receives original content of a panel row (ipiv[r0+j] >= r0+j), so the
+// displaced moves can be applied in place before the panel rows are overwritten.
+__global__ void build_moves_kernel(const int* __restrict__ ipiv, int n, int r0, int np, int* __restrict__ src,
+                                   int* __restrict__ disp, int stride) {
+  extern __shared__ int mv[];
+  int* pos = mv;              // [2 np]
+  int* cont = mv + 2 * np;    // [2 np]
+  const int b = blockIdx.x;
+  const int* piv = ipiv + (size_t)b * n;
+  const int lane = threadIdx.x;
+  int k = 0;
+  for (int j = 0; j < np; ++j) {
+    const int a = r0 + j, q = piv[r0 + j];
+    int ia = -1, iq = -1;
+    for (int base = 0; base < k; base += 32) {
+      const int t = base + lane;
+      const int pv = t < k ? pos[t] : -1;
+      const unsigned ba = __ballot_sync(0xffffffffu, pv == a);
+      const unsigned bq = __ballot_sync(0xffffffffu, pv == q);
+      if (ba && ia < 0) ia = base + __ffs(ba) - 1;
+      if (bq && iq < 0) iq = base + __ffs(bq) - 1;
+    }
+    if (ia < 0) {
+      if (lane == 0) { pos[k] = a; cont[k] = a; }
+      ia = k++;
+    }
+    if (q == a) iq = ia;
+    if (iq < 0) {
+      if (lane == 0) { pos[k] = q; cont[k] = q; }
+      iq = k++;
+    }
+    __syncwarp();
+    if (lane == 0 && ia != iq) { int t = cont[ia]; cont[ia] = cont[iq]; cont[iq] = t; }
+    __syncwarp();
+  }
+  int* s = src + (size_t)b * stride;
+  int* d = disp + (size_t)b * (2 * stride + 1);
+  // displaced moves, compacted with a warp ballot
+  int nd = 0;
+  for (int base = 0; base < k; base += 32) {
+    const int t = base + lane;
+    const bool below = t < k && pos[t] >= r0 + np && cont[t] != pos[t];
+    if (t < k && pos[t] < r0 + np) s[pos[t] - r0] = cont[t];
+    const unsigned bal = __ballot_sync(0xffffffffu, below);
+    if (below) {
+      const int slot = nd + __popc(bal & ((1u << lane) - 1));
+      d[1 + 2 * slot] = pos[t];
+      d[2 + 2 * slot] = cont[t];
+    }
+    nd += __popc(bal);
+  }
+  if (lane == 0) d[0] = nd;
+}
+
+cudaError_t build_moves(const int* ipiv, int n, int r0, int np, int* src, int* disp, int stride, int batch,
+                        cudaStream_t s) {
+  build_moves_kernel<<<batch, 32, 4 * np * sizeof(int), s>>>(ipiv, n, r0, np, src, disp, stride);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------- L11^{-1}
+// Linv = L11^{-1} for the unit-lower np x np block at (r0, r0): one warp per column j; lanes
+// split each dot product, a warp reduction closes it. Row-major output with pitch np.
+__global__ void trinv_lower_kernel(const double2* __restrict__ mats, int ld, long long stride, int r0, int np,
+                                   double2* __restrict__ linv, long long lstride) {
+  const int b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (j >= np) return;
+  const double2* Mb = mats + b * stride + (size_t)r0 * ld + r0;
+  double2* out = linv + (size_t)b * lstride;
+  constexpr int QMAX = 4;   // np <= 128
+  double2 x[QMAX];
+#pragma unroll
+  for (int q = 0; q < QMAX; ++q) x[q] = make_double2((lane + 32 * q) == j ? 1.0 : 0.0, 0.0);
+  // rows in ascending order; the owning slot qi of row i = 32 qi + ii is a compile-time index
+#pragma unroll
+  for (int qi = 0; qi < QMAX; ++qi) {
+    for (int ii = 0; ii < 32; ++ii) {
+      const int i = 32 * qi + ii;
+      if (i <= j || i >= np) continue;
+      double sr = 0.0, si = 0.0;
+      const double2* Li = Mb + (size_t)i * ld;
+#pragma unroll
+      for (int q = 0; q <= qi; ++q) {
+        const int l = lane + 32 * q;
+        if (l >= j && l < i) {
+          const double2 L = Li[l];
+          sr += L.x * x[q].x - L.y * x[q].y;
+          si += L.x * x[q].y + L.y * x[q].x;
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        sr += __shfl_xor_sync(0xffffffffu, sr, off);
+        si += __shfl_xor_sync(0xffffffffu, si, off);
+      }
+      if (lane == ii) x[qi] = make_double2(-sr, -si);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < QMAX; ++q) {
+    const int i = lane + 32 * q;
+    if (i < np) out[(size_t)i * np + j] = i >= j ? x[q] : make_double2(0.0, 0.0);
+  }
+}
+
+cudaError_t trinv_lower(const double2* mats, int ld, long long stride, int r0, int np, double2* linv,
+                        long long lstride, int batch, cudaStream_t s) {
+  if (np > 128) return cudaErrorInvalidValue;
+  const int wpb = 4;
+  dim3 grid((np + wpb - 1) / wpb, batch);
+  trinv_lower_kernel<<<grid, 32 * wpb, 0, s>>>(mats, ld, stride, r0, np, linv, lstride);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------- scatter + copy
+// Columns [c0, c1): displaced rows get their (original panel-row) content, then the panel rows
+// r0..r0+np receive U12 = T (np x (c1-c0), pitch ldt). Each thread owns one column, so the
+// panel rows are read (as displaced sources) before they are overwritten.
+__global__ void scatter_copy_kernel(double2* mats, int ld, long long stride, int r0, int np, int c0, int c1,
+                                    const int* __restrict__ disp, int dstride, const double2* __restrict__ T,
+                                    int ldt, long long tstride) {
+  const int b = blockIdx.y;
+  const int c = c0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= c1) return;
+  double2* Mb = mats + b * stride;
+  const int* d = disp + (size_t)b * (2 * dstride + 1);
+  const int nd = d[0];
+  for (int t = 0; t < nd; ++t) Mb[(size_t)d[1 + 2 * t] * ld + c] = Mb[(size_t)d[2 + 2 * t] * ld + c];
+  const double2* Tb = T + b * tstride;
+  for (int q = 0; q < np; ++q) Mb[(size_t)(r0 + q) * ld + c] = Tb[(size_t)q * ldt + (c - c0)];
+}
+
+cudaError_t scatter_copy(double2* mats, int ld, long long stride, int r0, int np, int c0, int c1, const int* disp,
+                         int dstride, const double2* T, int ldt, long long tstride, int batch, cudaStream_t s) {
+  if (c1 <= c0) return cudaSuccess;
+  dim3 grid((c1 - c0 + 127) / 128, batch);
+  scatter_copy_kernel<<<grid, 128, 0, s>>>(mats, ld, stride, r0, np, c0, c1, disp, dstride, T, ldt, tstride);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------- back substitution
+// Rows r0..r0+np of the columns [c0,c1): x = U11^{-1} y by substitution (backward stable), one
+// warp per (column, shift); lanes split each dot product; x stays distributed over the lanes.
+__global__ void trsm_upper_warp_kernel(double2* mats, int ld, long long stride, int r0, int np, int c0, int c1) {
+  const int b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = c0 + blockIdx.x * (blockDim.x >> 5) + warp;
+  if (c >= c1) return;
+  double2* Mb = mats + b * stride;
+  constexpr int QMAX = 4;
+  double2 x[QMAX];
+#pragma unroll
+  for (int q = 0; q < QMAX; ++q) {
+    const int i = lane + 32 * q;
+    x[q] = i < np ? Mb[(size_t)(r0 + i) * ld + c] : make_double2(0.0, 0.0);
+  }
+#pragma unroll
+  for (int qi = QMAX - 1; qi >= 0; --qi) {
+    for (int ii = 31; ii >= 0; --ii) {
+      const int i = 32 * qi + ii;
+      if (i >= np) continue;
+      const double2* Ui = Mb + (size_t)(r0 + i) * ld + r0;
+      double sr = 0.0, si = 0.0;
+#pragma unroll
+      for (int q = qi; q < QMAX; ++q) {
+        const int l = lane + 32 * q;
+        if (l > i && l < np) {
+          const double2 U = Ui[l];
+          sr += U.x * x[q].x - U.y * x[q].y;
+          si += U.x * x[q].y + U.y * x[q].x;
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        sr += __shfl_xor_sync(0xffffffffu, sr, off);
+        si += __shfl_xor_sync(0xffffffffu, si, off);
+      }
+      if (lane == ii) {
+        const double2 u = Ui[i];
+        const double2 inv = cabs2(u) != 0.0 ? crecip(u) : make_double2(1.0, 0.0);
+        x[qi] = cmul(make_double2(x[qi].x - sr, x[qi].y - si), inv);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < QMAX; ++q) {
+    const int i = lane + 32 * q;
+    if (i < np) Mb[(size_t)(r0 + i) * ld + c] = x[q];
+  }
+}
+
+cudaError_t trsm_upper_warp(double2* mats, int ld, long long stride, int r0, int np, int c0, int c1, int batch,
+                            cudaStream_t s) {
+  if (c1 <= c0 || np <= 0) return cudaSuccess;
+  if (np > 128) return cudaErrorInvalidValue;
+  const int wpb = 4;
+  dim3 grid((c1 - c0 + wpb - 1) / wpb, batch);
+  trsm_upper_warp_kernel<<<grid, 32 * wpb, 0, s>>>(mats, ld, stride, r0, np, c0, c1);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace sssvd_gpu

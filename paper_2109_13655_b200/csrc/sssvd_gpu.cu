@@ -19,6 +19,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <numeric>
@@ -143,6 +144,7 @@ struct sssvd_gpu_ctx {
   bool has_gram = false;
   DBuf A, G, gmax, mats, ipiv, shifts, coef, S, V, status, minpiv, scratch;
   DBuf t0, t1, t2, t7, work, info;
+  DBuf lw_linv, lw_T, lw_src, lw_disp;
   DBuf tail[24];
   double t_gram = 0, t_solves = 0, t_allreduce = 0, solve_flops = 0;
 };
@@ -194,15 +196,42 @@ static LuPlan make_plan(int n, int L) {
   return p;
 }
 
+// Workspace of the batched LU: L11^{-1} per shift, the U12 staging block T, the interchange map.
+struct LuWork {
+  double2* linv;   // [nb][NB][NB]
+  double2* T;      // [nb][NB][n + L]
+  int* src;        // [nb][NB]
+  int* disp;       // [nb][2 NB + 1]
+  long long tstride;
+};
+
+// Applies the interchanges + unit-lower factor of the panel block (rows/cols r0..r0+np) to the
+// columns [c0, c1) and updates rows [r0+np, n) of those columns:
+//   T = L11^{-1} P A12  (DMMA GEMM gathering the pivoted rows on load)  -> U12
+//   displaced rows + U12 written back (scatter_copy), then A22 -= L21 T (DMMA GEMM)
+static void apply_panel(const LuPlan& P, const LuWork& W, double2* mats, const int* ipiv, int nb, cudaStream_t s,
+                        int r0, int np, int c0, int c1) {
+  const int n = P.n, N = c1 - c0;
+  if (N <= 0) return;
+  CK(build_moves(ipiv, n, r0, np, W.src, W.disp, P.NB, nb, s));
+  CK(trinv_lower(mats, P.ld, P.stride, r0, np, W.linv, (long long)P.NB * P.NB, nb, s));
+  CK(zgemm_set_gather(np, N, np, W.linv, np, (long long)P.NB * P.NB, mats + c0, P.ld, P.stride, W.src, P.NB, W.T, N,
+                      W.tstride, nb, s));
+  CK(scatter_copy(mats, P.ld, P.stride, r0, np, c0, c1, W.disp, P.NB, W.T, N, W.tstride, nb, s));
+  const int M = n - (r0 + np);
+  if (M > 0)
+    CK(zgemm_sub(M, N, np, mats + (size_t)(r0 + np) * P.ld + r0, P.ld, P.stride, W.T, N, W.tstride,
+                 mats + (size_t)(r0 + np) * P.ld + c0, P.ld, P.stride, nb, s));
+}
+
 // Recursive (getrf2-style) factorisation of the panel columns [c0, c0+w) over rows [c0, n),
-// confined to the current NB block [cb, ce): leaves of width <= W run the cluster kernel; an
-// internal node factors its left half, applies those interchanges + the unit-lower solve to its
-// right half, updates the right half with one DMMA GEMM (K = left width), then factors the right
-// half. Each leaf applies its interchanges to the block columns on its left; the columns on its
-// right receive them from the lowest common ancestor, so every block column sees every
-// interchange of the block exactly once and in order (LAPACK semantics within the block).
-static void factor_rec(const LuPlan& P, double2* mats, int* ipiv, int nb, cudaStream_t s, int c0, int w,
-                       int cb) {
+// confined to the current NB block starting at column cb: leaves of width <= W run the cluster
+// kernel; an internal node factors its left half, applies it to its right half (apply_panel,
+// K = left width), then factors the right half. Each leaf applies its interchanges to the
+// block columns on its left; the columns on its right receive them from the lowest common
+// ancestor, so every block column sees every interchange of the block once and in order.
+static void factor_rec(const LuPlan& P, const LuWork& W, double2* mats, int* ipiv, int nb, cudaStream_t s, int c0,
+                       int w, int cb) {
   const int n = P.n;
   if (w <= P.W) {
     CK(leaf_lu(mats, P.ld, P.stride, n, c0, w, P.W, P.cluster, ipiv, nb, s));
@@ -211,52 +240,53 @@ static void factor_rec(const LuPlan& P, double2* mats, int* ipiv, int nb, cudaSt
   }
   int wl = ((w / 2) + P.W - 1) / P.W * P.W;
   if (wl >= w) wl = w - P.W;
-  factor_rec(P, mats, ipiv, nb, s, c0, wl, cb);
-  const int r0 = c0 + wl, wr = w - wl;
-  CK(swap_trsm(mats, P.ld, P.stride, n, c0, wl, r0, r0 + wr, ipiv, true, nb, s));
-  if (n - r0 > 0)
-    CK(zgemm_sub(n - r0, wr, wl, mats + (size_t)r0 * P.ld + c0, P.ld, P.stride, mats + (size_t)c0 * P.ld + r0, P.ld,
-                 P.stride, mats + (size_t)r0 * P.ld + r0, P.ld, P.stride, nb, s));
-  factor_rec(P, mats, ipiv, nb, s, r0, wr, cb);
+  factor_rec(P, W, mats, ipiv, nb, s, c0, wl, cb);
+  apply_panel(P, W, mats, ipiv, nb, s, c0, wl, c0 + wl, c0 + w);
+  factor_rec(P, W, mats, ipiv, nb, s, c0 + wl, w - wl, cb);
 }
 
 // LU of nb augmented matrices [z I - G | V] in place (rows 0..n-1, cols 0..n+L-1), then the
 // back substitution U^{-1} on the L right-hand-side columns. ipiv: nb x n.
-static void lu_solve_batch(const LuPlan& P, double2* mats, int* ipiv, int nb, cudaStream_t s) {
+static void lu_solve_batch(const LuPlan& P, const LuWork& W, double2* mats, int* ipiv, int nb, cudaStream_t s) {
   const int n = P.n, ncols = n + P.L;
   for (int kb = 0; kb < n; kb += P.NB) {
     const int nbk = std::min(P.NB, n - kb);
-    factor_rec(P, mats, ipiv, nb, s, kb, nbk, kb);
-    const int c0 = kb + nbk;
-    if (c0 < ncols) {
-      // trailing columns (incl. the right-hand side): all NB interchanges, U12 = L11^{-1} A12,
-      // then A22 -= L21 U12 on the FP64 tensor cores
-      CK(swap_trsm(mats, P.ld, P.stride, n, kb, nbk, c0, ncols, ipiv, true, nb, s));
-      const int M = n - c0, N = ncols - c0;
-      if (M > 0)
-        CK(zgemm_sub(M, N, nbk, mats + (size_t)c0 * P.ld + kb, P.ld, P.stride,
-                     mats + (size_t)kb * P.ld + c0, P.ld, P.stride, mats + (size_t)c0 * P.ld + c0, P.ld,
-                     P.stride, nb, s));
-    }
+    factor_rec(P, W, mats, ipiv, nb, s, kb, nbk, kb);
+    // trailing columns (incl. the right-hand side): all NB interchanges, U12, A22 -= L21 U12
+    apply_panel(P, W, mats, ipiv, nb, s, kb, nbk, kb + nbk, ncols);
   }
-  // back substitution on the RHS columns [n, n+L)
+  // back substitution on the RHS columns [n, n+L): substitution per diagonal block (warp per
+  // column), DMMA GEMM for the off-diagonal blocks
   const int nblocks = (n + P.NB - 1) / P.NB;
   for (int bi = nblocks - 1; bi >= 0; --bi) {
     const int kb = bi * P.NB, nbk = std::min(P.NB, n - kb);
-    CK(trsm_upper(mats, P.ld, P.stride, kb, nbk, n, ncols, nb, s));
+    CK(trsm_upper_warp(mats, P.ld, P.stride, kb, nbk, n, ncols, nb, s));
     if (kb > 0)
       CK(zgemm_sub(kb, P.L, nbk, mats + kb, P.ld, P.stride, mats + (size_t)kb * P.ld + n, P.ld, P.stride,
                    mats + n, P.ld, P.stride, nb, s));
   }
 }
 
-static size_t bytes_per_shift(const LuPlan& P) { return (size_t)P.stride * sizeof(double2) + (size_t)P.n * sizeof(int); }
+static LuWork make_work(sssvd_gpu_ctx* ctx, const LuPlan& P, int B) {
+  LuWork W;
+  W.tstride = (long long)P.NB * (P.n + P.L);
+  W.linv = ctx->lw_linv.as<double2>((size_t)B * P.NB * P.NB);
+  W.T = ctx->lw_T.as<double2>((size_t)B * W.tstride);
+  W.src = ctx->lw_src.as<int>((size_t)B * P.NB);
+  W.disp = ctx->lw_disp.as<int>((size_t)B * (2 * P.NB + 1));
+  return W;
+}
+
+static size_t bytes_per_shift(const LuPlan& P) {
+  return (size_t)P.stride * sizeof(double2) + (size_t)P.n * sizeof(int) +
+         (size_t)P.NB * (P.n + P.L + P.NB) * sizeof(double2);
+}
 
 static int choose_batch(sssvd_gpu_ctx* ctx, const LuPlan& P, int64_t shifts) {
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
   // keep what is already allocated for mats reusable; leave 4 GiB headroom for the tail
-  size_t avail = free_b + ctx->mats.cap + ctx->ipiv.cap;
+  size_t avail = free_b + ctx->mats.cap + ctx->ipiv.cap + ctx->lw_T.cap + ctx->lw_linv.cap;
   const size_t headroom = (size_t)4 << 30;
   avail = avail > headroom ? avail - headroom : avail / 2;
   int64_t b = std::max<int64_t>(1, (int64_t)(avail / bytes_per_shift(P)));
@@ -283,6 +313,7 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
   double2* dcoef = ctx->coef.as<double2>((size_t)(M + 1) * B);
   int* dstatus = ctx->status.as<int>(B);
   double* dmin = ctx->minpiv.as<double>(B);
+  const LuWork work = make_work(ctx, P, B);
   std::vector<double2> hshift(B), hcoef((size_t)(M + 1) * B);
   std::vector<int> hstatus(B);
   for (int64_t j0 = jb; j0 < je; j0 += B) {
@@ -296,7 +327,7 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
     CK(cudaMemcpyAsync(dshift, hshift.data(), sizeof(double2) * nb, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(dcoef, hcoef.data(), sizeof(double2) * (M + 1) * nb, cudaMemcpyHostToDevice, s));
     CK(assemble(ctx->G.as<double>(0), n, n, V_dev, L, dshift, mats, P.ld, P.stride, nb, s));
-    lu_solve_batch(P, mats, ipiv, nb, s);
+    lu_solve_batch(P, work, mats, ipiv, nb, s);
     CK(pivot_floor(mats, P.ld, P.stride, n, dshift, ctx->gmax.as<double>(1), dstatus, dmin, nb, s));
     CK(moments(mats, P.ld, P.stride, n, n, L, nb, dcoef, M, S_dev, s));
     CK(cudaMemcpyAsync(hstatus.data(), dstatus, sizeof(int) * nb, cudaMemcpyDeviceToHost, s));
@@ -360,8 +391,40 @@ static void thin_qr(sssvd_gpu_ctx* ctx, double* A, int m, int k, double* R) {
   CKS(cusolverDnDorgqr(ctx->solver, m, k, k, A, m, tau, work, std::max(lw1, lw2), dinfo));
 }
 
-// full SVD of a square k x k matrix B (destroyed): U (k x k), S (k, descending), V (k x k)
+// full SVD of a square k x k matrix B (destroyed): U (k x k), S (k, descending), V (k x k).
+// Method (round-1 interim, cuSOLVER): SSSVD_TAIL_SVD = gesvdj (default; one-sided Jacobi like
+// the reference's JacobiSVD), gesvdp (polar decomposition) or gesvd (bidiagonal QR).
 static void svd_square(sssvd_gpu_ctx* ctx, double* B, int k, double* U, double* S, double* V) {
+  static const char* env = std::getenv("SSSVD_TAIL_SVD");
+  const std::string method = env ? env : "gesvdj";
+  int* dinfo = ctx->info.as<int>(1);
+  if (method == "gesvdp" || method == "gesvd") {
+    cusolverDnParams_t params;
+    CKS(cusolverDnCreateParams(&params));
+    size_t dws = 0, hws = 0;
+    if (method == "gesvdp") {
+      CKS(cusolverDnXgesvdp_bufferSize(ctx->solver, params, CUSOLVER_EIG_MODE_VECTOR, 0, k, k, CUDA_R_64F, B, k,
+                                       CUDA_R_64F, S, CUDA_R_64F, U, k, CUDA_R_64F, V, k, CUDA_R_64F, &dws, &hws));
+      void* dw = ctx->work.get(dws);
+      std::vector<char> hw(hws + 1);
+      double err = 0;
+      CKS(cusolverDnXgesvdp(ctx->solver, params, CUSOLVER_EIG_MODE_VECTOR, 0, k, k, CUDA_R_64F, B, k, CUDA_R_64F, S,
+                            CUDA_R_64F, U, k, CUDA_R_64F, V, k, CUDA_R_64F, dw, dws, hw.data(), hws, dinfo, &err));
+    } else {
+      // gesvd returns V^T; transpose into V afterwards
+      double* VT = ctx->t7.as<double>((size_t)k * k + 64);
+      CKS(cusolverDnXgesvd_bufferSize(ctx->solver, params, 'A', 'A', k, k, CUDA_R_64F, B, k, CUDA_R_64F, S,
+                                      CUDA_R_64F, U, k, CUDA_R_64F, VT, k, CUDA_R_64F, &dws, &hws));
+      void* dw = ctx->work.get(dws);
+      std::vector<char> hw(hws + 1);
+      CKS(cusolverDnXgesvd(ctx->solver, params, 'A', 'A', k, k, CUDA_R_64F, B, k, CUDA_R_64F, S, CUDA_R_64F, U, k,
+                           CUDA_R_64F, VT, k, CUDA_R_64F, dw, dws, hw.data(), hws, dinfo));
+      const double one = 1.0, zero = 0.0;
+      CKB(cublasDgeam(ctx->blas, CUBLAS_OP_T, CUBLAS_OP_N, k, k, &one, VT, k, &zero, V, k, V, k));
+    }
+    cusolverDnDestroyParams(params);
+    return;
+  }
   gesvdjInfo_t params;
   CKS(cusolverDnCreateGesvdjInfo(&params));
   CKS(cusolverDnXgesvdjSetTolerance(params, 1e-15));
@@ -370,7 +433,6 @@ static void svd_square(sssvd_gpu_ctx* ctx, double* B, int k, double* U, double* 
   CKS(cusolverDnDgesvdj_bufferSize(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, 0, k, k, B, k, S, U, k, V, k, &lwork,
                                    params));
   double* work = ctx->work.as<double>(lwork);
-  int* dinfo = ctx->info.as<int>(1);
   CKS(cusolverDnDgesvdj(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, 0, k, k, B, k, S, U, k, V, k, work, lwork, dinfo,
                         params));
   cusolverDnDestroyGesvdjInfo(params);
@@ -762,7 +824,7 @@ void sssvd_gpu_destroy(sssvd_gpu_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   DBuf* bufs[] = {&ctx->A, &ctx->G, &ctx->gmax, &ctx->mats, &ctx->ipiv, &ctx->shifts, &ctx->coef, &ctx->S, &ctx->V,
                   &ctx->status, &ctx->minpiv, &ctx->scratch, &ctx->t0, &ctx->t1, &ctx->t2, &ctx->t7, &ctx->work,
-                  &ctx->info};
+                  &ctx->info, &ctx->lw_linv, &ctx->lw_T, &ctx->lw_src, &ctx->lw_disp};
   for (DBuf* b : bufs) b->release();
   for (auto& b : ctx->tail) b.release();
   if (ctx->comm) nccl().CommDestroy(ctx->comm);
@@ -886,7 +948,7 @@ sssvd_status sssvd_gpu_shifted_solve(sssvd_gpu_ctx* ctx, const double* g, int64_
       for (int64_t i = 0; i < n; ++i) hrow[(size_t)i * L + c] = make_double2(rhs[2 * (c * n + i)], rhs[2 * (c * n + i) + 1]);
     CK(cudaMemcpy2DAsync(mats + n, sizeof(double2) * P.ld, hrow.data(), sizeof(double2) * L, sizeof(double2) * L, n,
                          cudaMemcpyHostToDevice, s));
-    lu_solve_batch(P, mats, ipiv, 1, s);
+    lu_solve_batch(P, make_work(ctx, P, 1), mats, ipiv, 1, s);
     int* dstatus = ctx->status.as<int>(1);
     double* dmin = ctx->minpiv.as<double>(1);
     CK(pivot_floor(mats, P.ld, P.stride, (int)n, dz, gmax, dstatus, dmin, 1, s));

@@ -61,8 +61,9 @@ constexpr int A_STAGE = BM * LDA_S;
 constexpr int B_STAGE = BK * LDB_S;
 constexpr int THREADS = 128;
 
+template <bool GATHER>
 __device__ __forceinline__ void load_stage(double2* As, double2* Bs, const double2* A, int lda,
-                                           const double2* B, int ldb, int M, int N, int K,
+                                           const double2* B, int ldb, const int* brow, int M, int N, int K,
                                            int m0, int n0, int k0, int tid) {
 #pragma unroll
   for (int i = 0; i < (BM * BK) / THREADS; ++i) {
@@ -77,16 +78,20 @@ __device__ __forceinline__ void load_stage(double2* As, double2* Bs, const doubl
     int idx = tid + i * THREADS;
     int kk = idx / BN, c = idx % BN;
     bool p = (k0 + kk < K) && (n0 + c < N);
-    const double2* src = p ? B + (size_t)(k0 + kk) * ldb + (n0 + c) : B;
+    const int row = p ? (GATHER ? brow[k0 + kk] : k0 + kk) : 0;
+    const double2* src = p ? B + (size_t)row * ldb + (n0 + c) : B;
     cp_async16(Bs + kk * LDB_S + c, src, p);
   }
 }
 }  // namespace
 
+// SET: C = A B (C is not read); otherwise C -= A B. GATHER: row k of B is row brow[k] of the
+// B matrix (the pivoted rows of the panel block, read straight from their pre-interchange place).
+template <bool SET, bool GATHER>
 __global__ void __launch_bounds__(THREADS, 2)
-zgemm_sub_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long long sA,
-                 const double2* __restrict__ B, int ldb, long long sB, double2* C, int ldc,
-                 long long sC) {
+zgemm_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long long sA,
+             const double2* __restrict__ B, int ldb, long long sB, const int* __restrict__ brow, int sR,
+             double2* C, int ldc, long long sC) {
   extern __shared__ __align__(16) double2 smem[];
   double2* As = smem;
   double2* Bs = smem + STAGES * A_STAGE;
@@ -96,6 +101,7 @@ zgemm_sub_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, lo
   A += blockIdx.z * sA;
   B += blockIdx.z * sB;
   C += blockIdx.z * sC;
+  if (GATHER) brow += blockIdx.z * sR;
 
   double acc_re[4][4][2], acc_im[4][4][2];
 #pragma unroll
@@ -109,7 +115,7 @@ zgemm_sub_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, lo
   const int KT = (K + BK - 1) / BK;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) load_stage(As + s * A_STAGE, Bs + s * B_STAGE, A, lda, B, ldb, M, N, K, m0, n0, s * BK, tid);
+    if (s < KT) load_stage<GATHER>(As + s * A_STAGE, Bs + s * B_STAGE, A, lda, B, ldb, brow, M, N, K, m0, n0, s * BK, tid);
     cp_async_commit();
   }
   const int fr = lane >> 2, fc = lane & 3;
@@ -120,7 +126,7 @@ zgemm_sub_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, lo
       int nk = kt + STAGES - 1;
       if (nk < KT) {
         int st = nk % STAGES;
-        load_stage(As + st * A_STAGE, Bs + st * B_STAGE, A, lda, B, ldb, M, N, K, m0, n0, nk * BK, tid);
+        load_stage<GATHER>(As + st * A_STAGE, Bs + st * B_STAGE, A, lda, B, ldb, brow, M, N, K, m0, n0, nk * BK, tid);
       }
       cp_async_commit();
     }
@@ -157,7 +163,10 @@ zgemm_sub_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, lo
     for (int j = 0; j < 4; ++j) {
       const int c = n0 + wn * 32 + j * 8 + 2 * fc;
       double2* cp = C + (size_t)r * ldc + c;
-      if (c + 1 < N) {
+      if (SET) {
+        if (c < N) cp[0] = make_double2(acc_re[i][j][0], acc_im[i][j][0]);
+        if (c + 1 < N) cp[1] = make_double2(acc_re[i][j][1], acc_im[i][j][1]);
+      } else if (c + 1 < N) {
         double2 v0 = cp[0], v1 = cp[1];
         v0.x -= acc_re[i][j][0];
         v0.y -= acc_im[i][j][0];
@@ -177,13 +186,14 @@ zgemm_sub_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, lo
 
 size_t zgemm_sub_smem() { return (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double2); }
 
-cudaError_t zgemm_sub(int M, int N, int K, const double2* A, int lda, long long sA,
-                      const double2* B, int ldb, long long sB, double2* C, int ldc, long long sC,
-                      int batch, cudaStream_t stream) {
+template <bool SET, bool GATHER>
+static cudaError_t launch(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B, int ldb,
+                          long long sB, const int* brow, int sR, double2* C, int ldc, long long sC, int batch,
+                          cudaStream_t stream) {
   if (M <= 0 || N <= 0 || K <= 0 || batch <= 0) return cudaSuccess;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(zgemm_sub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(zgemm_kernel<SET, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)zgemm_sub_smem());
     if (e != cudaSuccess) return e;
     configured = true;
@@ -199,8 +209,8 @@ cudaError_t zgemm_sub(int M, int N, int K, const double2* A, int lda, long long 
     }
     cudaEventRecord(g_prof.ev[2 * g_prof.used], stream);
   }
-  zgemm_sub_kernel<<<grid, THREADS, zgemm_sub_smem(), stream>>>(M, N, K, A, lda, sA, B, ldb, sB, C,
-                                                                 ldc, sC);
+  zgemm_kernel<SET, GATHER><<<grid, THREADS, zgemm_sub_smem(), stream>>>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR,
+                                                                         C, ldc, sC);
   note_launch();
   if (g_prof.on) {
     cudaEventRecord(g_prof.ev[2 * g_prof.used + 1], stream);
@@ -208,6 +218,18 @@ cudaError_t zgemm_sub(int M, int N, int K, const double2* A, int lda, long long 
     ++g_prof.used;
   }
   return cudaGetLastError();
+}
+
+cudaError_t zgemm_sub(int M, int N, int K, const double2* A, int lda, long long sA,
+                      const double2* B, int ldb, long long sB, double2* C, int ldc, long long sC,
+                      int batch, cudaStream_t stream) {
+  return launch<false, false>(M, N, K, A, lda, sA, B, ldb, sB, nullptr, 0, C, ldc, sC, batch, stream);
+}
+
+cudaError_t zgemm_set_gather(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B,
+                             int ldb, long long sB, const int* brow, int sR, double2* C, int ldc, long long sC,
+                             int batch, cudaStream_t stream) {
+  return launch<true, true>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stream);
 }
 
 }  // namespace sssvd_gpu
