@@ -26,6 +26,11 @@ cudaError_t assemble(const double* G, int n, int ldg, const double* V, int L, co
 size_t leaf_smem_bytes(int n, int W, int cluster);
 cudaError_t leaf_lu(double2* mats, int ld, long long stride, int n, int r0, int w, int W, int cluster,
                     int* ipiv, int batch, cudaStream_t s);
+// K2 v2 (lu.cu): register-resident leaf; variant 0: W32 (<=256 rows/CTA), 1: W16 (<=512), 2: W8 (<=1024)
+int leaf_v2_rows_per_cta(int variant);
+int leaf_v2_width(int variant);
+cudaError_t leaf_lu_v2(double2* mats, int ld, long long stride, int n, int r0, int w, int variant, int cluster,
+                       int* ipiv, int batch, cudaStream_t s);
 // K3/K4 (lu.cu): interchanges ipiv[r0..r0+np) on columns [c0,c1), then optional unit-lower TRSM
 cudaError_t swap_trsm(double2* mats, int ld, long long stride, int n, int r0, int np, int c0, int c1,
                       const int* ipiv, bool do_trsm, int batch, cudaStream_t s);

@@ -533,21 +533,36 @@ __global__ void trinv_lower_kernel(const double2* __restrict__ mats, int ld, lon
   double2 x[QMAX];
 #pragma unroll
   for (int q = 0; q < QMAX; ++q) x[q] = make_double2((lane + 32 * q) == j ? 1.0 : 0.0, 0.0);
-  // rows in ascending order; the owning slot qi of row i = 32 qi + ii is a compile-time index
+  // rows in ascending order; the owning slot qi of row i = 32 qi + ii is a compile-time index,
+  // and row i's multipliers L[i][l] (l = lane + 32 q) are prefetched one row ahead
+  double2 ln[QMAX];
+#pragma unroll
+  for (int q = 0; q < QMAX; ++q) {
+    const int l = lane + 32 * q;
+    ln[q] = (j + 1 < np && l < np) ? Mb[(size_t)(j + 1) * ld + l] : make_double2(0.0, 0.0);
+  }
 #pragma unroll
   for (int qi = 0; qi < QMAX; ++qi) {
     for (int ii = 0; ii < 32; ++ii) {
       const int i = 32 * qi + ii;
       if (i <= j || i >= np) continue;
+      double2 lr[QMAX];
+#pragma unroll
+      for (int q = 0; q < QMAX; ++q) lr[q] = ln[q];
+      if (i + 1 < np) {
+#pragma unroll
+        for (int q = 0; q < QMAX; ++q) {
+          const int l = lane + 32 * q;
+          ln[q] = l < np ? Mb[(size_t)(i + 1) * ld + l] : make_double2(0.0, 0.0);
+        }
+      }
       double sr = 0.0, si = 0.0;
-      const double2* Li = Mb + (size_t)i * ld;
 #pragma unroll
       for (int q = 0; q <= qi; ++q) {
         const int l = lane + 32 * q;
         if (l >= j && l < i) {
-          const double2 L = Li[l];
-          sr += L.x * x[q].x - L.y * x[q].y;
-          si += L.x * x[q].y + L.y * x[q].x;
+          sr += lr[q].x * x[q].x - lr[q].y * x[q].y;
+          si += lr[q].x * x[q].y + lr[q].y * x[q].x;
         }
       }
 #pragma unroll
@@ -611,27 +626,46 @@ __global__ void trsm_upper_warp_kernel(double2* mats, int ld, long long stride, 
   const int c = c0 + blockIdx.x * (blockDim.x >> 5) + warp;
   if (c >= c1) return;
   double2* Mb = mats + b * stride;
+  const double2* U = Mb + (size_t)r0 * ld + r0;
   constexpr int QMAX = 4;
-  double2 x[QMAX];
+  double2 x[QMAX], invd[QMAX];
 #pragma unroll
   for (int q = 0; q < QMAX; ++q) {
     const int i = lane + 32 * q;
     x[q] = i < np ? Mb[(size_t)(r0 + i) * ld + c] : make_double2(0.0, 0.0);
+    // reciprocal of the pivot of the row this lane owns, off the serial critical path
+    const double2 u = i < np ? U[(size_t)i * ld + i] : make_double2(1.0, 0.0);
+    invd[q] = cabs2(u) != 0.0 ? crecip(u) : make_double2(1.0, 0.0);
+  }
+  // row i's multipliers U[i][l] (l = lane + 32 q) are prefetched one row ahead
+  double2 un[QMAX];
+#pragma unroll
+  for (int q = 0; q < QMAX; ++q) {
+    const int l = lane + 32 * q;
+    un[q] = l < np ? U[(size_t)(np - 1) * ld + l] : make_double2(0.0, 0.0);
   }
 #pragma unroll
   for (int qi = QMAX - 1; qi >= 0; --qi) {
     for (int ii = 31; ii >= 0; --ii) {
       const int i = 32 * qi + ii;
       if (i >= np) continue;
-      const double2* Ui = Mb + (size_t)(r0 + i) * ld + r0;
+      double2 ur[QMAX];
+#pragma unroll
+      for (int q = 0; q < QMAX; ++q) ur[q] = un[q];
+      if (i > 0) {
+#pragma unroll
+        for (int q = 0; q < QMAX; ++q) {
+          const int l = lane + 32 * q;
+          un[q] = l < np ? U[(size_t)(i - 1) * ld + l] : make_double2(0.0, 0.0);
+        }
+      }
       double sr = 0.0, si = 0.0;
 #pragma unroll
       for (int q = qi; q < QMAX; ++q) {
         const int l = lane + 32 * q;
         if (l > i && l < np) {
-          const double2 U = Ui[l];
-          sr += U.x * x[q].x - U.y * x[q].y;
-          si += U.x * x[q].y + U.y * x[q].x;
+          sr += ur[q].x * x[q].x - ur[q].y * x[q].y;
+          si += ur[q].x * x[q].y + ur[q].y * x[q].x;
         }
       }
 #pragma unroll
@@ -639,11 +673,7 @@ __global__ void trsm_upper_warp_kernel(double2* mats, int ld, long long stride, 
         sr += __shfl_xor_sync(0xffffffffu, sr, off);
         si += __shfl_xor_sync(0xffffffffu, si, off);
       }
-      if (lane == ii) {
-        const double2 u = Ui[i];
-        const double2 inv = cabs2(u) != 0.0 ? crecip(u) : make_double2(1.0, 0.0);
-        x[qi] = cmul(make_double2(x[qi].x - sr, x[qi].y - si), inv);
-      }
+      if (lane == ii) x[qi] = cmul(make_double2(x[qi].x - sr, x[qi].y - si), invd[qi]);
     }
   }
 #pragma unroll
@@ -662,6 +692,223 @@ cudaError_t trsm_upper_warp(double2* mats, int ld, long long stride, int r0, int
   trsm_upper_warp_kernel<<<grid, 32 * wpb, 0, s>>>(mats, ld, stride, r0, np, c0, c1);
   note_launch();
   return cudaGetLastError();
+}
+
+}  // namespace sssvd_gpu
+
+namespace sssvd_gpu {
+
+// ----------------------------------------------------------------------------- K2 leaf, v2
+// Register-resident leaf panel LU. One cluster of C CTAs per shift (blockIdx.y); CTA c owns
+// rows [r0 + c R, r0 + (c+1) R) of the leaf columns [r0, r0 + w), thread t of that CTA owns
+// rows t + q*NT (q < RPT) with all W columns in registers. The column loop is fully unrolled so
+// every register index is static. Per column j:
+//   scale + rank-1 update of the thread's own rows (no block barrier: rows are thread-private)
+//   -> score of column j+1 fused into the same pass -> warp argmax -> CTA argmax (1 barrier)
+//   -> candidate row / diagonal row published in shared memory -> cluster barrier
+//   -> warp 0 reduces the C candidates over DSMEM (1 barrier) -> winner row fetched over DSMEM
+//   (1 barrier) -> the owners of rows d and p swap contents.
+template <int W, int RPT, int NT>
+__global__ void __launch_bounds__(NT, 1)
+leaf_lu_v2_kernel(double2* mats, int ld, long long stride, int n, int r0, int w, int R, int* ipiv) {
+  __shared__ double2 cand_vals[2][W];
+  __shared__ double2 diag_vals[2][W];
+  __shared__ double2 urow[W];
+  __shared__ double cand_score[2];
+  __shared__ int cand_row[2];
+  __shared__ double red_s[NT / 32];
+  __shared__ int red_r[NT / 32];
+  __shared__ int win[2];
+
+  const int C = gridDim.x;
+  const unsigned rank = cluster_ctarank();
+  const int b = blockIdx.y;
+  double2* Mb = mats + b * stride;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int my0 = r0 + (int)rank * R;
+  const int myn = max(0, min(R, n - my0));
+
+  double2 a[RPT][W];
+  int gi[RPT];
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int li = tid + q * NT;
+    gi[q] = li < myn ? my0 + li : 0x7fffffff;
+#pragma unroll
+    for (int c = 0; c < W; ++c)
+      a[q][c] = (li < myn && c < w) ? Mb[(size_t)gi[q] * ld + r0 + c] : make_double2(0.0, 0.0);
+  }
+
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    if (j < w) {
+      const int d = r0 + j;
+      const int par = j & 1;
+      // ---- pivot search on column j (values already updated by the previous iteration)
+      double best = -1.0;
+      int brow = 0x7fffffff;
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) {
+        if (gi[q] >= d && gi[q] != 0x7fffffff) {
+          const double s = cabs2(a[q][j]);
+          if (s > best || (s == best && gi[q] < brow)) {
+            best = s;
+            brow = gi[q];
+          }
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const double os = __shfl_xor_sync(0xffffffffu, best, off);
+        const int orow = __shfl_xor_sync(0xffffffffu, brow, off);
+        if (os > best || (os == best && orow < brow)) {
+          best = os;
+          brow = orow;
+        }
+      }
+      if (lane == 0) {
+        red_s[warp] = best;
+        red_r[warp] = brow;
+      }
+      __syncthreads();
+      // every thread folds the NT/32 warp partials (so the owner of the CTA candidate knows)
+      best = -1.0;
+      brow = 0x7fffffff;
+#pragma unroll
+      for (int w2 = 0; w2 < NT / 32; ++w2) {
+        const double os = red_s[w2];
+        const int orow = red_r[w2];
+        if (os > best || (os == best && orow < brow)) {
+          best = os;
+          brow = orow;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) {
+        if (gi[q] == brow) {
+#pragma unroll
+          for (int c = 0; c < W; ++c) cand_vals[par][c] = a[q][c];
+        }
+        if (gi[q] == d) {
+#pragma unroll
+          for (int c = 0; c < W; ++c) diag_vals[par][c] = a[q][c];
+        }
+      }
+      if (tid == 0) {
+        cand_score[par] = best;
+        cand_row[par] = brow;
+      }
+      cluster_sync_all();
+      // ---- winner over the C candidates (DSMEM)
+      if (warp == 0) {
+        double s = -1.0;
+        int r = 0x7fffffff, rk = lane;
+        if (lane < C) {
+          s = ld_dsmem_f64(dsmem_addr(&cand_score[par], lane));
+          r = ld_dsmem_s32(dsmem_addr(&cand_row[par], lane));
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const double os = __shfl_xor_sync(0xffffffffu, s, off);
+          const int orow = __shfl_xor_sync(0xffffffffu, r, off);
+          const int ork = __shfl_xor_sync(0xffffffffu, rk, off);
+          if (os > s || (os == s && orow < r)) {
+            s = os;
+            r = orow;
+            rk = ork;
+          }
+        }
+        if (lane == 0) {
+          win[0] = rk;
+          win[1] = r;
+        }
+        // winner's row: every lane holds the reduced rank after the xor butterfly
+        for (int c = lane; c < W; c += 32) urow[c] = ld_dsmem_f64x2(dsmem_addr(&cand_vals[par][c], rk));
+      }
+      __syncthreads();
+      const int wrank = win[0], p = win[1];
+      const int downer = (d - r0) / R;
+      // ---- interchange rows d and p (owners only; p's owner reads the old row d via DSMEM)
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) {
+        if (gi[q] == p && p != d) {
+#pragma unroll
+          for (int c = 0; c < W; ++c) a[q][c] = ld_dsmem_f64x2(dsmem_addr(&diag_vals[par][c], downer));
+        } else if (gi[q] == d) {
+#pragma unroll
+          for (int c = 0; c < W; ++c) a[q][c] = urow[c];
+        }
+      }
+      (void)wrank;
+      if (rank == 0 && tid == 0) ipiv[(size_t)b * n + d] = p;
+      // ---- scale column j below the diagonal, rank-1 update of the columns right of j
+      const double2 u = urow[j];
+      if (cabs2(u) != 0.0) {
+        const double2 inv = crecip(u);
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+          if (gi[q] > d && gi[q] != 0x7fffffff) {
+            const double2 l = cmul(a[q][j], inv);
+            a[q][j] = l;
+#pragma unroll
+            for (int c = j + 1; c < W; ++c) a[q][c] = cfms(a[q][c], l, urow[c]);
+          }
+        }
+      }
+    }
+  }
+  // write back
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    if (gi[q] != 0x7fffffff) {
+#pragma unroll
+      for (int c = 0; c < W; ++c)
+        if (c < w) Mb[(size_t)gi[q] * ld + r0 + c] = a[q][c];
+    }
+  }
+  cluster_sync_all();   // keep every CTA's shared memory alive until all DSMEM reads are done
+}
+
+template <int W, int RPT, int NT>
+static cudaError_t launch_leaf_v2(double2* mats, int ld, long long stride, int n, int r0, int w, int cluster,
+                                  int* ipiv, int batch, cudaStream_t s) {
+  const int m = n - r0;
+  const int R = (m + cluster - 1) / cluster;
+  if (R > RPT * NT) return cudaErrorInvalidValue;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(leaf_lu_v2_kernel<W, RPT, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cluster, batch, 1);
+  cfg.blockDim = dim3(NT, 1, 1);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  note_launch();
+  return cudaLaunchKernelEx(&cfg, leaf_lu_v2_kernel<W, RPT, NT>, mats, ld, stride, n, r0, w, R, ipiv);
+}
+
+// variant ids: 0: W32/RPT1/256  1: W16/RPT1/512  2: W8/RPT2/512
+int leaf_v2_rows_per_cta(int variant) { return variant == 0 ? 256 : (variant == 1 ? 512 : 1024); }
+int leaf_v2_width(int variant) { return variant == 0 ? 32 : (variant == 1 ? 16 : 8); }
+
+cudaError_t leaf_lu_v2(double2* mats, int ld, long long stride, int n, int r0, int w, int variant, int cluster,
+                       int* ipiv, int batch, cudaStream_t s) {
+  switch (variant) {
+    case 0: return launch_leaf_v2<32, 1, 256>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s);
+    case 1: return launch_leaf_v2<16, 1, 512>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s);
+    case 2: return launch_leaf_v2<8, 2, 512>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace sssvd_gpu

@@ -161,6 +161,7 @@ namespace sssvd_gpu {
 // ----------------------------------------------------------------------------- LU driver
 struct LuPlan {
   int n, L, ld, NB, W, cluster;
+  int leaf_variant;   // >= 0: register-resident leaf_lu_v2 variant; -1: shared-memory leaf (v1)
   long long stride;
 };
 
@@ -193,6 +194,24 @@ static LuPlan make_plan(int n, int L) {
       }
   }
   if (!found) throw Status(SSSVD_E_LENGTH, "operator too large for the on-chip leaf panel");
+  // register-resident leaf (v2): rows per CTA <= threads x rows-per-thread of the variant
+  p.leaf_variant = -1;
+  static const char* leaf_env = std::getenv("SSSVD_LEAF");
+  if (!(leaf_env && std::string(leaf_env) == "v1")) {
+    for (int v = 0; v < 3 && p.leaf_variant < 0; ++v)
+      for (int c = 1; c <= 8; c *= 2)
+        if ((n + c - 1) / c <= leaf_v2_rows_per_cta(v)) {
+          p.leaf_variant = v;
+          p.cluster = c;
+          p.W = leaf_v2_width(v);
+          break;
+        }
+    if (p.leaf_variant < 0 && (n + 15) / 16 <= leaf_v2_rows_per_cta(2)) {
+      p.leaf_variant = 2;
+      p.cluster = 16;
+      p.W = leaf_v2_width(2);
+    }
+  }
   return p;
 }
 
@@ -234,7 +253,10 @@ static void factor_rec(const LuPlan& P, const LuWork& W, double2* mats, int* ipi
                        int w, int cb) {
   const int n = P.n;
   if (w <= P.W) {
-    CK(leaf_lu(mats, P.ld, P.stride, n, c0, w, P.W, P.cluster, ipiv, nb, s));
+    if (P.leaf_variant >= 0)
+      CK(leaf_lu_v2(mats, P.ld, P.stride, n, c0, w, P.leaf_variant, P.cluster, ipiv, nb, s));
+    else
+      CK(leaf_lu(mats, P.ld, P.stride, n, c0, w, P.W, P.cluster, ipiv, nb, s));
     if (c0 > cb) CK(swap_trsm(mats, P.ld, P.stride, n, c0, w, cb, c0, ipiv, false, nb, s));
     return;
   }
@@ -339,7 +361,7 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
 }
 
 static void allreduce_S(sssvd_gpu_ctx* ctx, double* S, size_t count) {
-  if (!ctx->comm || ctx->nranks <= 1) return;
+  if (!ctx->comm) return;   // a 1-rank communicator still runs the collective (exercised by the tests)
   CKN(nccl().AllReduce(S, S, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
 }
 

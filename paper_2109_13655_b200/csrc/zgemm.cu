@@ -83,6 +83,19 @@ __device__ __forceinline__ void load_stage(double2* As, double2* Bs, const doubl
     cp_async16(Bs + kk * LDB_S + c, src, p);
   }
 }
+// C half-tile h (rows 32h..32h+32 of the 64x64 tile) -> a free pipeline stage, pitch CP
+constexpr int CP = BN + 1;   // 65 double2: conflict-free fragment-pattern reads in the epilogue
+static_assert(32 * CP <= A_STAGE + B_STAGE, "C half-tile must fit one pipeline stage");
+__device__ __forceinline__ void load_c_half(double2* dst, const double2* C, int ldc, int M, int N, int m0,
+                                            int n0, int h, int tid) {
+#pragma unroll
+  for (int i = 0; i < (32 * BN) / THREADS; ++i) {
+    const int idx = tid + i * THREADS;
+    const int r = idx / BN, c = idx % BN;
+    const bool p = (m0 + 32 * h + r < M) && (n0 + c < N);
+    cp_async16(dst + r * CP + c, p ? C + (size_t)(m0 + 32 * h + r) * ldc + n0 + c : C, p);
+  }
+}
 }  // namespace
 
 // SET: C = A B (C is not read); otherwise C -= A B. GATHER: row k of B is row brow[k] of the
@@ -93,8 +106,10 @@ zgemm_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long l
              const double2* __restrict__ B, int ldb, long long sB, const int* __restrict__ brow, int sR,
              double2* C, int ldc, long long sC) {
   extern __shared__ __align__(16) double2 smem[];
+  // stage s occupies [s*(A_STAGE+B_STAGE), (s+1)*(A_STAGE+B_STAGE)): A tile then B tile
   double2* As = smem;
-  double2* Bs = smem + STAGES * A_STAGE;
+  double2* Bs = smem + A_STAGE;
+  constexpr int SSTRIDE = A_STAGE + B_STAGE;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
@@ -113,9 +128,16 @@ zgemm_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long l
     }
 
   const int KT = (K + BK - 1) / BK;
+  // C is prefetched into the two stages the k-loop no longer needs: half h goes to stage
+  // (KT + h) % 3, issued at iteration KT - 2 + h (or in the prologue when that is < 0)
+  auto c_stage = [&](int h) { return smem + ((KT + h) % STAGES) * (A_STAGE + B_STAGE); };
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) load_stage<GATHER>(As + s * A_STAGE, Bs + s * B_STAGE, A, lda, B, ldb, brow, M, N, K, m0, n0, s * BK, tid);
+    if (s < KT) load_stage<GATHER>(As + s * SSTRIDE, Bs + s * SSTRIDE, A, lda, B, ldb, brow, M, N, K, m0, n0, s * BK, tid);
+    if (!SET) {
+      for (int h = 0; h < 2; ++h)
+        if (KT - 2 + h < 0 && s == 0) load_c_half(c_stage(h), C, ldc, M, N, m0, n0, h, tid);
+    }
     cp_async_commit();
   }
   const int fr = lane >> 2, fc = lane & 3;
@@ -126,12 +148,15 @@ zgemm_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long l
       int nk = kt + STAGES - 1;
       if (nk < KT) {
         int st = nk % STAGES;
-        load_stage<GATHER>(As + st * A_STAGE, Bs + st * B_STAGE, A, lda, B, ldb, brow, M, N, K, m0, n0, nk * BK, tid);
+        load_stage<GATHER>(As + st * SSTRIDE, Bs + st * SSTRIDE, A, lda, B, ldb, brow, M, N, K, m0, n0, nk * BK, tid);
+      } else if (!SET) {
+        const int h = kt - (KT - 2);
+        if (h >= 0 && h < 2) load_c_half(c_stage(h), C, ldc, M, N, m0, n0, h, tid);
       }
       cp_async_commit();
     }
-    const double2* as = As + (kt % STAGES) * A_STAGE + (wm * 32 + fr) * LDA_S + fc;
-    const double2* bs = Bs + (kt % STAGES) * B_STAGE + fc * LDB_S + wn * 32 + fr;
+    const double2* as = As + (kt % STAGES) * SSTRIDE + (wm * 32 + fr) * LDA_S + fc;
+    const double2* bs = Bs + (kt % STAGES) * SSTRIDE + fc * LDB_S + wn * 32 + fr;
 #pragma unroll
     for (int kq = 0; kq < BK / 4; ++kq) {
       double2 a[4], b[4];
@@ -139,46 +164,61 @@ zgemm_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long l
       for (int i = 0; i < 4; ++i) a[i] = as[i * 8 * LDA_S + kq * 4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) b[j] = bs[kq * 4 * LDB_S + j * 8];
+      double nai[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const double nai = -a[i].y;
+      for (int i = 0; i < 4; ++i) nai[i] = -a[i].y;
+      // four passes over the 16 independent (i, j) accumulators: the two DMMAs feeding the
+      // same accumulator are 32 instructions apart, so the fixed-latency pipe never waits
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          dmma884(acc_re[i][j][0], acc_re[i][j][1], a[i].x, b[j].x);
-          dmma884(acc_re[i][j][0], acc_re[i][j][1], nai, b[j].y);
-          dmma884(acc_im[i][j][0], acc_im[i][j][1], a[i].x, b[j].y);
-          dmma884(acc_im[i][j][0], acc_im[i][j][1], a[i].y, b[j].x);
-        }
-      }
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc_re[i][j][0], acc_re[i][j][1], a[i].x, b[j].x);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc_im[i][j][0], acc_im[i][j][1], a[i].x, b[j].y);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc_re[i][j][0], acc_re[i][j][1], nai[i], b[j].y);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc_im[i][j][0], acc_im[i][j][1], a[i].y, b[j].x);
     }
   }
   cp_async_wait<0>();
+  __syncthreads();
 
-  // epilogue: C -= acc (fragment rows fr, cols 2*fc, 2*fc+1 of each 8x8 sub-tile)
+  // epilogue: C -= acc (fragment rows fr, cols 2*fc, 2*fc+1 of each 8x8 sub-tile). The 8 C
+  // values of a row block are loaded together before any store, so their latencies overlap.
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int r = m0 + wm * 32 + i * 8 + fr;
     if (r >= M) continue;
+    double2* crow = C + (size_t)r * ldc + n0 + wn * 32 + 2 * fc;
+    const int cbase = n0 + wn * 32 + 2 * fc;
+    if (SET) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int c = n0 + wn * 32 + j * 8 + 2 * fc;
-      double2* cp = C + (size_t)r * ldc + c;
-      if (SET) {
-        if (c < N) cp[0] = make_double2(acc_re[i][j][0], acc_im[i][j][0]);
-        if (c + 1 < N) cp[1] = make_double2(acc_re[i][j][1], acc_im[i][j][1]);
-      } else if (c + 1 < N) {
-        double2 v0 = cp[0], v1 = cp[1];
-        v0.x -= acc_re[i][j][0];
-        v0.y -= acc_im[i][j][0];
-        v1.x -= acc_re[i][j][1];
-        v1.y -= acc_im[i][j][1];
-        cp[0] = v0;
-        cp[1] = v1;
-      } else if (c < N) {
-        double2 v0 = cp[0];
-        v0.x -= acc_re[i][j][0];
-        v0.y -= acc_im[i][j][0];
-        cp[0] = v0;
+      for (int j = 0; j < 4; ++j) {
+        const int c = cbase + j * 8;
+        if (c < N) crow[j * 8] = make_double2(acc_re[i][j][0], acc_im[i][j][0]);
+        if (c + 1 < N) crow[j * 8 + 1] = make_double2(acc_re[i][j][1], acc_im[i][j][1]);
+      }
+    } else {
+      // C rows of this warp live in the prefetched half-tile wm (row i*8+fr, pitch CP)
+      const double2* cs = c_stage(wm) + (i * 8 + fr) * CP + wn * 32 + 2 * fc;
+      double2 v[4][2];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        v[j][0] = cs[j * 8];
+        v[j][1] = cs[j * 8 + 1];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = cbase + j * 8;
+        if (c < N) crow[j * 8] = make_double2(v[j][0].x - acc_re[i][j][0], v[j][0].y - acc_im[i][j][0]);
+        if (c + 1 < N) crow[j * 8 + 1] = make_double2(v[j][1].x - acc_re[i][j][1], v[j][1].y - acc_im[i][j][1]);
       }
     }
   }

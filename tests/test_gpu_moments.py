@@ -145,3 +145,19 @@ def test_ell2_matches_oracle(dev):
     ref = acc.accumulate(acc.refine(s0), 3).blocks
     for k in range(4):
         assert np.linalg.norm(blocks[k] - ref[k]) / np.linalg.norm(ref[k]) <= 1e-10
+
+
+def test_nccl_single_rank_comm_path(dev):
+    """The multi-GPU code path (dlopen'ed NCCL, shard range, ncclAllReduce of the partial
+    moments) run with a 1-rank communicator: results must be bitwise those without a comm."""
+    from paper_2109_13655_b200 import sssvd
+    a = constructed(300, 150, np.linspace(0.05, 1.5, 150), 3, 4)
+    rg, _ = rules(0.6, 0.9, 16, 0.1)
+    s0 = orc.random_start(150, 6, 42)
+    ref = gpu_blocks(dev, a, rg, s0, 3)
+    d2 = sssvd.Device(0)
+    d2.init_comm(sssvd.Device.nccl_unique_id(), 1, 0)
+    got = gpu_blocks(d2, a, rg, s0, 3)
+    d2.close()
+    for k in range(4):
+        assert np.array_equal(ref[k], got[k])
