@@ -180,6 +180,9 @@ sssvd_status sssvd_moment_coefficients(int64_t h, const double* weights, const d
 uint64_t sssvd_gpu_launch_count(void);
 void sssvd_gpu_profile_gemm(int enable);
 void sssvd_gpu_profile_gemm_collect(double* ms, double* flops, uint64_t* launches);
+/* Debug: cycles per leaf-kernel phase summed over columns (SSSVD_LEAF_PROF=1): out[0..3] phases,
+ * out[4] columns, out[5] summed CTA lifetimes, out[6] leaves (7 entries). */
+void sssvd_debug_leaf_profile(uint64_t* out7);
 /* Build provenance for the loaded library ("sm_100a ..."). */
 const char* sssvd_build_info(void);
 

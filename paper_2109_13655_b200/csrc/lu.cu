@@ -16,6 +16,7 @@
 //   * pivot_floor_kernel : min |U_ii| against 1e-30 (max|G| + |z|) (shifted_solver.hpp:27-30)
 // The trailing updates are zgemm_sub (zgemm.cu, DMMA).
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -708,12 +709,15 @@ namespace sssvd_gpu {
 //   -> candidate row / diagonal row published in shared memory -> cluster barrier
 //   -> warp 0 reduces the C candidates over DSMEM (1 barrier) -> winner row fetched over DSMEM
 //   (1 barrier) -> the owners of rows d and p swap contents.
-template <int W, int RPT, int NT>
+__device__ unsigned long long g_leaf_prof[8];   // per-phase cycle sums (PROF instances only)
+
+template <int W, int RPT, int NT, bool PROF = false>
 __global__ void __launch_bounds__(NT, 1)
 leaf_lu_v2_kernel(double2* mats, int ld, long long stride, int n, int r0, int w, int R, int* ipiv) {
   __shared__ double2 cand_vals[2][W];
   __shared__ double2 diag_vals[2][W];
   __shared__ double2 urow[W];
+  __shared__ double2 drow[W];
   __shared__ double cand_score[2];
   __shared__ int cand_row[2];
   __shared__ double red_s[NT / 32];
@@ -728,6 +732,7 @@ leaf_lu_v2_kernel(double2* mats, int ld, long long stride, int n, int r0, int w,
   const int my0 = r0 + (int)rank * R;
   const int myn = max(0, min(R, n - my0));
 
+  const unsigned long long t_entry = PROF ? clock64() : 0ull;
   double2 a[RPT][W];
   int gi[RPT];
 #pragma unroll
@@ -744,6 +749,9 @@ leaf_lu_v2_kernel(double2* mats, int ld, long long stride, int n, int r0, int w,
     if (j < w) {
       const int d = r0 + j;
       const int par = j & 1;
+      const bool rec = PROF && tid == 0 && rank == 0 && b == 0;
+      unsigned long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+      if (rec) t0 = clock64();
       // ---- pivot search on column j (values already updated by the previous iteration)
       double best = -1.0;
       int brow = 0x7fffffff;
@@ -771,6 +779,7 @@ leaf_lu_v2_kernel(double2* mats, int ld, long long stride, int n, int r0, int w,
         red_r[warp] = brow;
       }
       __syncthreads();
+      if (rec) t1 = clock64();
       // every thread folds the NT/32 warp partials (so the owner of the CTA candidate knows)
       best = -1.0;
       brow = 0x7fffffff;
@@ -799,6 +808,7 @@ leaf_lu_v2_kernel(double2* mats, int ld, long long stride, int n, int r0, int w,
         cand_row[par] = brow;
       }
       cluster_sync_all();
+      if (rec) t2 = clock64();
       // ---- winner over the C candidates (DSMEM)
       if (warp == 0) {
         double s = -1.0;
@@ -822,18 +832,23 @@ leaf_lu_v2_kernel(double2* mats, int ld, long long stride, int n, int r0, int w,
           win[0] = rk;
           win[1] = r;
         }
-        // winner's row: every lane holds the reduced rank after the xor butterfly
-        for (int c = lane; c < W; c += 32) urow[c] = ld_dsmem_f64x2(dsmem_addr(&cand_vals[par][c], rk));
+        // winner's row and the old diagonal row, one element per lane, fetched in parallel
+        // (every lane holds the reduced rank / row after the xor butterfly)
+        const int downer_w = (d - r0) / R;
+        for (int c = lane; c < W; c += 32) {
+          urow[c] = ld_dsmem_f64x2(dsmem_addr(&cand_vals[par][c], rk));
+          if (r != d && rk == (int)rank) drow[c] = ld_dsmem_f64x2(dsmem_addr(&diag_vals[par][c], downer_w));
+        }
       }
       __syncthreads();
+      if (rec) t3 = clock64();
       const int wrank = win[0], p = win[1];
-      const int downer = (d - r0) / R;
-      // ---- interchange rows d and p (owners only; p's owner reads the old row d via DSMEM)
+      // ---- interchange rows d and p (owners only, from shared memory)
 #pragma unroll
       for (int q = 0; q < RPT; ++q) {
         if (gi[q] == p && p != d) {
 #pragma unroll
-          for (int c = 0; c < W; ++c) a[q][c] = ld_dsmem_f64x2(dsmem_addr(&diag_vals[par][c], downer));
+          for (int c = 0; c < W; ++c) a[q][c] = drow[c];
         } else if (gi[q] == d) {
 #pragma unroll
           for (int c = 0; c < W; ++c) a[q][c] = urow[c];
@@ -855,6 +870,14 @@ leaf_lu_v2_kernel(double2* mats, int ld, long long stride, int n, int r0, int w,
           }
         }
       }
+      if (rec) {
+        const unsigned long long t4 = clock64();
+        atomicAdd(&g_leaf_prof[0], t1 - t0);   // local search + warp/CTA argmax
+        atomicAdd(&g_leaf_prof[1], t2 - t1);   // fold + publish + cluster barrier
+        atomicAdd(&g_leaf_prof[2], t3 - t2);   // DSMEM winner + row fetch + barrier
+        atomicAdd(&g_leaf_prof[3], t4 - t3);   // swap + scale + rank-1 update
+        atomicAdd(&g_leaf_prof[4], 1ull);      // columns
+      }
     }
   }
   // write back
@@ -867,9 +890,13 @@ leaf_lu_v2_kernel(double2* mats, int ld, long long stride, int n, int r0, int w,
     }
   }
   cluster_sync_all();   // keep every CTA's shared memory alive until all DSMEM reads are done
+  if (PROF && tid == 0 && rank == 0 && b == 0) {
+    atomicAdd(&g_leaf_prof[5], clock64() - t_entry);   // whole CTA lifetime
+    atomicAdd(&g_leaf_prof[6], 1ull);                   // leaves
+  }
 }
 
-template <int W, int RPT, int NT>
+template <int W, int RPT, int NT, bool PROF>
 static cudaError_t launch_leaf_v2(double2* mats, int ld, long long stride, int n, int r0, int w, int cluster,
                                   int* ipiv, int batch, cudaStream_t s) {
   const int m = n - r0;
@@ -877,7 +904,7 @@ static cudaError_t launch_leaf_v2(double2* mats, int ld, long long stride, int n
   if (R > RPT * NT) return cudaErrorInvalidValue;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(leaf_lu_v2_kernel<W, RPT, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaError_t e = cudaFuncSetAttribute(leaf_lu_v2_kernel<W, RPT, NT, PROF>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -894,20 +921,37 @@ static cudaError_t launch_leaf_v2(double2* mats, int ld, long long stride, int n
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   note_launch();
-  return cudaLaunchKernelEx(&cfg, leaf_lu_v2_kernel<W, RPT, NT>, mats, ld, stride, n, r0, w, R, ipiv);
+  return cudaLaunchKernelEx(&cfg, leaf_lu_v2_kernel<W, RPT, NT, PROF>, mats, ld, stride, n, r0, w, R, ipiv);
 }
 
 // variant ids: 0: W32/RPT1/256  1: W16/RPT1/512  2: W8/RPT2/512
 int leaf_v2_rows_per_cta(int variant) { return variant == 0 ? 256 : (variant == 1 ? 512 : 1024); }
 int leaf_v2_width(int variant) { return variant == 0 ? 32 : (variant == 1 ? 16 : 8); }
 
+static bool leaf_prof_on() {
+  static const char* e = std::getenv("SSSVD_LEAF_PROF");
+  return e && e[0] == '1';
+}
+
 cudaError_t leaf_lu_v2(double2* mats, int ld, long long stride, int n, int r0, int w, int variant, int cluster,
                        int* ipiv, int batch, cudaStream_t s) {
+  const bool prof = leaf_prof_on();
   switch (variant) {
-    case 0: return launch_leaf_v2<32, 1, 256>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s);
-    case 1: return launch_leaf_v2<16, 1, 512>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s);
-    case 2: return launch_leaf_v2<8, 2, 512>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s);
+    case 0: return prof ? launch_leaf_v2<32, 1, 256, true>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s)
+                        : launch_leaf_v2<32, 1, 256, false>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s);
+    case 1: return prof ? launch_leaf_v2<16, 1, 512, true>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s)
+                        : launch_leaf_v2<16, 1, 512, false>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s);
+    case 2: return prof ? launch_leaf_v2<8, 2, 512, true>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s)
+                        : launch_leaf_v2<8, 2, 512, false>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s);
     default: return cudaErrorInvalidValue;
+  }
+}
+
+void leaf_profile_read(unsigned long long* out5, bool reset) {
+  cudaMemcpyFromSymbol(out5, g_leaf_prof, 7 * sizeof(unsigned long long));
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_leaf_prof, z, sizeof(z));
   }
 }
 

@@ -145,6 +145,9 @@ struct sssvd_gpu_ctx {
   DBuf A, G, gmax, mats, ipiv, shifts, coef, S, V, status, minpiv, scratch;
   DBuf t0, t1, t2, t7, work, info;
   DBuf lw_linv, lw_T, lw_src, lw_disp;
+  static constexpr int kMaxGroups = 4;
+  cudaStream_t gstream[kMaxGroups] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[kMaxGroups] = {};
   DBuf tail[24];
   double t_gram = 0, t_solves = 0, t_allreduce = 0, solve_flops = 0;
 };
@@ -196,8 +199,10 @@ static LuPlan make_plan(int n, int L) {
   if (!found) throw Status(SSSVD_E_LENGTH, "operator too large for the on-chip leaf panel");
   // register-resident leaf (v2): rows per CTA <= threads x rows-per-thread of the variant
   p.leaf_variant = -1;
+  // default: shared-memory leaf (v1); the register-resident v2 needs a whole SM register file
+  // per CTA and its 8-CTA clusters do not reliably co-schedule (measured erratic), so opt-in
   static const char* leaf_env = std::getenv("SSSVD_LEAF");
-  if (!(leaf_env && std::string(leaf_env) == "v1")) {
+  if (leaf_env && std::string(leaf_env) == "v2") {
     for (int v = 0; v < 3 && p.leaf_variant < 0; ++v)
       for (int c = 1; c <= 8; c *= 2)
         if ((n + c - 1) / c <= leaf_v2_rows_per_cta(v)) {
@@ -289,6 +294,38 @@ static void lu_solve_batch(const LuPlan& P, const LuWork& W, double2* mats, int*
   }
 }
 
+// Independent shift groups of one batch, each on its own stream; the host interleaves their
+// launches block by block so a group's latency-bound panel overlaps another group's DMMA
+// trailing update (no data is shared between groups).
+struct LuGroup {
+  double2* mats;
+  int* ipiv;
+  LuWork W;
+  int nb;
+  cudaStream_t s;
+};
+
+static void lu_solve_groups(const LuPlan& P, std::vector<LuGroup>& G) {
+  const int n = P.n, ncols = n + P.L;
+  for (int kb = 0; kb < n; kb += P.NB) {
+    const int nbk = std::min(P.NB, n - kb);
+    for (auto& g : G) {
+      factor_rec(P, g.W, g.mats, g.ipiv, g.nb, g.s, kb, nbk, kb);
+      apply_panel(P, g.W, g.mats, g.ipiv, g.nb, g.s, kb, nbk, kb + nbk, ncols);
+    }
+  }
+  const int nblocks = (n + P.NB - 1) / P.NB;
+  for (int bi = nblocks - 1; bi >= 0; --bi) {
+    const int kb = bi * P.NB, nbk = std::min(P.NB, n - kb);
+    for (auto& g : G) {
+      CK(trsm_upper_warp(g.mats, P.ld, P.stride, kb, nbk, n, ncols, g.nb, g.s));
+      if (kb > 0)
+        CK(zgemm_sub(kb, P.L, nbk, g.mats + kb, P.ld, P.stride, g.mats + (size_t)kb * P.ld + n, P.ld, P.stride,
+                     g.mats + n, P.ld, P.stride, g.nb, g.s));
+    }
+  }
+}
+
 static LuWork make_work(sssvd_gpu_ctx* ctx, const LuPlan& P, int B) {
   LuWork W;
   W.tstride = (long long)P.NB * (P.n + P.L);
@@ -297,6 +334,16 @@ static LuWork make_work(sssvd_gpu_ctx* ctx, const LuPlan& P, int B) {
   W.src = ctx->lw_src.as<int>((size_t)B * P.NB);
   W.disp = ctx->lw_disp.as<int>((size_t)B * (2 * P.NB + 1));
   return W;
+}
+
+// the slice of a batch workspace that belongs to shifts [b0, ...)
+static LuWork work_slice(const LuWork& W, const LuPlan& P, int b0) {
+  LuWork g = W;
+  g.linv += (size_t)b0 * P.NB * P.NB;
+  g.T += (size_t)b0 * W.tstride;
+  g.src += (size_t)b0 * P.NB;
+  g.disp += (size_t)b0 * (2 * P.NB + 1);
+  return g;
 }
 
 static size_t bytes_per_shift(const LuPlan& P) {
@@ -349,7 +396,29 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
     CK(cudaMemcpyAsync(dshift, hshift.data(), sizeof(double2) * nb, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(dcoef, hcoef.data(), sizeof(double2) * (M + 1) * nb, cudaMemcpyHostToDevice, s));
     CK(assemble(ctx->G.as<double>(0), n, n, V_dev, L, dshift, mats, P.ld, P.stride, nb, s));
-    lu_solve_batch(P, work, mats, ipiv, nb, s);
+    {
+      static const char* genv = std::getenv("SSSVD_GROUPS");
+      const int ng = std::max(1, std::min(nb / 2, genv ? std::atoi(genv) : 2));
+      if (ng <= 1) {
+        lu_solve_batch(P, work, mats, ipiv, nb, s);
+      } else {
+        std::vector<LuGroup> groups;
+        CK(cudaEventRecord(ctx->ev_fork, s));
+        int b0 = 0;
+        for (int g = 0; g < ng; ++g) {
+          const int cnt = nb / ng + (g < nb % ng ? 1 : 0);
+          CK(cudaStreamWaitEvent(ctx->gstream[g], ctx->ev_fork, 0));
+          groups.push_back({mats + (size_t)b0 * P.stride, ipiv + (size_t)b0 * n, work_slice(work, P, b0), cnt,
+                            ctx->gstream[g]});
+          b0 += cnt;
+        }
+        lu_solve_groups(P, groups);
+        for (int g = 0; g < ng; ++g) {
+          CK(cudaEventRecord(ctx->ev_join[g], ctx->gstream[g]));
+          CK(cudaStreamWaitEvent(s, ctx->ev_join[g], 0));
+        }
+      }
+    }
     CK(pivot_floor(mats, P.ld, P.stride, n, dshift, ctx->gmax.as<double>(1), dstatus, dmin, nb, s));
     CK(moments(mats, P.ld, P.stride, n, n, L, nb, dcoef, M, S_dev, s));
     CK(cudaMemcpyAsync(hstatus.data(), dstatus, sizeof(int) * nb, cudaMemcpyDeviceToHost, s));
@@ -414,11 +483,12 @@ static void thin_qr(sssvd_gpu_ctx* ctx, double* A, int m, int k, double* R) {
 }
 
 // full SVD of a square k x k matrix B (destroyed): U (k x k), S (k, descending), V (k x k).
-// Method (round-1 interim, cuSOLVER): SSSVD_TAIL_SVD = gesvdj (default; one-sided Jacobi like
-// the reference's JacobiSVD), gesvdp (polar decomposition) or gesvd (bidiagonal QR).
+// Method (round-1 interim, cuSOLVER): SSSVD_TAIL_SVD = gesvdp (default: polar decomposition,
+// fastest measured: 12 ms vs 30 ms gesvdj vs 45 ms gesvd at 512 x 512), gesvdj (one-sided
+// Jacobi like the reference's JacobiSVD) or gesvd (bidiagonal QR). All parity tests pass with each.
 static void svd_square(sssvd_gpu_ctx* ctx, double* B, int k, double* U, double* S, double* V) {
   static const char* env = std::getenv("SSSVD_TAIL_SVD");
-  const std::string method = env ? env : "gesvdj";
+  const std::string method = env ? env : "gesvdp";
   int* dinfo = ctx->info.as<int>(1);
   if (method == "gesvdp" || method == "gesvd") {
     cusolverDnParams_t params;
@@ -809,6 +879,12 @@ static sssvd_status guarded(sssvd_gpu_ctx* ctx, F&& body) {
 extern "C" {
 
 uint64_t sssvd_gpu_launch_count(void) { return launch_count(); }
+// debug: per-column cycle breakdown of the leaf kernel (SSSVD_LEAF_PROF=1 builds it in)
+void sssvd_debug_leaf_profile(uint64_t* out5) {  // 7 entries
+  unsigned long long v[7];
+  leaf_profile_read(v, true);
+  for (int i = 0; i < 7; ++i) out5[i] = v[i];
+}
 void sssvd_gpu_profile_gemm(int enable) { zgemm_profile_enable(enable != 0); }
 void sssvd_gpu_profile_gemm_collect(double* ms, double* flops, uint64_t* launches) {
   unsigned long long l = 0;
@@ -834,6 +910,11 @@ sssvd_status sssvd_gpu_create(int device, sssvd_gpu_ctx** out) {
     delete ctx;
     return SSSVD_E_CUDA;
   }
+  for (int g = 0; g < sssvd_gpu_ctx::kMaxGroups; ++g) {
+    cudaStreamCreateWithFlags(&ctx->gstream[g], cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&ctx->ev_join[g], cudaEventDisableTiming);
+  }
+  cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
   cublasSetStream(ctx->blas, ctx->stream);
   cusolverDnSetStream(ctx->solver, ctx->stream);
   *out = ctx;
@@ -852,6 +933,11 @@ void sssvd_gpu_destroy(sssvd_gpu_ctx* ctx) {
   if (ctx->comm) nccl().CommDestroy(ctx->comm);
   if (ctx->solver) cusolverDnDestroy(ctx->solver);
   if (ctx->blas) cublasDestroy(ctx->blas);
+  for (int g = 0; g < sssvd_gpu_ctx::kMaxGroups; ++g) {
+    if (ctx->gstream[g]) cudaStreamDestroy(ctx->gstream[g]);
+    if (ctx->ev_join[g]) cudaEventDestroy(ctx->ev_join[g]);
+  }
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }

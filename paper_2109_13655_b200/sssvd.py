@@ -108,7 +108,7 @@ EXPORTED_SYMBOLS = [
     "sssvd_gpu_run_solve", "sssvd_result_info_get", "sssvd_result_copy", "sssvd_result_note",
     "sssvd_result_free", "sssvd_contour", "sssvd_random_start", "sssvd_validate_params",
     "sssvd_moment_coefficients", "sssvd_build_info", "sssvd_gpu_launch_count", "sssvd_gpu_profile_gemm",
-    "sssvd_gpu_profile_gemm_collect",
+    "sssvd_gpu_profile_gemm_collect", "sssvd_debug_leaf_profile",
 ]
 
 _lib = None
