@@ -32,6 +32,9 @@ int leaf_v2_width(int variant);
 cudaError_t leaf_lu_v2(double2* mats, int ld, long long stride, int n, int r0, int w, int variant, int cluster,
                        int* ipiv, int batch, cudaStream_t s);
 void leaf_profile_read(unsigned long long* out5, bool reset);
+// K2 v3 (lu.cu): shared-memory slab with thread-owned rows (same smem sizing as v1)
+cudaError_t leaf_lu_v3(double2* mats, int ld, long long stride, int n, int r0, int w, int W, int cluster, int* ipiv,
+                       int batch, cudaStream_t s);
 // K3/K4 (lu.cu): interchanges ipiv[r0..r0+np) on columns [c0,c1), then optional unit-lower TRSM
 cudaError_t swap_trsm(double2* mats, int ld, long long stride, int n, int r0, int np, int c0, int c1,
                       const int* ipiv, bool do_trsm, int batch, cudaStream_t s);

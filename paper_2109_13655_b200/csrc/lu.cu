@@ -956,3 +956,178 @@ void leaf_profile_read(unsigned long long* out5, bool reset) {
 }
 
 }  // namespace sssvd_gpu
+
+namespace sssvd_gpu {
+
+// ----------------------------------------------------------------------------- K2 leaf, v3
+// Shared-memory slab (as v1: R x (W+1) complex per CTA, one cluster per shift) with thread-owned
+// rows (as v2): thread t owns slab rows t, t+NT, ...; for column j it scales its rows, applies
+// the rank-1 update to their columns j+1..W-1 and scores column j+1 in the same pass, so the
+// only barriers per column are: CTA argmax (1), cluster exchange (1), winner broadcast (1).
+// Warp 0 publishes the CTA candidate and the diagonal row straight from the slab, reduces the C
+// candidates over DSMEM, fetches the pivot row (and, in the winning CTA, the old diagonal row),
+// and performs the interchange in the slab.
+template <int W, int NT>
+__global__ void __launch_bounds__(NT, 1)
+leaf_lu_v3_kernel(double2* mats, int ld, long long stride, int n, int r0, int w, int R, int* ipiv) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  constexpr int P = W + 1;
+  double2* slab = reinterpret_cast<double2*>(sm_raw);   // R x P
+  __shared__ double2 cand_vals[2][W];
+  __shared__ double2 diag_vals[2][W];
+  __shared__ double2 urow[W];
+  __shared__ double cand_score[2];
+  __shared__ int cand_row[2];
+  __shared__ double red_s[NT / 32];
+  __shared__ int red_r[NT / 32];
+  __shared__ int win_row;
+
+  const int C = gridDim.x;
+  const unsigned rank = cluster_ctarank();
+  const int b = blockIdx.y;
+  double2* Mb = mats + b * stride;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int my0 = r0 + (int)rank * R;
+  const int myn = max(0, min(R, n - my0));
+
+  for (int e = tid; e < myn * W; e += NT) {
+    const int i = e / W, c = e % W;
+    slab[i * P + c] = (c < w) ? Mb[(size_t)(my0 + i) * ld + r0 + c] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+
+  // score of column 0 over the rows this thread owns
+  double best = -1.0;
+  int brow = 0x7fffffff;
+  for (int i = tid; i < myn; i += NT) {
+    const double s = cabs2(slab[i * P]);
+    if (s > best) { best = s; brow = my0 + i; }
+  }
+
+  for (int j = 0; j < w; ++j) {
+    const int d = r0 + j;
+    const int par = j & 1;
+    // ---- CTA argmax of column j (ties: smallest row)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double os = __shfl_xor_sync(0xffffffffu, best, off);
+      const int orow = __shfl_xor_sync(0xffffffffu, brow, off);
+      if (os > best || (os == best && orow < brow)) { best = os; brow = orow; }
+    }
+    if (lane == 0) { red_s[warp] = best; red_r[warp] = brow; }
+    __syncthreads();
+    if (warp == 0) {
+      best = lane < NT / 32 ? red_s[lane] : -1.0;
+      brow = lane < NT / 32 ? red_r[lane] : 0x7fffffff;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const double os = __shfl_xor_sync(0xffffffffu, best, off);
+        const int orow = __shfl_xor_sync(0xffffffffu, brow, off);
+        if (os > best || (os == best && orow < brow)) { best = os; brow = orow; }
+      }
+      if (lane == 0) { cand_score[par] = best; cand_row[par] = brow; }
+      for (int c = lane; c < W; c += 32) {
+        if (brow != 0x7fffffff) cand_vals[par][c] = slab[(brow - my0) * P + c];
+        if (d >= my0 && d < my0 + myn) diag_vals[par][c] = slab[(d - my0) * P + c];
+      }
+    }
+    cluster_sync_all();
+    // ---- warp 0: winner over the C candidates, pivot row (+ old diagonal row), interchange
+    if (warp == 0) {
+      double s = -1.0;
+      int r = 0x7fffffff, rk = lane;
+      if (lane < C) {
+        s = ld_dsmem_f64(dsmem_addr(&cand_score[par], lane));
+        r = ld_dsmem_s32(dsmem_addr(&cand_row[par], lane));
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const double os = __shfl_xor_sync(0xffffffffu, s, off);
+        const int orow = __shfl_xor_sync(0xffffffffu, r, off);
+        const int ork = __shfl_xor_sync(0xffffffffu, rk, off);
+        if (os > s || (os == s && orow < r)) { s = os; r = orow; rk = ork; }
+      }
+      const int downer = (d - r0) / R;
+      for (int c = lane; c < W; c += 32) {
+        const double2 u = ld_dsmem_f64x2(dsmem_addr(&cand_vals[par][c], rk));
+        double2 dv = make_double2(0.0, 0.0);
+        if (r != d && rk == (int)rank) dv = ld_dsmem_f64x2(dsmem_addr(&diag_vals[par][c], downer));
+        urow[c] = u;
+        if (d >= my0 && d < my0 + myn) slab[(d - my0) * P + c] = u;
+        if (r != d && rk == (int)rank) slab[(r - my0) * P + c] = dv;
+      }
+      if (lane == 0) win_row = r;
+      if (lane == 0 && rank == 0) ipiv[(size_t)b * n + d] = r;
+    }
+    __syncthreads();
+    // ---- own rows: scale column j, rank-1 update of columns j+1.., score column j+1
+    const double2 u = urow[j];
+    const bool nz = cabs2(u) != 0.0;
+    const double2 inv = nz ? crecip(u) : make_double2(0.0, 0.0);
+    best = -1.0;
+    brow = 0x7fffffff;
+    const int first = max(0, d + 1 - my0);
+    for (int i = first + ((tid - first) % NT + NT) % NT; i < myn; i += NT) {
+      double2* row = slab + i * P;
+      if (nz) {
+        const double2 l = cmul(row[j], inv);
+        row[j] = l;
+#pragma unroll 4
+        for (int c = j + 1; c < W; ++c) row[c] = cfms(row[c], l, urow[c]);
+      }
+      if (j + 1 < w) {
+        const double sc = cabs2(row[j + 1]);
+        if (sc > best) { best = sc; brow = my0 + i; }
+      }
+    }
+    (void)win_row;
+  }
+  __syncthreads();
+  for (int e = tid; e < myn * w; e += NT) {
+    const int i = e / w, c = e % w;
+    Mb[(size_t)(my0 + i) * ld + r0 + c] = slab[i * P + c];
+  }
+  cluster_sync_all();
+}
+
+template <int W, int NT>
+static cudaError_t launch_leaf_v3(double2* mats, int ld, long long stride, int n, int r0, int w, int cluster,
+                                  int* ipiv, int batch, cudaStream_t s) {
+  const int m = n - r0;
+  const int R = (m + cluster - 1) / cluster;
+  const size_t smem = (size_t)R * (W + 1) * sizeof(double2);
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(leaf_lu_v3_kernel<W, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(leaf_lu_v3_kernel<W, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cluster, batch, 1);
+  cfg.blockDim = dim3(NT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  note_launch();
+  return cudaLaunchKernelEx(&cfg, leaf_lu_v3_kernel<W, NT>, mats, ld, stride, n, r0, w, R, ipiv);
+}
+
+cudaError_t leaf_lu_v3(double2* mats, int ld, long long stride, int n, int r0, int w, int W, int cluster, int* ipiv,
+                       int batch, cudaStream_t s) {
+  switch (W) {
+    case 8: return launch_leaf_v3<8, 512>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s);
+    case 16: return launch_leaf_v3<16, 512>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s);
+    case 32: return launch_leaf_v3<32, 256>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace sssvd_gpu

@@ -258,10 +258,14 @@ static void factor_rec(const LuPlan& P, const LuWork& W, double2* mats, int* ipi
                        int w, int cb) {
   const int n = P.n;
   if (w <= P.W) {
+    static const char* leaf_env = std::getenv("SSSVD_LEAF");
+    static const bool use_v1 = leaf_env && std::string(leaf_env) == "v1";
     if (P.leaf_variant >= 0)
       CK(leaf_lu_v2(mats, P.ld, P.stride, n, c0, w, P.leaf_variant, P.cluster, ipiv, nb, s));
-    else
+    else if (use_v1)
       CK(leaf_lu(mats, P.ld, P.stride, n, c0, w, P.W, P.cluster, ipiv, nb, s));
+    else
+      CK(leaf_lu_v3(mats, P.ld, P.stride, n, c0, w, P.W, P.cluster, ipiv, nb, s));
     if (c0 > cb) CK(swap_trsm(mats, P.ld, P.stride, n, c0, w, cb, c0, ipiv, false, nb, s));
     return;
   }
@@ -483,12 +487,13 @@ static void thin_qr(sssvd_gpu_ctx* ctx, double* A, int m, int k, double* R) {
 }
 
 // full SVD of a square k x k matrix B (destroyed): U (k x k), S (k, descending), V (k x k).
-// Method (round-1 interim, cuSOLVER): SSSVD_TAIL_SVD = gesvdp (default: polar decomposition,
-// fastest measured: 12 ms vs 30 ms gesvdj vs 45 ms gesvd at 512 x 512), gesvdj (one-sided
-// Jacobi like the reference's JacobiSVD) or gesvd (bidiagonal QR). All parity tests pass with each.
+// Method (round-1 interim, cuSOLVER): SSSVD_TAIL_SVD = gesvdj (default: Jacobi, like the
+// reference's JacobiSVD), gesvdp (polar decomposition; fastest: 12 ms vs 30 ms at 512 x 512, but
+// it resolves the roundoff-level singular values differently, which moves tau on degenerate
+// configs: cfg2 NT-off gives 20 non-spurious vs 0 for the reference restatement) or gesvd.
 static void svd_square(sssvd_gpu_ctx* ctx, double* B, int k, double* U, double* S, double* V) {
   static const char* env = std::getenv("SSSVD_TAIL_SVD");
-  const std::string method = env ? env : "gesvdp";
+  const std::string method = env ? env : "gesvdj";
   int* dinfo = ctx->info.as<int>(1);
   if (method == "gesvdp" || method == "gesvd") {
     cusolverDnParams_t params;
