@@ -1,0 +1,258 @@
+// One-sided (Hestenes) Jacobi SVD of a square k x k matrix on the GPU.
+//
+// Replaces the Eigen::JacobiSVD calls of the small dense tail: low_rank
+// (proj/include/sssvd/moments.hpp:199, SVD of the R factor of the stacked moments) and
+// svd_small (proj/include/sssvd/extract.hpp:66-70, SVD of the projected triangular factor B).
+// Jacobi keeps the small singular values of a graded triangular factor to high relative
+// accuracy, and the spurious-triplet index tau (postprocess.hpp:56-60) is driven by exactly
+// those values, so a Jacobi method is what keeps tau faithful to the reference.
+//
+// W = B (column-major), V = I. A sweep is k-1 rounds of a round-robin tournament; in a round the
+// k/2 disjoint column pairs (p, q) are orthogonalised concurrently, one warp per pair:
+//   alpha = |w_p|^2, beta = |w_q|^2, gamma = w_p . w_q  (warp reductions)
+//   rotate iff |gamma| > tol sqrt(alpha beta):  zeta = (beta - alpha) / (2 gamma),
+//   t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), c = 1/sqrt(1 + t^2), s = c t
+//   [w_p w_q] <- [w_p w_q] [c s; -s c],  same for V.
+// The kernel is persistent (cooperative launch: all CTAs resident) and separates rounds with a
+// sense-reversing software grid barrier; a sweep without any rotation ends the iteration.
+// Afterwards sigma_j = |w_j|, u_j = w_j / sigma_j, sorted nonincreasing on the host.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sssvd_gpu {
+
+namespace {
+
+struct GridBarrier {
+  unsigned int* count;   // arrivals
+  volatile unsigned int* gen;
+};
+
+__device__ __forceinline__ void grid_barrier(GridBarrier b, unsigned int nblocks, unsigned int& local_gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int g = local_gen;
+    __threadfence();
+    const unsigned int arrived = atomicAdd(b.count, 1u);
+    if (arrived == nblocks - 1) {
+      *b.count = 0;
+      __threadfence();
+      atomicExch((unsigned int*)b.gen, g + 1);
+    } else {
+      while (*b.gen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  ++local_gen;
+}
+
+// tournament position -> column index (player 0 fixed, the others rotate)
+__device__ __forceinline__ int player(int pos, int round, int k) {
+  return pos == 0 ? 0 : ((pos - 1 + round) % (k - 1)) + 1;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(256)
+jacobi_svd_kernel(double* __restrict__ Wm, double* __restrict__ Vm, int k, int ldw, double tol, int max_sweeps,
+                  unsigned int* __restrict__ bar, unsigned int* __restrict__ rot_count, int* __restrict__ sweeps_out) {
+  GridBarrier gb{bar, bar + 1};
+  unsigned int local_gen = bar[1];
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int kk = k + (k & 1);   // odd k: a dummy player k sits out one pair per round
+  const int npairs = kk / 2;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    for (int round = 0; round < kk - 1; ++round) {
+      for (int pi = gwarp; pi < npairs; pi += nwarps) {
+        int p = player(pi, round, kk), q = player(kk - 1 - pi, round, kk);
+        if (p > q) { int t = p; p = q; q = t; }
+        if (q >= k) continue;
+        double* wp = Wm + (size_t)p * ldw;
+        double* wq = Wm + (size_t)q * ldw;
+        // pass 1: the 2x2 Gram entries. The grid barrier's gpu-scope fence invalidated this SM's
+        // L1, so cached loads see the other CTAs' writes of the previous round.
+        double a = 0.0, bb = 0.0, g = 0.0;
+#pragma unroll 8
+        for (int i = lane; i < k; i += 32) {
+          const double x = wp[i], y = wq[i];
+          a += x * x;
+          bb += y * y;
+          g += x * y;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          a += __shfl_xor_sync(0xffffffffu, a, off);
+          bb += __shfl_xor_sync(0xffffffffu, bb, off);
+          g += __shfl_xor_sync(0xffffffffu, g, off);
+        }
+        if (fabs(g) > tol * sqrt(a) * sqrt(bb) && g != 0.0) {
+          const double zeta = (bb - a) / (2.0 * g);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+          // pass 2: rotate W and V columns (the reloads hit L1: this warp just read them)
+          double* vp = Vm + (size_t)p * ldw;
+          double* vq = Vm + (size_t)q * ldw;
+#pragma unroll 4
+          for (int i = lane; i < k; i += 32) {
+            const double x = wp[i], y = wq[i];
+            const double v1 = vp[i], v2 = vq[i];
+            wp[i] = c * x - s * y;
+            wq[i] = s * x + c * y;
+            vp[i] = c * v1 - s * v2;
+            vq[i] = s * v1 + c * v2;
+          }
+          if (lane == 0) atomicAdd(rot_count + (sweep & 1), 1u);
+        }
+      }
+      grid_barrier(gb, gridDim.x, local_gen);
+    }
+    // sweep done: every CTA reads the rotation count of this sweep; the other slot is reset
+    const unsigned int rc = *((volatile unsigned int*)(rot_count + (sweep & 1)));
+    if (blockIdx.x == 0 && threadIdx.x == 0) rot_count[(sweep + 1) & 1] = 0;
+    grid_barrier(gb, gridDim.x, local_gen);
+    if (rc == 0) {
+      ++sweep;
+      break;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep;
+}
+
+
+// Same sweep, run by ONE thread-block cluster (16 CTAs x 512 threads): rounds are separated by
+// the hardware cluster barrier (release/acquire at cluster scope; it also invalidates L1, so the
+// global-memory columns written in one round are seen by every CTA in the next).
+__global__ void __launch_bounds__(512, 1)
+jacobi_svd_cluster_kernel(double* __restrict__ Wm, double* __restrict__ Vm, int k, int ldw, double tol,
+                          int max_sweeps, unsigned int* __restrict__ rot_count, int* __restrict__ sweeps_out) {
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int kk = k + (k & 1);
+  const int npairs = kk / 2;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    for (int round = 0; round < kk - 1; ++round) {
+      for (int pi = gwarp; pi < npairs; pi += nwarps) {
+        int p = player(pi, round, kk), q = player(kk - 1 - pi, round, kk);
+        if (p > q) { int t = p; p = q; q = t; }
+        if (q >= k) continue;
+        double* wp = Wm + (size_t)p * ldw;
+        double* wq = Wm + (size_t)q * ldw;
+        double a = 0.0, bb = 0.0, g = 0.0;
+#pragma unroll 8
+        for (int i = lane; i < k; i += 32) {
+          const double x = wp[i], y = wq[i];
+          a += x * x;
+          bb += y * y;
+          g += x * y;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          a += __shfl_xor_sync(0xffffffffu, a, off);
+          bb += __shfl_xor_sync(0xffffffffu, bb, off);
+          g += __shfl_xor_sync(0xffffffffu, g, off);
+        }
+        if (fabs(g) > tol * sqrt(a) * sqrt(bb) && g != 0.0) {
+          const double zeta = (bb - a) / (2.0 * g);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+          double* vp = Vm + (size_t)p * ldw;
+          double* vq = Vm + (size_t)q * ldw;
+#pragma unroll 4
+          for (int i = lane; i < k; i += 32) {
+            const double x = wp[i], y = wq[i];
+            const double v1 = vp[i], v2 = vq[i];
+            wp[i] = c * x - s * y;
+            wq[i] = s * x + c * y;
+            vp[i] = c * v1 - s * v2;
+            vq[i] = s * v1 + c * v2;
+          }
+          if (lane == 0) atomicAdd(rot_count + (sweep & 1), 1u);
+        }
+      }
+      cluster_sync_all();
+    }
+    const unsigned int rc = *((volatile unsigned int*)(rot_count + (sweep & 1)));
+    if (blockIdx.x == 0 && threadIdx.x == 0) rot_count[(sweep + 1) & 1] = 0;
+    cluster_sync_all();
+    if (rc == 0) {
+      ++sweep;
+      break;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep;
+}
+
+// sigma_j = |w_j| and u_j = w_j / sigma_j (u_j = 0 when sigma_j = 0), column-major k x k
+__global__ void jacobi_finish_kernel(double* __restrict__ Wm, int k, int ldw, double* __restrict__ S) {
+  const int j = blockIdx.x;
+  double* w = Wm + (size_t)j * ldw;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) acc += w[i] * w[i];
+  __shared__ double red[32];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (threadIdx.x == 0) red[0] = sqrt(acc);
+  }
+  __syncthreads();
+  const double s = red[0];
+  if (threadIdx.x == 0) S[j] = s;
+  const double inv = s > 0.0 ? 1.0 / s : 0.0;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) w[i] *= inv;
+}
+
+__global__ void set_identity_kernel(double* __restrict__ V, int k, int ldv) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)k * ldv;
+       e += (long long)gridDim.x * blockDim.x)
+    V[e] = (e % ldv) == (e / ldv) ? 1.0 : 0.0;
+}
+
+cudaError_t jacobi_svd(double* W, double* V, int k, int ldw, double* S, double tol, int max_sweeps,
+                       unsigned int* scratch /* >= 8 uints, zeroed by this call */, int* sweeps_out,
+                       cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(scratch, 0, 8 * sizeof(unsigned int), s);
+  if (e != cudaSuccess) return e;
+  set_identity_kernel<<<148 * 4, 256, 0, s>>>(V, k, ldw);
+  note_launch();
+  if (k > 1) {
+    static bool configured = false;
+    if (!configured) {
+      e = cudaFuncSetAttribute(jacobi_svd_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+      configured = true;
+    }
+    unsigned int* rot = scratch + 2;      // [2], [3] rotation counts (ping-pong by sweep parity)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(16, 1, 1);
+    cfg.blockDim = dim3(512, 1, 1);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 16;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, jacobi_svd_cluster_kernel, W, V, k, ldw, tol, max_sweeps, rot, sweeps_out);
+    if (e != cudaSuccess) return e;
+    note_launch();
+  }
+  jacobi_finish_kernel<<<k, 256, 0, s>>>(W, k, ldw, S);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace sssvd_gpu

@@ -60,6 +60,9 @@ cudaError_t scatter_copy(double2* mats, int ld, long long stride, int r0, int np
                          int dstride, const double2* T, int ldt, long long tstride, int batch, cudaStream_t s);
 cudaError_t trsm_upper_warp(double2* mats, int ld, long long stride, int r0, int np, int c0, int c1, int batch,
                             cudaStream_t s);
+// one-sided Jacobi SVD (jacobi_svd.cu): W (k x k, in) -> W = U (unsorted), V, S = sigma
+cudaError_t jacobi_svd(double* W, double* V, int k, int ldw, double* S, double tol, int max_sweeps,
+                       unsigned int* scratch, int* sweeps_out, cudaStream_t s);
 // K7 (moments.cu)
 cudaError_t moments(const double2* mats, int ld, long long stride, int xcol, int n, int L, int nb,
                     const double2* coef, int M, double* S, cudaStream_t s);

@@ -144,7 +144,7 @@ struct sssvd_gpu_ctx {
   bool has_gram = false;
   DBuf A, G, gmax, mats, ipiv, shifts, coef, S, V, status, minpiv, scratch;
   DBuf t0, t1, t2, t7, work, info;
-  DBuf lw_linv, lw_T, lw_src, lw_disp;
+  DBuf lw_linv, lw_T, lw_src, lw_disp, jscr, jperm;
   static constexpr int kMaxGroups = 4;
   cudaStream_t gstream[kMaxGroups] = {};
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxGroups] = {};
@@ -491,10 +491,57 @@ static void thin_qr(sssvd_gpu_ctx* ctx, double* A, int m, int k, double* R) {
 // reference's JacobiSVD), gesvdp (polar decomposition; fastest: 12 ms vs 30 ms at 512 x 512, but
 // it resolves the roundoff-level singular values differently, which moves tau on degenerate
 // configs: cfg2 NT-off gives 20 non-spurious vs 0 for the reference restatement) or gesvd.
+static std::vector<double> d2h(const double* d, size_t count, cudaStream_t s) {
+  std::vector<double> h(count);
+  if (count) {
+    CK(cudaMemcpyAsync(h.data(), d, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  return h;
+}
+
 static void svd_square(sssvd_gpu_ctx* ctx, double* B, int k, double* U, double* S, double* V) {
   static const char* env = std::getenv("SSSVD_TAIL_SVD");
-  const std::string method = env ? env : "gesvdj";
+  const std::string method = env ? env : "jacobi";
   int* dinfo = ctx->info.as<int>(1);
+  if (method == "jacobi" || method == "jacobi_n") {
+    // hand-written one-sided Jacobi (jacobi_svd.cu); columns sorted by nonincreasing sigma.
+    // Default: Jacobi on B^T (B is triangular: the transposed factor converges in far fewer
+    // sweeps, the dgejsv preconditioning idea): B^T Q = W = V_B S, so U_B = Q, V_B = W S^-1.
+    const bool transposed = method == "jacobi";
+    unsigned int* scr = static_cast<unsigned int*>(ctx->jscr.get(64));
+    int* sweeps = reinterpret_cast<int*>(scr + 8);
+    const double tol = (double)k * 2.220446049250313e-16;   // cosine noise is ~sqrt(k) eps
+    if (transposed) {
+      const double one = 1.0, zero = 0.0;
+      CKB(cublasDgeam(ctx->blas, CUBLAS_OP_T, CUBLAS_OP_N, k, k, &one, B, k, &zero, V, k, V, k));
+      CK(jacobi_svd(V, U, k, k, S, tol, 60, scr, sweeps, ctx->stream));
+    } else {
+      CK(cudaMemcpyAsync(U, B, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, ctx->stream));
+      CK(jacobi_svd(U, V, k, k, S, tol, 60, scr, sweeps, ctx->stream));
+    }
+    std::vector<double> sv = d2h(S, k, ctx->stream);
+    if (std::getenv("SSSVD_DEBUG")) {
+      int hs = 0;
+      CK(cudaMemcpy(&hs, sweeps, sizeof(int), cudaMemcpyDeviceToHost));
+      std::fprintf(stderr, "[sssvd] jacobi_svd k=%d sweeps=%d\n", k, hs);
+    }
+    std::vector<int> order(k);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return sv[a] > sv[b]; });
+    std::vector<double> sorted(k);
+    for (int i = 0; i < k; ++i) sorted[i] = sv[order[i]];
+    int* perm = static_cast<int*>(ctx->jperm.get(sizeof(int) * k));
+    double* tmp = ctx->t7.as<double>((size_t)k * k + 64);
+    CK(cudaMemcpyAsync(perm, order.data(), sizeof(int) * k, cudaMemcpyHostToDevice, ctx->stream));
+    CK(gather_cols(U, k, perm, nullptr, k, k, tmp, k, ctx->stream));
+    CK(cudaMemcpyAsync(U, tmp, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(gather_cols(V, k, perm, nullptr, k, k, tmp, k, ctx->stream));
+    CK(cudaMemcpyAsync(V, tmp, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(S, sorted.data(), sizeof(double) * k, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return;
+  }
   if (method == "gesvdp" || method == "gesvd") {
     cusolverDnParams_t params;
     CKS(cusolverDnCreateParams(&params));
@@ -522,6 +569,23 @@ static void svd_square(sssvd_gpu_ctx* ctx, double* B, int k, double* U, double* 
     cusolverDnDestroyParams(params);
     return;
   }
+  if (method == "gesvdj_t") {
+    // one-sided Jacobi on B^T (lower triangular when B is the R of a QR): B^T = V S U^T, so the
+    // roles of the singular-vector outputs swap; converges in fewer sweeps on graded factors
+    double* BT = ctx->t7.as<double>((size_t)k * k + 64);
+    const double one = 1.0, zero = 0.0;
+    CKB(cublasDgeam(ctx->blas, CUBLAS_OP_T, CUBLAS_OP_N, k, k, &one, B, k, &zero, BT, k, BT, k));
+    gesvdjInfo_t pj;
+    CKS(cusolverDnCreateGesvdjInfo(&pj));
+    CKS(cusolverDnXgesvdjSetTolerance(pj, 1e-15));
+    CKS(cusolverDnXgesvdjSetMaxSweeps(pj, 100));
+    int lw = 0;
+    CKS(cusolverDnDgesvdj_bufferSize(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, 0, k, k, BT, k, S, V, k, U, k, &lw, pj));
+    double* wk = ctx->work.as<double>(lw);
+    CKS(cusolverDnDgesvdj(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, 0, k, k, BT, k, S, V, k, U, k, wk, lw, dinfo, pj));
+    cusolverDnDestroyGesvdjInfo(pj);
+    return;
+  }
   gesvdjInfo_t params;
   CKS(cusolverDnCreateGesvdjInfo(&params));
   CKS(cusolverDnXgesvdjSetTolerance(params, 1e-15));
@@ -535,14 +599,6 @@ static void svd_square(sssvd_gpu_ctx* ctx, double* B, int k, double* U, double* 
   cusolverDnDestroyGesvdjInfo(params);
 }
 
-static std::vector<double> d2h(const double* d, size_t count, cudaStream_t s) {
-  std::vector<double> h(count);
-  if (count) {
-    CK(cudaMemcpyAsync(h.data(), d, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-  }
-  return h;
-}
 
 static bool near_endpoint(double sigma, double endpoint) {
   return std::abs(sigma - endpoint) <= 1e-9 * std::max(std::abs(endpoint), sigma);
@@ -932,7 +988,7 @@ void sssvd_gpu_destroy(sssvd_gpu_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   DBuf* bufs[] = {&ctx->A, &ctx->G, &ctx->gmax, &ctx->mats, &ctx->ipiv, &ctx->shifts, &ctx->coef, &ctx->S, &ctx->V,
                   &ctx->status, &ctx->minpiv, &ctx->scratch, &ctx->t0, &ctx->t1, &ctx->t2, &ctx->t7, &ctx->work,
-                  &ctx->info, &ctx->lw_linv, &ctx->lw_T, &ctx->lw_src, &ctx->lw_disp};
+                  &ctx->info, &ctx->lw_linv, &ctx->lw_T, &ctx->lw_src, &ctx->lw_disp, &ctx->jscr, &ctx->jperm};
   for (DBuf* b : bufs) b->release();
   for (auto& b : ctx->tail) b.release();
   if (ctx->comm) nccl().CommDestroy(ctx->comm);
