@@ -136,8 +136,11 @@ jacobi_svd_cluster_kernel(double* __restrict__ Wm, double* __restrict__ Vm, int 
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int kk = k + (k & 1);
   const int npairs = kk / 2;
+  __shared__ unsigned int cta_rot;
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
+    unsigned int my_rot = 0;   // rotations by this warp in this sweep (no per-round atomics)
+    if (threadIdx.x == 0) cta_rot = 0;
     for (int round = 0; round < kk - 1; ++round) {
       for (int pi = gwarp; pi < npairs; pi += nwarps) {
         int p = player(pi, round, kk), q = player(kk - 1 - pi, round, kk);
@@ -174,11 +177,16 @@ jacobi_svd_cluster_kernel(double* __restrict__ Wm, double* __restrict__ Vm, int 
             vp[i] = c * v1 - s * v2;
             vq[i] = s * v1 + c * v2;
           }
-          if (lane == 0) atomicAdd(rot_count + (sweep & 1), 1u);
+          ++my_rot;
         }
       }
       cluster_sync_all();
     }
+    // one atomic per CTA per sweep
+    if (lane == 0 && my_rot) atomicAdd(&cta_rot, my_rot);
+    __syncthreads();
+    if (threadIdx.x == 0 && cta_rot) atomicAdd(rot_count + (sweep & 1), cta_rot);
+    cluster_sync_all();
     const unsigned int rc = *((volatile unsigned int*)(rot_count + (sweep & 1)));
     if (blockIdx.x == 0 && threadIdx.x == 0) rot_count[(sweep + 1) & 1] = 0;
     cluster_sync_all();

@@ -22,6 +22,7 @@ cudaError_t absmax(const double* a, long long count, double* out, cudaStream_t s
 // K1 assembly (lu.cu): mats[b] = [z_b I - G | V]  row-major, pitch ld
 cudaError_t assemble(const double* G, int n, int ldg, const double* V, int L, const double2* shifts,
                      double2* out, int ld, long long stride, int batch, cudaStream_t s);
+cudaError_t load_rhs(const double* V, int n, int L, double2* out, int ld, long long stride, int batch, cudaStream_t s);
 // K2 leaf panel LU (lu.cu): rows [r0, n) x cols [r0, r0+w), W in {8,16,32}
 size_t leaf_smem_bytes(int n, int W, int cluster);
 cudaError_t leaf_lu(double2* mats, int ld, long long stride, int n, int r0, int w, int W, int cluster,

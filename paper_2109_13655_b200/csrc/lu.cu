@@ -51,6 +51,25 @@ __global__ void assemble_kernel(const double* __restrict__ G, int n, int ldg,
   }
 }
 
+// new right-hand side into the augmented columns n..n+L of resident factors (factor cache)
+__global__ void load_rhs_kernel(const double* __restrict__ V, int n, int L, double2* __restrict__ out, int ld,
+                                long long stride) {
+  const int b = blockIdx.y;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)n * L;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / L), c = (int)(e % L);
+    out[b * stride + (size_t)i * ld + n + c] = make_double2(V[(size_t)c * n + i], 0.0);
+  }
+}
+
+cudaError_t load_rhs(const double* V, int n, int L, double2* out, int ld, long long stride, int batch, cudaStream_t s) {
+  long long total = (long long)n * L;
+  int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 4);
+  load_rhs_kernel<<<dim3(blocks, batch), 256, 0, s>>>(V, n, L, out, ld, stride);
+  note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t assemble(const double* G, int n, int ldg, const double* V, int L, const double2* shifts,
                      double2* out, int ld, long long stride, int batch, cudaStream_t s) {
   long long total = (long long)n * (n + L);

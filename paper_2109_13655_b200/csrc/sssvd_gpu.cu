@@ -144,7 +144,14 @@ struct sssvd_gpu_ctx {
   bool has_gram = false;
   DBuf A, G, gmax, mats, ipiv, shifts, coef, S, V, status, minpiv, scratch;
   DBuf t0, t1, t2, t7, work, info;
-  DBuf lw_linv, lw_T, lw_src, lw_disp, jscr, jperm;
+  DBuf lw_linv, lw_T, lw_src, lw_disp, jscr, jperm, jq, jr, jj;
+  // factor cache (moments.hpp:106-116): the last pass left shifts [fact_jb, fact_je) factored in
+  // one resident batch of `mats`, so a later pass with the same operator/shifts/L only replays the
+  // forward elimination of its new right-hand side and the back substitution
+  bool fact_valid = false;
+  int64_t fact_jb = 0, fact_je = 0;
+  int fact_n = 0, fact_L = 0;
+  std::vector<std::complex<double>> fact_shifts;
   static constexpr int kMaxGroups = 4;
   cudaStream_t gstream[kMaxGroups] = {};
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxGroups] = {};
@@ -276,6 +283,20 @@ static void factor_rec(const LuPlan& P, const LuWork& W, double2* mats, int* ipi
   factor_rec(P, W, mats, ipiv, nb, s, c0 + wl, w - wl, cb);
 }
 
+// back substitution on the RHS columns [n, n+L): substitution per diagonal block (warp per
+// column), DMMA GEMM for the off-diagonal blocks
+static void back_substitute(const LuPlan& P, double2* mats, int nb, cudaStream_t s) {
+  const int n = P.n, ncols = n + P.L;
+  const int nblocks = (n + P.NB - 1) / P.NB;
+  for (int bi = nblocks - 1; bi >= 0; --bi) {
+    const int kb = bi * P.NB, nbk = std::min(P.NB, n - kb);
+    CK(trsm_upper_warp(mats, P.ld, P.stride, kb, nbk, n, ncols, nb, s));
+    if (kb > 0)
+      CK(zgemm_sub(kb, P.L, nbk, mats + kb, P.ld, P.stride, mats + (size_t)kb * P.ld + n, P.ld, P.stride,
+                   mats + n, P.ld, P.stride, nb, s));
+  }
+}
+
 // LU of nb augmented matrices [z I - G | V] in place (rows 0..n-1, cols 0..n+L-1), then the
 // back substitution U^{-1} on the L right-hand-side columns. ipiv: nb x n.
 static void lu_solve_batch(const LuPlan& P, const LuWork& W, double2* mats, int* ipiv, int nb, cudaStream_t s) {
@@ -286,16 +307,7 @@ static void lu_solve_batch(const LuPlan& P, const LuWork& W, double2* mats, int*
     // trailing columns (incl. the right-hand side): all NB interchanges, U12, A22 -= L21 U12
     apply_panel(P, W, mats, ipiv, nb, s, kb, nbk, kb + nbk, ncols);
   }
-  // back substitution on the RHS columns [n, n+L): substitution per diagonal block (warp per
-  // column), DMMA GEMM for the off-diagonal blocks
-  const int nblocks = (n + P.NB - 1) / P.NB;
-  for (int bi = nblocks - 1; bi >= 0; --bi) {
-    const int kb = bi * P.NB, nbk = std::min(P.NB, n - kb);
-    CK(trsm_upper_warp(mats, P.ld, P.stride, kb, nbk, n, ncols, nb, s));
-    if (kb > 0)
-      CK(zgemm_sub(kb, P.L, nbk, mats + kb, P.ld, P.stride, mats + (size_t)kb * P.ld + n, P.ld, P.stride,
-                   mats + n, P.ld, P.stride, nb, s));
-  }
+  back_substitute(P, mats, nb, s);
 }
 
 // Independent shift groups of one batch, each on its own stream; the host interleaves their
@@ -379,7 +391,10 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
   LuPlan P = make_plan(n, L);
   CK(cudaMemsetAsync(S_dev, 0, sizeof(double) * (size_t)(M + 1) * n * L, s));
   if (je <= jb) return;
-  const int B = choose_batch(ctx, P, je - jb);
+  const bool reuse = ctx->fact_valid && ctx->fact_jb == jb && ctx->fact_je == je && ctx->fact_n == n &&
+                     ctx->fact_L == L && ctx->fact_shifts == std::vector<std::complex<double>>(shifts.begin() + jb,
+                                                                                               shifts.begin() + je);
+  const int B = reuse ? (int)(je - jb) : choose_batch(ctx, P, je - jb);
   double2* mats = ctx->mats.as<double2>((size_t)B * P.stride);
   int* ipiv = ctx->ipiv.as<int>((size_t)B * n);
   double2* dshift = ctx->shifts.as<double2>(B);
@@ -399,6 +414,17 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
       }
     CK(cudaMemcpyAsync(dshift, hshift.data(), sizeof(double2) * nb, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(dcoef, hcoef.data(), sizeof(double2) * (M + 1) * nb, cudaMemcpyHostToDevice, s));
+    if (reuse) {
+      // cached factors: new RHS into the augmented columns, forward elimination, back substitution
+      CK(load_rhs(V_dev, n, L, mats, P.ld, P.stride, nb, s));
+      for (int kb = 0; kb < n; kb += P.NB)
+        apply_panel(P, work, mats, ipiv, nb, s, kb, std::min(P.NB, n - kb), n, n + L);
+      back_substitute(P, mats, nb, s);
+      CK(moments(mats, P.ld, P.stride, n, n, L, nb, dcoef, M, S_dev, s));
+      CK(cudaStreamSynchronize(s));
+      ctx->solve_flops += nb * (8.0 * (double)n * n * L);
+      continue;
+    }
     CK(assemble(ctx->G.as<double>(0), n, n, V_dev, L, dshift, mats, P.ld, P.stride, nb, s));
     {
       static const char* genv = std::getenv("SSSVD_GROUPS");
@@ -430,6 +456,15 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
     for (int b = 0; b < nb; ++b)
       if (hstatus[b]) throw Status(SSSVD_E_NUMERICAL, "ShiftedFactorization: shift numerically on the spectrum");
     ctx->solve_flops += nb * (8.0 * n * (double)n * n / 3.0 + 8.0 * (double)n * n * L);
+  }
+  // the factors stay resident when the whole shard fit one batch
+  ctx->fact_valid = (je - jb) <= B;
+  if (ctx->fact_valid) {
+    ctx->fact_jb = jb;
+    ctx->fact_je = je;
+    ctx->fact_n = n;
+    ctx->fact_L = L;
+    ctx->fact_shifts.assign(shifts.begin() + jb, shifts.begin() + je);
   }
 }
 
@@ -513,9 +548,34 @@ static void svd_square(sssvd_gpu_ctx* ctx, double* B, int k, double* U, double* 
     int* sweeps = reinterpret_cast<int*>(scr + 8);
     const double tol = (double)k * 2.220446049250313e-16;   // cosine noise is ~sqrt(k) eps
     if (transposed) {
+      // dgejsv-style preconditioning: B^T = Q2 R2 (QR), one-sided Jacobi on X = R2^T (lower
+      // triangular, nearly orthogonal columns): X J = W = U S  =>  B = R2^T Q2^T = U S (Q2 J)^T,
+      // so U_B = W S^{-1} and V_B = Q2 J.
       const double one = 1.0, zero = 0.0;
-      CKB(cublasDgeam(ctx->blas, CUBLAS_OP_T, CUBLAS_OP_N, k, k, &one, B, k, &zero, V, k, V, k));
-      CK(jacobi_svd(V, U, k, k, S, tol, 60, scr, sweeps, ctx->stream));
+      double* Q2 = ctx->jq.as<double>((size_t)k * k);
+      double* R2 = ctx->jr.as<double>((size_t)k * k);
+      CKB(cublasDgeam(ctx->blas, CUBLAS_OP_T, CUBLAS_OP_N, k, k, &one, B, k, &zero, Q2, k, Q2, k));
+      thin_qr(ctx, Q2, k, k, R2);                     // Q2 <- Q, R2 <- R of B^T
+      CKB(cublasDgeam(ctx->blas, CUBLAS_OP_T, CUBLAS_OP_N, k, k, &one, R2, k, &zero, U, k, U, k));   // X = R2^T
+      double* J = ctx->jj.as<double>((size_t)k * k);
+      cudaEvent_t je0 = nullptr, je1 = nullptr;
+      const bool dbg = std::getenv("SSSVD_DEBUG") != nullptr;
+      if (dbg) {
+        cudaEventCreate(&je0);
+        cudaEventCreate(&je1);
+        cudaEventRecord(je0, ctx->stream);
+      }
+      CK(jacobi_svd(U, J, k, k, S, tol, 60, scr, sweeps, ctx->stream));   // U <- W S^-1, S
+      if (dbg) {
+        cudaEventRecord(je1, ctx->stream);
+        cudaEventSynchronize(je1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, je0, je1);
+        std::fprintf(stderr, "[sssvd] jacobi kernel %.2f ms\n", ms);
+        cudaEventDestroy(je0);
+        cudaEventDestroy(je1);
+      }
+      CKB(cublasDgemm(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_N, k, k, k, &one, Q2, k, J, k, &zero, V, k));
     } else {
       CK(cudaMemcpyAsync(U, B, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, ctx->stream));
       CK(jacobi_svd(U, V, k, k, S, tol, 60, scr, sweeps, ctx->stream));
@@ -627,9 +687,11 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
   info.cols = ctx->transposed ? m : n;
   ctx->t_solves = ctx->t_allreduce = ctx->solve_flops = 0;
 
-  // ---- steps 1-2 (form_gram is part of steps 1-2 in every run, pipeline.hpp:124-125)
+  // ---- steps 1-2 (form_gram is part of steps 1-2 in every run, pipeline.hpp:124-125); the factor
+  // cache lives only inside one solve, like the reference's per-accumulator cache
   double t0 = now_s();
   ctx->has_gram = false;
+  ctx->fact_valid = false;
   ensure_gram(ctx, cfg.gram_cap > 0 ? cfg.gram_cap : 8192);
   std::vector<double> v0 = random_start(n, L, cfg.params.seed);
   double start_norm2 = 0;
@@ -988,7 +1050,7 @@ void sssvd_gpu_destroy(sssvd_gpu_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   DBuf* bufs[] = {&ctx->A, &ctx->G, &ctx->gmax, &ctx->mats, &ctx->ipiv, &ctx->shifts, &ctx->coef, &ctx->S, &ctx->V,
                   &ctx->status, &ctx->minpiv, &ctx->scratch, &ctx->t0, &ctx->t1, &ctx->t2, &ctx->t7, &ctx->work,
-                  &ctx->info, &ctx->lw_linv, &ctx->lw_T, &ctx->lw_src, &ctx->lw_disp, &ctx->jscr, &ctx->jperm};
+                  &ctx->info, &ctx->lw_linv, &ctx->lw_T, &ctx->lw_src, &ctx->lw_disp, &ctx->jscr, &ctx->jperm, &ctx->jq, &ctx->jr, &ctx->jj};
   for (DBuf* b : bufs) b->release();
   for (auto& b : ctx->tail) b.release();
   if (ctx->comm) nccl().CommDestroy(ctx->comm);
@@ -1075,6 +1137,7 @@ sssvd_status sssvd_gpu_set_operator(sssvd_gpu_ctx* ctx, const double* a, int64_t
     ctx->lda = ldp;
     ctx->transposed = tr;
     ctx->has_gram = false;
+    ctx->fact_valid = false;
   });
 }
 
@@ -1098,6 +1161,7 @@ sssvd_status sssvd_gpu_shifted_solve(sssvd_gpu_ctx* ctx, const double* g, int64_
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
     LuPlan P = make_plan((int)n, (int)L);
+    ctx->fact_valid = false;   // this entry point overwrites the factor workspace
     double2* mats = ctx->mats.as<double2>(P.stride);
     int* ipiv = ctx->ipiv.as<int>(n);
     double* Gd = ctx->t0.as<double>((size_t)n * n);
@@ -1153,6 +1217,7 @@ sssvd_status sssvd_gpu_moments(sssvd_gpu_ctx* ctx, int64_t h, const double* shif
     int64_t jb = 0, je = h;
     shard_range(h, ctx->nranks, ctx->rank, &jb, &je);
     double* Vd = ctx->V.as<double>((size_t)n * L);
+    ctx->fact_valid = false;   // the cache lives inside one accumulator call
     CK(cudaMemcpyAsync(Vd, s0, sizeof(double) * n * L, cudaMemcpyHostToDevice, s));
     double* S = ctx->S.as<double>((size_t)(M + 1) * n * L);
     for (int64_t nu = 1; nu < ell; ++nu) {

@@ -161,3 +161,16 @@ def test_nccl_single_rank_comm_path(dev):
     d2.close()
     for k in range(4):
         assert np.array_equal(ref[k], got[k])
+
+
+def test_ell3_factor_cache_matches_oracle(dev):
+    """ell > 1 with resident factors (moments.hpp:106-128): the refinement passes replay only the
+    forward/back substitution of the new block; results must equal the oracle's to rounding."""
+    a = constructed(400, 300, np.linspace(0.05, 1.5, 300), 17, 18)
+    rg, ro = rules(0.6, 0.9, 32, 0.1)
+    s0 = orc.random_start(300, 8, 42)
+    blocks = gpu_blocks(dev, a, rg, s0, 3, ell=3)
+    acc = orc.MomentAccumulator(orc.form_gram(orc.ProblemMatrix(a)), ro)
+    ref = acc.accumulate(acc.refine(acc.refine(s0)), 3).blocks
+    for k in range(4):
+        assert np.linalg.norm(blocks[k] - ref[k]) / np.linalg.norm(ref[k]) <= 1e-10
