@@ -180,6 +180,9 @@ sssvd_status sssvd_moment_coefficients(int64_t h, const double* weights, const d
 uint64_t sssvd_gpu_launch_count(void);
 void sssvd_gpu_profile_gemm(int enable);
 void sssvd_gpu_profile_gemm_collect(double* ms, double* flops, uint64_t* launches);
+/* Debug: tile share `part` of `nparts` of form_gram (the multi-GPU Gram sharding), zeros
+ * elsewhere; n x n column-major. */
+sssvd_status sssvd_debug_gram_part(sssvd_gpu_ctx* ctx, int part, int nparts, double* g_out);
 /* Debug: cycles per leaf-kernel phase summed over columns (SSSVD_LEAF_PROF=1): out[0..3] phases,
  * out[4] columns, out[5] summed CTA lifetimes, out[6] leaves (7 entries). */
 void sssvd_debug_leaf_profile(uint64_t* out7);

@@ -31,13 +31,16 @@ __device__ __forceinline__ void load_tile(double* Ps, double* Qs, const double* 
 }
 }  // namespace
 
+// part/nparts: multi-GPU sharding - this launch computes the lower-triangle tiles
+// t = part, part + nparts, ... (the other entries of G are left for the all-reduce)
 __global__ void __launch_bounds__(THREADS, 2)
-gram_kernel(const double* __restrict__ A, int lda, int K, int n, double* __restrict__ G, int ldg) {
+gram_kernel(const double* __restrict__ A, int lda, int K, int n, double* __restrict__ G, int ldg, int part,
+            int nparts) {
   extern __shared__ __align__(16) double gsm[];
   double* Ps = gsm;
   double* Qs = gsm + STAGES * TILE;
   // decode lower-triangle tile (ti >= tj) from the linear block index
-  const long long t = blockIdx.x;
+  const long long t = (long long)blockIdx.x * nparts + part;
   int ti = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
   while ((long long)(ti + 1) * (ti + 2) / 2 <= t) ++ti;
   while ((long long)ti * (ti + 1) / 2 > t) --ti;
@@ -100,7 +103,7 @@ gram_kernel(const double* __restrict__ A, int lda, int K, int n, double* __restr
   }
 }
 
-cudaError_t gram(const double* A, int lda, int K, int n, double* G, int ldg, cudaStream_t s) {
+cudaError_t gram(const double* A, int lda, int K, int n, double* G, int ldg, int part, int nparts, cudaStream_t s) {
   const size_t smem = (size_t)2 * STAGES * TILE * sizeof(double);
   static bool configured = false;
   if (!configured) {
@@ -109,7 +112,10 @@ cudaError_t gram(const double* A, int lda, int K, int n, double* G, int ldg, cud
     configured = true;
   }
   const long long T = (n + BM - 1) / BM;
-  gram_kernel<<<(unsigned)(T * (T + 1) / 2), THREADS, smem, s>>>(A, lda, K, n, G, ldg);
+  const long long tiles = T * (T + 1) / 2;
+  const long long mine = (tiles - part + nparts - 1) / nparts;
+  if (mine <= 0) return cudaSuccess;
+  gram_kernel<<<(unsigned)mine, THREADS, smem, s>>>(A, lda, K, n, G, ldg, part, nparts);
   note_launch();
   return cudaGetLastError();
 }

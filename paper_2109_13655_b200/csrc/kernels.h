@@ -15,7 +15,7 @@ void zgemm_profile_enable(bool on);
 void zgemm_profile_collect(double* ms, double* flops, unsigned long long* launches);
 
 // K0 Gram (gram.cu): G = A^T A, A column-major (lda even, K = rows incl. zero padding)
-cudaError_t gram(const double* A, int lda, int K, int n, double* G, int ldg, cudaStream_t s);
+cudaError_t gram(const double* A, int lda, int K, int n, double* G, int ldg, int part, int nparts, cudaStream_t s);
 // max |a_i| (lu.cu)
 cudaError_t absmax(const double* a, long long count, double* out, cudaStream_t s);
 

@@ -483,7 +483,16 @@ static void ensure_gram(sssvd_gpu_ctx* ctx, int64_t cap) {
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, ctx->stream));
   double* G = ctx->G.as<double>((size_t)ctx->n * ctx->n);
-  CK(gram(ctx->A.as<double>(0), (int)ctx->lda, (int)ctx->lda, (int)ctx->n, G, (int)ctx->n, ctx->stream));
+  if (ctx->comm && ctx->nranks > 1) {
+    // multi-GPU: each rank forms its share of the lower-triangle tiles, one all-reduce assembles
+    // G (every entry is written by exactly one rank, so the sum is exact)
+    CK(cudaMemsetAsync(G, 0, sizeof(double) * ctx->n * ctx->n, ctx->stream));
+    CK(gram(ctx->A.as<double>(0), (int)ctx->lda, (int)ctx->lda, (int)ctx->n, G, (int)ctx->n, ctx->rank, ctx->nranks,
+            ctx->stream));
+    CKN(nccl().AllReduce(G, G, (size_t)ctx->n * ctx->n, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+  } else {
+    CK(gram(ctx->A.as<double>(0), (int)ctx->lda, (int)ctx->lda, (int)ctx->n, G, (int)ctx->n, 0, 1, ctx->stream));
+  }
   CK(absmax(G, (long long)ctx->n * ctx->n, ctx->gmax.as<double>(1), ctx->stream));
   CK(cudaEventRecord(e1, ctx->stream));
   CK(cudaEventSynchronize(e1));
@@ -1150,6 +1159,20 @@ sssvd_status sssvd_gpu_form_gram(sssvd_gpu_ctx* ctx, int64_t cap, double* g_out)
                          ctx->stream));
       CK(cudaStreamSynchronize(ctx->stream));
     }
+  });
+}
+
+// debug: the lower-triangle tile share `part` of `nparts` of the Gram (the multi-GPU sharding of
+// form_gram), zeros elsewhere; column-major n x n into g_out
+sssvd_status sssvd_debug_gram_part(sssvd_gpu_ctx* ctx, int part, int nparts, double* g_out) {
+  return guarded(ctx, [&]() {
+    if (ctx->n <= 0 || nparts < 1 || part < 0 || part >= nparts) throw Status(SSSVD_E_INVALID_ARGUMENT, "bad part");
+    CK(cudaSetDevice(ctx->device));
+    double* G = ctx->t2.as<double>((size_t)ctx->n * ctx->n);
+    CK(cudaMemsetAsync(G, 0, sizeof(double) * ctx->n * ctx->n, ctx->stream));
+    CK(gram(ctx->A.as<double>(0), (int)ctx->lda, (int)ctx->lda, (int)ctx->n, G, (int)ctx->n, part, nparts, ctx->stream));
+    CK(cudaMemcpyAsync(g_out, G, sizeof(double) * ctx->n * ctx->n, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
   });
 }
 

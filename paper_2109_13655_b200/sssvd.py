@@ -108,7 +108,7 @@ EXPORTED_SYMBOLS = [
     "sssvd_gpu_run_solve", "sssvd_result_info_get", "sssvd_result_copy", "sssvd_result_note",
     "sssvd_result_free", "sssvd_contour", "sssvd_random_start", "sssvd_validate_params",
     "sssvd_moment_coefficients", "sssvd_build_info", "sssvd_gpu_launch_count", "sssvd_gpu_profile_gemm",
-    "sssvd_gpu_profile_gemm_collect", "sssvd_debug_leaf_profile",
+    "sssvd_gpu_profile_gemm_collect", "sssvd_debug_leaf_profile", "sssvd_debug_gram_part",
 ]
 
 _lib = None
@@ -149,6 +149,7 @@ def lib():
     L.sssvd_validate_params.argtypes = [ctypes.POINTER(_Params), i64]
     L.sssvd_moment_coefficients.argtypes = [i64, dp, dp, i64, dp]
     L.sssvd_build_info.restype = ctypes.c_char_p
+    L.sssvd_debug_gram_part.argtypes = [vp, ctypes.c_int, ctypes.c_int, dp]
     L.sssvd_gpu_launch_count.restype = ctypes.c_uint64
     L.sssvd_gpu_profile_gemm.argtypes = [ctypes.c_int]
     L.sssvd_gpu_profile_gemm.restype = None

@@ -146,3 +146,18 @@ def test_pivoting_is_exercised(dev):
     berr = np.linalg.norm(shifted @ x - rhs) / (np.linalg.norm(shifted, 2) * np.linalg.norm(x) + np.linalg.norm(rhs))
     berr_o = np.linalg.norm(shifted @ xo - rhs) / (np.linalg.norm(shifted, 2) * np.linalg.norm(xo) + np.linalg.norm(rhs))
     assert berr <= max(1e-15, 10 * berr_o)
+
+
+def test_gram_sharding_is_exact(dev):
+    """Multi-GPU form_gram: the round-robin tile shares of 3 ranks sum to the single-GPU G bitwise
+    (every entry is written by exactly one share)."""
+    from paper_2109_13655_b200 import sssvd
+    a = orc.random_matrix(700, 333, 77)
+    g = sssvd.form_gram(sssvd.ProblemMatrix.from_dense(a), device=dev)
+    parts = []
+    for p in range(3):
+        out = np.empty((333, 333), order="F")
+        dev.check(sssvd.lib().sssvd_debug_gram_part(dev.h, p, 3, sssvd._ptr(out)))
+        parts.append(out)
+    assert np.array_equal(parts[0] + parts[1] + parts[2], g)
+    assert all(np.count_nonzero(p) > 0 for p in parts)
