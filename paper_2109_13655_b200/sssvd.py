@@ -388,10 +388,7 @@ class Device:
         c = config._c()
         res = ctypes.c_void_p()
         self.check(lib().sssvd_gpu_run_solve(self.h, ctypes.byref(c), ctypes.byref(res)))
-        try:
-            return RunResult._from_handle(res)
-        finally:
-            lib().sssvd_result_free(res)
+        return RunResult._from_handle(res)
 
 
 _default_device: Optional[Device] = None
@@ -556,82 +553,102 @@ class TripletSet:
     def count(self): return self.sigma.size
 
 
-@dataclass
+class _Handle:
+    """Owns a sssvd_gpu_result; freed with the last Python reference."""
+
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().sssvd_result_free(self.h)
+        except Exception:
+            pass
+
+
 class RunResult:
-    """pipeline.hpp:74-95 (host copies of the device results)."""
-    triplets: Optional[TripletSet] = None
-    tau: Optional[np.ndarray] = None
-    spurious: Optional[np.ndarray] = None
-    estimated: Optional[np.ndarray] = None
-    exact: Optional[np.ndarray] = None
-    galerkin: Optional[np.ndarray] = None
-    basis_singular_values: Optional[np.ndarray] = None
-    blocks: Optional[MomentBlocks] = None
-    rank_deficient_qr: bool = False
-    timings: StepTimings = field(default_factory=StepTimings)
-    empty: bool = False
-    note: str = ""
-    input_transposed: bool = False
-    count_in_interval: int = 0
-    count_nonspurious_in_interval: int = 0
-    count_interior: int = 0
-    count_boundary: int = 0
-    calibration_index: Optional[int] = None
-    mu: Optional[float] = None
-    spurious_threshold: float = 0.0
-    device_times: dict = field(default_factory=dict)
+    """pipeline.hpp:74-95. Scalars are read eagerly; the arrays (triplet vectors, tau,
+    residuals, moment blocks) are copied out of the C result handle on first access."""
+
+    def __init__(self, handle: _Handle):
+        L = lib()
+        info = _Info()
+        L.sssvd_result_info_get(handle.h, ctypes.byref(info))
+        self._h, self._info = handle, info
+        self.empty = bool(info.empty)
+        self.note = L.sssvd_result_note(handle.h).decode()
+        self.input_transposed = bool(info.input_transposed)
+        self.rank_deficient_qr = bool(info.rank_deficient_qr)
+        self.timings = StepTimings(info.steps_1_2, info.step_3, info.step_4, info.step_5, info.postprocess)
+        self.device_times = {"gram_s": info.t_gram, "shifted_solves_s": info.t_shifted_solves,
+                             "allreduce_s": info.t_allreduce, "shifted_solve_flops": info.shifted_solve_flops}
+        self.count_in_interval = info.count_in_interval
+        self.count_nonspurious_in_interval = info.count_nonspurious_in_interval
+        self.count_interior, self.count_boundary = info.count_interior, info.count_boundary
+        self.calibration_index = None if info.calibration_index < 0 else info.calibration_index
+        self.mu = info.mu if info.calibration_index >= 0 else None
+        self.spurious_threshold = info.spurious_threshold
+        self._cache = {}
+
+    def _get(self, field, count, dtype=np.float64):
+        key = (field, count)
+        if key not in self._cache:
+            out = np.empty(count, dtype=dtype)
+            if count:
+                lib().sssvd_result_copy(self._h.h, field, _ptr(out))
+            self._cache[key] = out
+        return self._cache[key]
 
     def retained_rank(self):
-        return 0 if self.basis_singular_values is None else self.basis_singular_values.size
+        return self._info.retained_rank
+
+    @property
+    def basis_singular_values(self):
+        return self._get(9, self._info.retained_rank)
+
+    @property
+    def blocks(self):
+        i = self._info
+        n, Lb, M = i.n_internal, i.block_size, i.moment_degree
+        blk = self._get(10, (M + 1) * n * Lb)
+        return MomentBlocks([blk[k * n * Lb:(k + 1) * n * Lb].reshape((Lb, n)).T for k in range(M + 1)])
+
+    @property
+    def triplets(self):
+        i = self._info
+        if self.empty:
+            return TripletSet(np.empty(0), np.empty((i.rows, 0)), np.empty((i.cols, 0)), np.empty((0, 0)),
+                              np.empty(0, dtype=bool))
+        t = i.count
+        return TripletSet(self._get(0, t), self._get(7, i.rows * t).reshape((t, i.rows)).T,
+                          self._get(8, i.cols * t).reshape((t, i.cols)).T,
+                          self._get(11, i.retained_rank * t).reshape((t, i.retained_rank)).T,
+                          self._get(5, t, np.int32).astype(bool))
+
+    @property
+    def tau(self):
+        return None if self.empty else self._get(1, self._info.count)
+
+    @property
+    def spurious(self):
+        return None if self.empty else self._get(6, self._info.count, np.int32).astype(bool)
+
+    @property
+    def estimated(self):
+        return None if self.empty else self._get(2, self._info.count)
+
+    @property
+    def exact(self):
+        return None if self.empty else self._get(3, self._info.count)
+
+    @property
+    def galerkin(self):
+        return None if self.empty else self._get(4, self._info.count)
 
     @staticmethod
     def _from_handle(h) -> "RunResult":
-        L = lib()
-        info = _Info()
-        L.sssvd_result_info_get(h, ctypes.byref(info))
-        r = RunResult()
-        r.empty = bool(info.empty)
-        r.note = L.sssvd_result_note(h).decode()
-        r.input_transposed = bool(info.input_transposed)
-        r.rank_deficient_qr = bool(info.rank_deficient_qr)
-        r.timings = StepTimings(info.steps_1_2, info.step_3, info.step_4, info.step_5, info.postprocess)
-        r.device_times = {"gram_s": info.t_gram, "shifted_solves_s": info.t_shifted_solves,
-                          "allreduce_s": info.t_allreduce, "shifted_solve_flops": info.shifted_solve_flops}
-        n, Lb, M = info.n_internal, info.block_size, info.moment_degree
-
-        def get(field, count, dtype=np.float64):
-            out = np.empty(count, dtype=dtype)
-            if count:
-                L.sssvd_result_copy(h, field, _ptr(out))
-            return out
-
-        blk = get(10, (M + 1) * n * Lb)
-        r.blocks = MomentBlocks([blk[k * n * Lb:(k + 1) * n * Lb].reshape((Lb, n)).T.copy(order="F")
-                                 for k in range(M + 1)])
-        r.basis_singular_values = get(9, info.retained_rank)
-        t = info.count
-        r.count_in_interval = info.count_in_interval
-        r.count_nonspurious_in_interval = info.count_nonspurious_in_interval
-        r.count_interior, r.count_boundary = info.count_interior, info.count_boundary
-        r.calibration_index = None if info.calibration_index < 0 else info.calibration_index
-        r.mu = info.mu if info.calibration_index >= 0 else None
-        r.spurious_threshold = info.spurious_threshold
-        if r.empty:
-            r.triplets = TripletSet(np.empty(0), np.empty((info.rows, 0)), np.empty((info.cols, 0)),
-                                    np.empty((0, 0)), np.empty(0, dtype=bool))
-            return r
-        sigma = get(0, t)
-        left = get(7, info.rows * t).reshape((t, info.rows)).T
-        right = get(8, info.cols * t).reshape((t, info.cols)).T
-        q = get(11, info.retained_rank * t).reshape((t, info.retained_rank)).T
-        in_int = get(5, t, np.int32).astype(bool)
-        r.triplets = TripletSet(sigma, left, right, q, in_int)
-        r.tau = get(1, t)
-        r.spurious = get(6, t, np.int32).astype(bool)
-        r.estimated = get(2, t)
-        r.exact = get(3, t)
-        r.galerkin = get(4, t)
-        return r
+        return RunResult(_Handle(h))
 
 
 def run_solve(a, config: RunConfig, device: Optional[Device] = None) -> RunResult:
