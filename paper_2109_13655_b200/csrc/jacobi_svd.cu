@@ -17,6 +17,8 @@
 // sense-reversing software grid barrier; a sweep without any rotation ends the iteration.
 // Afterwards sigma_j = |w_j|, u_j = w_j / sigma_j, sorted nonincreasing on the host.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -257,6 +259,267 @@ cudaError_t jacobi_svd(double* W, double* V, int k, int ldw, double* S, double t
     e = cudaLaunchKernelEx(&cfg, jacobi_svd_cluster_kernel, W, V, k, ldw, tol, max_sweeps, rot, sweeps_out);
     if (e != cudaSuccess) return e;
     note_launch();
+  }
+  jacobi_finish_kernel<<<k, 256, 0, s>>>(W, k, ldw, S);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace sssvd_gpu
+
+namespace sssvd_gpu {
+
+// ----------------------------------------------------------------------------- block Jacobi
+// Block one-sided Jacobi for k <= 512 (the tail's k x k factors of configs 1, 2, 4). The k columns
+// are split into 32 blocks of b = ceil(k/32) columns (zero padding columns never rotate). One
+// cluster of 16 CTAs; outer round = a tournament pairing of the 32 blocks: CTA c loads its block
+// pair (2b columns x k rows) into shared memory, orthogonalises all 2b columns with one inner
+// sweep (2b-1 inner rounds of b disjoint pairs, one warp per pair, __syncthreads between inner
+// rounds) while accumulating the 2b x 2b rotation Q, writes the block pair back, and applies
+// V[:, pair] <- V[:, pair] Q. Outer rounds are separated by the cluster barrier (blocks travel
+// through L2). Same rotations and threshold as the scalar kernel; 31 cluster barriers per sweep
+// instead of k-1.
+constexpr int BJ_THREADS = 512;
+
+__global__ void __launch_bounds__(BJ_THREADS, 1)
+jacobi_block_kernel(double* __restrict__ Wm, double* __restrict__ Vm, int k, int ldw, int b, double tol,
+                    int max_sweeps, unsigned int* __restrict__ rot_count, int* __restrict__ sweeps_out,
+                    unsigned long long* __restrict__ prof) {
+  extern __shared__ __align__(16) double bsm[];
+  const int w2 = 2 * b;                 // columns per block pair
+  double* Ws = bsm;                     // [w2][k] columns
+  double* Qs = Ws + (size_t)w2 * k;     // [w2][w2] column-major
+  __shared__ int colid[32];             // global column of local column c (or -1)
+  __shared__ unsigned int cta_rot;
+  __shared__ __align__(8) unsigned long long mbar;
+  unsigned phase = 0;
+  const bool bulk = (k % 2) == 0;       // 16-byte aligned columns: TMA bulk copies
+  if (threadIdx.x == 0) mbar_init(&mbar, 1);
+  __syncthreads();
+  // columns colid[0..w2) of M -> Ws (zeros for padding columns), via TMA bulk copies
+  auto load_pair = [&](const double* M) {
+    if (bulk) {
+      if (threadIdx.x == 0) {
+        unsigned bytes = 0;
+        for (int lc = 0; lc < w2; ++lc)
+          if (colid[lc] >= 0) bytes += (unsigned)k * 8u;
+        mbar_expect_tx(&mbar, bytes);
+        for (int lc = 0; lc < w2; ++lc)
+          if (colid[lc] >= 0) bulk_g2s(Ws + (size_t)lc * k, M + (size_t)colid[lc] * ldw, (unsigned)k * 8u, &mbar);
+      }
+      for (int e = threadIdx.x; e < w2 * k; e += BJ_THREADS)
+        if (colid[e / k] < 0) Ws[e] = 0.0;
+      mbar_wait(&mbar, phase);
+      phase ^= 1u;
+    } else {
+#pragma unroll 8
+      for (int e = threadIdx.x; e < w2 * k; e += BJ_THREADS) {
+        const int lc = e / k, r = e % k;
+        const int gc = colid[lc];
+        Ws[e] = gc >= 0 ? M[(size_t)gc * ldw + r] : 0.0;
+      }
+    }
+  };
+  // Ws -> columns colid[..] of M
+  auto store_pair = [&](double* M) {
+    if (bulk) {
+      fence_proxy_async();   // make the generic-proxy smem writes visible to the bulk engine
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int lc = 0; lc < w2; ++lc)
+          if (colid[lc] >= 0) bulk_s2g(M + (size_t)colid[lc] * ldw, Ws + (size_t)lc * k, (unsigned)k * 8u);
+        bulk_commit();
+        bulk_wait_all();
+        __threadfence();
+      }
+      __syncthreads();
+    } else {
+#pragma unroll 8
+      for (int e = threadIdx.x; e < w2 * k; e += BJ_THREADS) {
+        const int lc = e / k, r = e % k;
+        const int gc = colid[lc];
+        if (gc >= 0) M[(size_t)gc * ldw + r] = Ws[e];
+      }
+      __syncthreads();
+    }
+  };
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c = blockIdx.x;             // block pair slot 0..15
+  const bool rec = blockIdx.x == 0 && tid == 0 && prof != nullptr;
+  unsigned long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    unsigned int my_rot = 0;
+    if (tid == 0) cta_rot = 0;
+    for (int round = 0; round < 31; ++round) {
+      if (rec) t0 = clock64();
+      // blocks at tournament positions c and 31 - c
+      const int bx = player(c, round, 32), by = player(31 - c, round, 32);
+      if (tid < w2) {
+        const int blk = tid < b ? bx : by;
+        const int gc = blk * b + (tid < b ? tid : tid - b);
+        colid[tid] = gc < k ? gc : -1;
+      }
+      __syncthreads();
+      load_pair(Wm);
+      for (int e = tid; e < w2 * w2; e += BJ_THREADS) Qs[e] = (e / w2) == (e % w2) ? 1.0 : 0.0;
+      __syncthreads();
+      if (rec) t1 = clock64();
+      // one inner sweep over all pairs of the 2b local columns
+      for (int ir = 0; ir < w2 - 1; ++ir) {
+        for (int pi = warp; pi < b; pi += BJ_THREADS / 32) {
+          int p = player(pi, ir, w2), q = player(w2 - 1 - pi, ir, w2);
+          if (p > q) { int t = p; p = q; q = t; }
+          double* wp = Ws + (size_t)p * k;
+          double* wq = Ws + (size_t)q * k;
+          double a = 0.0, bb = 0.0, g = 0.0, a2 = 0.0, bb2 = 0.0, g2 = 0.0;
+          int r = lane;
+#pragma unroll 4
+          for (; r + 32 < k; r += 64) {
+            const double x = wp[r], y = wq[r], x2 = wp[r + 32], y2 = wq[r + 32];
+            a += x * x;
+            bb += y * y;
+            g += x * y;
+            a2 += x2 * x2;
+            bb2 += y2 * y2;
+            g2 += x2 * y2;
+          }
+          if (r < k) {
+            const double x = wp[r], y = wq[r];
+            a += x * x;
+            bb += y * y;
+            g += x * y;
+          }
+          a += a2;
+          bb += bb2;
+          g += g2;
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, off);
+            bb += __shfl_xor_sync(0xffffffffu, bb, off);
+            g += __shfl_xor_sync(0xffffffffu, g, off);
+          }
+          if (g * g > tol * tol * a * bb && g != 0.0) {
+            const double zeta = (bb - a) / (2.0 * g);
+            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            const double cs = rsqrt(1.0 + t * t), sn = cs * t;
+#pragma unroll 8
+            for (int r = lane; r < k; r += 32) {
+              const double x = wp[r], y = wq[r];
+              wp[r] = cs * x - sn * y;
+              wq[r] = sn * x + cs * y;
+            }
+            double* qp = Qs + (size_t)p * w2;
+            double* qq = Qs + (size_t)q * w2;
+            for (int r = lane; r < w2; r += 32) {
+              const double x = qp[r], y = qq[r];
+              qp[r] = cs * x - sn * y;
+              qq[r] = sn * x + cs * y;
+            }
+            ++my_rot;
+          }
+        }
+        __syncthreads();
+      }
+      if (rec) t2 = clock64();
+      // write the block pair back
+      store_pair(Wm);
+      // V[:, pair] <- V[:, pair] Q  (rows owned by threads; staged through the W buffer)
+      load_pair(Vm);
+      __syncthreads();
+      for (int r = tid; r < k; r += BJ_THREADS) {
+        double row[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i < w2) row[i] = Ws[(size_t)i * k + r];
+#pragma unroll 4
+        for (int j = 0; j < w2; ++j) {
+          double acc = 0.0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i < w2) acc += row[i] * Qs[(size_t)j * w2 + i];
+          Ws[(size_t)j * k + r] = acc;   // own row: no other thread touches it
+        }
+      }
+      __syncthreads();
+      store_pair(Vm);
+      if (rec) t3 = clock64();
+      cluster_sync_all();
+      if (rec) {
+        const unsigned long long t4 = clock64();
+        prof[0] += t1 - t0;   // load block pair
+        prof[1] += t2 - t1;   // inner sweep
+        prof[2] += t3 - t2;   // write back + V update
+        prof[3] += t4 - t3;   // cluster barrier
+        prof[4] += 1;
+      }
+    }
+    if (lane == 0 && my_rot) atomicAdd(&cta_rot, my_rot);
+    __syncthreads();
+    if (tid == 0 && cta_rot) atomicAdd(rot_count + (sweep & 1), cta_rot);
+    cluster_sync_all();
+    const unsigned int rc = *((volatile unsigned int*)(rot_count + (sweep & 1)));
+    if (c == 0 && tid == 0) rot_count[(sweep + 1) & 1] = 0;
+    cluster_sync_all();
+    if (rc == 0) {
+      ++sweep;
+      break;
+    }
+  }
+  if (c == 0 && tid == 0) *sweeps_out = sweep;
+}
+
+size_t jacobi_block_smem(int k) {
+  const int b = (k + 31) / 32;
+  return ((size_t)2 * b * k + (size_t)4 * b * b) * sizeof(double);
+}
+
+cudaError_t jacobi_svd_block(double* W, double* V, int k, int ldw, double* S, double tol, int max_sweeps,
+                             unsigned int* scratch, int* sweeps_out, cudaStream_t s) {
+  const int b = (k + 31) / 32;
+  const size_t smem = jacobi_block_smem(k);
+  if (2 * b > 32 || smem > 220 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e = cudaMemsetAsync(scratch, 0, 8 * sizeof(unsigned int), s);
+  if (e != cudaSuccess) return e;
+  set_identity_kernel<<<148 * 4, 256, 0, s>>>(V, k, ldw);
+  note_launch();
+  static size_t configured = 0;
+  if (smem > configured) {
+    e = cudaFuncSetAttribute(jacobi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(jacobi_block_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  unsigned int* rot = scratch + 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(16, 1, 1);
+  cfg.blockDim = dim3(BJ_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 16;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  static const bool prof_on = std::getenv("SSSVD_JACOBI_PROF") != nullptr;
+  static unsigned long long* dprof = nullptr;
+  if (prof_on && !dprof) {
+    cudaMalloc(&dprof, 8 * sizeof(unsigned long long));
+  }
+  if (prof_on) cudaMemsetAsync(dprof, 0, 8 * sizeof(unsigned long long), s);
+  e = cudaLaunchKernelEx(&cfg, jacobi_block_kernel, W, V, k, ldw, b, tol, max_sweeps, rot, sweeps_out,
+                         prof_on ? dprof : (unsigned long long*)nullptr);
+  if (e != cudaSuccess) return e;
+  note_launch();
+  if (prof_on) {
+    unsigned long long v[8];
+    cudaMemcpyAsync(v, dprof, sizeof(v), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    if (v[4]) std::fprintf(stderr, "[sssvd] block jacobi k=%d cycles/outer round: load %llu inner %llu store+V %llu barrier %llu\n",
+                           k, v[0] / v[4], v[1] / v[4], v[2] / v[4], v[3] / v[4]);
   }
   jacobi_finish_kernel<<<k, 256, 0, s>>>(W, k, ldw, S);
   note_launch();

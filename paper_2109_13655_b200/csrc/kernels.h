@@ -64,6 +64,9 @@ cudaError_t trsm_upper_warp(double2* mats, int ld, long long stride, int r0, int
 // one-sided Jacobi SVD (jacobi_svd.cu): W (k x k, in) -> W = U (unsorted), V, S = sigma
 cudaError_t jacobi_svd(double* W, double* V, int k, int ldw, double* S, double tol, int max_sweeps,
                        unsigned int* scratch, int* sweeps_out, cudaStream_t s);
+cudaError_t jacobi_svd_block(double* W, double* V, int k, int ldw, double* S, double tol, int max_sweeps,
+                             unsigned int* scratch, int* sweeps_out, cudaStream_t s);
+size_t jacobi_block_smem(int k);
 // K7 (moments.cu)
 cudaError_t moments(const double2* mats, int ld, long long stride, int xcol, int n, int L, int nb,
                     const double2* coef, int M, double* S, cudaStream_t s);

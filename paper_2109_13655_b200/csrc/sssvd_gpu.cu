@@ -574,7 +574,14 @@ static void svd_square(sssvd_gpu_ctx* ctx, double* B, int k, double* U, double* 
         cudaEventCreate(&je1);
         cudaEventRecord(je0, ctx->stream);
       }
-      CK(jacobi_svd(U, J, k, k, S, tol, 60, scr, sweeps, ctx->stream));   // U <- W S^-1, S
+      // block Jacobi (shared-memory inner sweeps) where the block pair fits, else the scalar one
+      static const char* jb = std::getenv("SSSVD_JACOBI");
+      const bool use_block = !(jb && std::string(jb) == "scalar") && k <= 512 && k >= 64 &&
+                             jacobi_block_smem(k) <= 220 * 1024;
+      if (use_block)
+        CK(jacobi_svd_block(U, J, k, k, S, tol, 60, scr, sweeps, ctx->stream));
+      else
+        CK(jacobi_svd(U, J, k, k, S, tol, 60, scr, sweeps, ctx->stream));   // U <- W S^-1, S
       if (dbg) {
         cudaEventRecord(je1, ctx->stream);
         cudaEventSynchronize(je1);
