@@ -153,8 +153,10 @@ struct sssvd_gpu_ctx {
   int fact_n = 0, fact_L = 0;
   std::vector<std::complex<double>> fact_shifts;
   static constexpr int kMaxGroups = 4;
-  cudaStream_t gstream[kMaxGroups] = {};
+  cudaStream_t gstream[kMaxGroups] = {};      // high priority: panels, small kernels
+  cudaStream_t gstream_lo[kMaxGroups] = {};   // low priority: the big trailing-update GEMMs
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxGroups] = {};
+  cudaEvent_t ev_pre[kMaxGroups] = {}, ev_gemm[kMaxGroups] = {};
   DBuf tail[24];
   double t_gram = 0, t_solves = 0, t_allreduce = 0, solve_flops = 0;
 };
@@ -241,7 +243,8 @@ struct LuWork {
 //   T = L11^{-1} P A12  (DMMA GEMM gathering the pivoted rows on load)  -> U12
 //   displaced rows + U12 written back (scatter_copy), then A22 -= L21 T (DMMA GEMM)
 static void apply_panel(const LuPlan& P, const LuWork& W, double2* mats, const int* ipiv, int nb, cudaStream_t s,
-                        int r0, int np, int c0, int c1) {
+                        int r0, int np, int c0, int c1, cudaStream_t s_gemm = nullptr, cudaEvent_t ev_pre = nullptr,
+                        cudaEvent_t ev_done = nullptr) {
   const int n = P.n, N = c1 - c0;
   if (N <= 0) return;
   CK(build_moves(ipiv, n, r0, np, W.src, W.disp, P.NB, nb, s));
@@ -250,9 +253,21 @@ static void apply_panel(const LuPlan& P, const LuWork& W, double2* mats, const i
                       W.tstride, nb, s));
   CK(scatter_copy(mats, P.ld, P.stride, r0, np, c0, c1, W.disp, P.NB, W.T, N, W.tstride, nb, s));
   const int M = n - (r0 + np);
+  cudaStream_t sg = s;
+  if (s_gemm) {
+    // the trailing GEMM runs on a low-priority stream, so pending panel CTAs of other groups
+    // are scheduled ahead of its queued tiles
+    CK(cudaEventRecord(ev_pre, s));
+    CK(cudaStreamWaitEvent(s_gemm, ev_pre, 0));
+    sg = s_gemm;
+  }
   if (M > 0)
     CK(zgemm_sub(M, N, np, mats + (size_t)(r0 + np) * P.ld + r0, P.ld, P.stride, W.T, N, W.tstride,
-                 mats + (size_t)(r0 + np) * P.ld + c0, P.ld, P.stride, nb, s));
+                 mats + (size_t)(r0 + np) * P.ld + c0, P.ld, P.stride, nb, sg));
+  if (s_gemm) {
+    CK(cudaEventRecord(ev_done, s_gemm));
+    CK(cudaStreamWaitEvent(s, ev_done, 0));
+  }
 }
 
 // Recursive (getrf2-style) factorisation of the panel columns [c0, c0+w) over rows [c0, n),
@@ -318,7 +333,9 @@ struct LuGroup {
   int* ipiv;
   LuWork W;
   int nb;
-  cudaStream_t s;
+  cudaStream_t s;      // high priority
+  cudaStream_t s_lo;   // low priority (trailing GEMMs)
+  cudaEvent_t ev_pre, ev_gemm;
 };
 
 static void lu_solve_groups(const LuPlan& P, std::vector<LuGroup>& G) {
@@ -327,7 +344,7 @@ static void lu_solve_groups(const LuPlan& P, std::vector<LuGroup>& G) {
     const int nbk = std::min(P.NB, n - kb);
     for (auto& g : G) {
       factor_rec(P, g.W, g.mats, g.ipiv, g.nb, g.s, kb, nbk, kb);
-      apply_panel(P, g.W, g.mats, g.ipiv, g.nb, g.s, kb, nbk, kb + nbk, ncols);
+      apply_panel(P, g.W, g.mats, g.ipiv, g.nb, g.s, kb, nbk, kb + nbk, ncols, g.s_lo, g.ev_pre, g.ev_gemm);
     }
   }
   const int nblocks = (n + P.NB - 1) / P.NB;
@@ -428,7 +445,7 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
     CK(assemble(ctx->G.as<double>(0), n, n, V_dev, L, dshift, mats, P.ld, P.stride, nb, s));
     {
       static const char* genv = std::getenv("SSSVD_GROUPS");
-      const int ng = std::max(1, std::min(nb / 2, genv ? std::atoi(genv) : 2));
+      const int ng = std::max(1, std::min(nb / 2, genv ? std::atoi(genv) : 3));
       if (ng <= 1) {
         lu_solve_batch(P, work, mats, ipiv, nb, s);
       } else {
@@ -439,7 +456,7 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
           const int cnt = nb / ng + (g < nb % ng ? 1 : 0);
           CK(cudaStreamWaitEvent(ctx->gstream[g], ctx->ev_fork, 0));
           groups.push_back({mats + (size_t)b0 * P.stride, ipiv + (size_t)b0 * n, work_slice(work, P, b0), cnt,
-                            ctx->gstream[g]});
+                            ctx->gstream[g], ctx->gstream_lo[g], ctx->ev_pre[g], ctx->ev_gemm[g]});
           b0 += cnt;
         }
         lu_solve_groups(P, groups);
@@ -1049,9 +1066,14 @@ sssvd_status sssvd_gpu_create(int device, sssvd_gpu_ctx** out) {
     delete ctx;
     return SSSVD_E_CUDA;
   }
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   for (int g = 0; g < sssvd_gpu_ctx::kMaxGroups; ++g) {
-    cudaStreamCreateWithFlags(&ctx->gstream[g], cudaStreamNonBlocking);
+    cudaStreamCreateWithPriority(&ctx->gstream[g], cudaStreamNonBlocking, prio_hi);
+    cudaStreamCreateWithPriority(&ctx->gstream_lo[g], cudaStreamNonBlocking, prio_lo);
     cudaEventCreateWithFlags(&ctx->ev_join[g], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->ev_pre[g], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->ev_gemm[g], cudaEventDisableTiming);
   }
   cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
   cublasSetStream(ctx->blas, ctx->stream);
@@ -1074,7 +1096,10 @@ void sssvd_gpu_destroy(sssvd_gpu_ctx* ctx) {
   if (ctx->blas) cublasDestroy(ctx->blas);
   for (int g = 0; g < sssvd_gpu_ctx::kMaxGroups; ++g) {
     if (ctx->gstream[g]) cudaStreamDestroy(ctx->gstream[g]);
+    if (ctx->gstream_lo[g]) cudaStreamDestroy(ctx->gstream_lo[g]);
     if (ctx->ev_join[g]) cudaEventDestroy(ctx->ev_join[g]);
+    if (ctx->ev_pre[g]) cudaEventDestroy(ctx->ev_pre[g]);
+    if (ctx->ev_gemm[g]) cudaEventDestroy(ctx->ev_gemm[g]);
   }
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
