@@ -38,7 +38,9 @@ typedef enum {
   SSSVD_E_EMPTY_SUBSPACE = 5,   /* EmptySubspaceError (moments.hpp:201-203) */
   SSSVD_E_CUDA = 6,
   SSSVD_E_NCCL = 7,
-  SSSVD_E_OOM = 8
+  SSSVD_E_OOM = 8,
+  SSSVD_E_FORMAT = 9,           /* MatrixMarketError (matrix_market.hpp:17-21): "path:line: what" */
+  SSSVD_E_IO = 10               /* std::runtime_error: cannot open / write failed */
 } sssvd_status;
 
 /* SolveMode (pipeline.hpp:24) */
@@ -100,6 +102,14 @@ void sssvd_shard_range(int64_t h, int nranks, int rank, int64_t* begin, int64_t*
  * means `a` is a device pointer on the context's GPU. */
 sssvd_status sssvd_gpu_set_operator(sssvd_gpu_ctx* ctx, const double* a, int64_t rows, int64_t cols,
                                     int64_t lda, int on_device);
+/* ProblemMatrix::from_sparse (problem.hpp:27-35) + upload: A given as compressed sparse column
+ * (Eigen's SparseMatrix layout) in the user orientation, colptr[cols+1], rowind[nnz] strictly
+ * increasing inside each column, values[nnz]; all three are device pointers if on_device != 0.
+ * The operator is densified in HBM; wide inputs are stored transposed
+ * exactly as from_sparse does. INVALID_ARGUMENT for a malformed CSC or a NaN/Inf value. */
+sssvd_status sssvd_gpu_set_operator_csc(sssvd_gpu_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz,
+                                        const int64_t* colptr, const int64_t* rowind, const double* values,
+                                        int on_device);
 /* form_gram (problem.hpp:81-95) of the current operator; G_out (cols x cols, column-major) may
  * be NULL to keep G on the device only. */
 sssvd_status sssvd_gpu_form_gram(sssvd_gpu_ctx* ctx, int64_t size_cap, double* g_out);
@@ -186,6 +196,32 @@ sssvd_status sssvd_debug_gram_part(sssvd_gpu_ctx* ctx, int part, int nparts, dou
 /* Debug: cycles per leaf-kernel phase summed over columns (SSSVD_LEAF_PROF=1): out[0..3] phases,
  * out[4] columns, out[5] summed CTA lifetimes, out[6] leaves (7 entries). */
 void sssvd_debug_leaf_profile(uint64_t* out7);
+/* ---- Matrix Market ingest (matrix_market.hpp:34-149; host only) ---------------------------- *
+ * sssvd_mm_read mirrors read_matrix_market: real/integer/double `array` (dense) and `coordinate`
+ * (sparse, duplicates summed in file order, (skew-)symmetric expanded) formats; `complex` and
+ * `pattern` are rejected. Data are in the FILE's orientation (the caller's ProblemMatrix applies
+ * the rows >= cols normalisation): dense = rows x cols column-major values; sparse = CSC colptr /
+ * rowind / values. Errors: SSSVD_E_IO (cannot open), SSSVD_E_FORMAT ("path:line: what"); the
+ * message is sssvd_host_last_error(). */
+typedef struct sssvd_mm_matrix sssvd_mm_matrix;
+typedef struct {
+  int64_t rows, cols, nnz; /* nnz = rows*cols for dense */
+  int sparse;
+} sssvd_mm_info;
+sssvd_status sssvd_mm_read(const char* path, sssvd_mm_matrix** out);
+void sssvd_mm_info_get(const sssvd_mm_matrix* mm, sssvd_mm_info* info);
+const double* sssvd_mm_values(const sssvd_mm_matrix* mm);
+const int64_t* sssvd_mm_colptr(const sssvd_mm_matrix* mm); /* NULL for dense */
+const int64_t* sssvd_mm_rowind(const sssvd_mm_matrix* mm); /* NULL for dense */
+void sssvd_mm_free(sssvd_mm_matrix* mm);
+/* write_matrix_market (matrix_market.hpp:121-149), given the USER orientation: colptr == NULL
+ * writes `values` (rows x cols column-major) in array format, else the CSC in coordinate format;
+ * 17 significant digits; `comment` (may be NULL/empty) becomes a "% comment" line. */
+sssvd_status sssvd_mm_write(const char* path, int64_t rows, int64_t cols, int64_t nnz, const int64_t* colptr,
+                            const int64_t* rowind, const double* values, const char* comment);
+/* Message of the last failing host-only call on this thread. */
+const char* sssvd_host_last_error(void);
+
 /* Build provenance for the loaded library ("sm_100a ..."). */
 const char* sssvd_build_info(void);
 

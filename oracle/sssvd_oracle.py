@@ -259,9 +259,23 @@ class RunConfig:
 
 # ----------------------------------------------------------------------------- problem / Gram
 class ProblemMatrix:
-    """problem.hpp:14-77 (dense storage; auto-transpose when rows < cols; NaN check)."""
+    """problem.hpp:14-77: dense (numpy) or sparse (scipy CSC) storage; auto-transpose when
+    rows < cols; NaN check (:20-35, :56-58)."""
 
-    def __init__(self, a: np.ndarray):
+    def __init__(self, a):
+        import scipy.sparse as sp
+        self.is_sparse = sp.issparse(a)
+        if self.is_sparse:
+            a = sp.csc_matrix(a, dtype=np.float64)
+            self.transposed = a.shape[0] < a.shape[1]
+            if self.transposed:
+                a = a.T.tocsc()
+            a.sum_duplicates()
+            a.sort_indices()
+            if not np.all(np.isfinite(a.data)):
+                raise ValueError("ProblemMatrix: NaN/Inf entry")
+            self.sparse = a
+            return
         a = np.asarray(a, dtype=np.float64)
         self.transposed = a.shape[0] < a.shape[1]
         if self.transposed:
@@ -271,28 +285,151 @@ class ProblemMatrix:
         self.dense = np.asfortranarray(a)
 
     @property
+    def shape(self):
+        return self.sparse.shape if self.is_sparse else self.dense.shape
+
+    @property
     def rows(self):
-        return self.dense.shape[0]
+        return self.shape[0]
 
     @property
     def cols(self):
-        return self.dense.shape[1]
+        return self.shape[1]
+
+    def to_dense(self):
+        return np.asfortranarray(self.sparse.toarray()) if self.is_sparse else self.dense
 
     def apply(self, x):
-        return self.dense @ x
+        return np.asarray(self.sparse @ x) if self.is_sparse else self.dense @ x
 
     def apply_adjoint(self, x):
-        return self.dense.T @ x
+        return np.asarray(self.sparse.T @ x) if self.is_sparse else self.dense.T @ x
 
 
 def form_gram(a: ProblemMatrix, size_cap: int = 8192) -> np.ndarray:
-    """problem.hpp:81-95: G = A^T A then (G + G^T)/2; length_error above the cap.
+    """problem.hpp:81-95: G = A^T A (sparse product for sparse storage, :87-89) then
+    (G + G^T)/2; length_error above the cap.
 
     The BASELINE config 5 (n = 16384) lifts the cap (documented deviation)."""
     if a.cols > size_cap:
         raise LengthError("form_gram: column count exceeds the dense Gram cap")
-    g = a.dense.T @ a.dense
+    if a.is_sparse:
+        g = (a.sparse.T @ a.sparse).toarray()
+    else:
+        g = a.dense.T @ a.dense
     return np.asfortranarray((g + g.T) / 2.0)
+
+
+class MatrixMarketError(RuntimeError):
+    """matrix_market.hpp:17-21."""
+
+
+def read_matrix_market(path: str) -> ProblemMatrix:
+    """matrix_market.hpp:34-119 restated in Python (checker for the library's C++ reader).
+    Numbers are parsed with the same acceptance rules as std::istream >> for the inputs the tests
+    use (plain decimal / exponent notation); duplicates are summed in file order."""
+    import scipy.sparse as sp
+
+    def err(line, what):
+        return MatrixMarketError(f"{path}:{line}: {what}")
+
+    try:
+        f = open(path, "r")
+    except OSError:
+        raise RuntimeError("read_matrix_market: cannot open " + path)
+    with f:
+        lines = f.read().split("\n")
+    if lines and lines[-1] == "":
+        lines.pop()
+    if not lines:
+        raise err(1, "empty file")
+    tok = lines[0].split() + [""] * 5
+    banner, obj, fmt, field_, sym = tok[:5]
+    if banner != "%%MatrixMarket" or obj.lower() != "matrix":
+        raise err(1, "not a MatrixMarket matrix header")
+    fmt, field_, sym = fmt.lower(), field_.lower(), sym.lower()
+    if field_ in ("complex", "pattern"):
+        raise err(1, f"unsupported field '{field_}' (real data required)")
+    if field_ not in ("real", "integer", "double"):
+        raise err(1, f"unknown field '{field_}'")
+    if sym not in ("general", "symmetric", "skew-symmetric"):
+        raise err(1, f"unsupported symmetry '{sym}'")
+    state = {"line": 1, "pos": 1}
+
+    def next_data():
+        while state["pos"] < len(lines):
+            ln = lines[state["pos"]]
+            state["pos"] += 1
+            state["line"] += 1
+            st = ln.lstrip(" \t\r")
+            if st == "" or st.startswith("%"):
+                continue
+            return ln
+        return None
+
+    def ints(ln, k):
+        parts = ln.split()
+        return [int(x) for x in parts[:k]] if len(parts) >= k else None
+
+    ln = next_data()
+    if ln is None:
+        raise err(state["line"], "missing size line")
+    if fmt == "array":
+        try:
+            rows, cols = ints(ln, 2)
+        except (TypeError, ValueError):
+            raise err(state["line"], "bad array size line")
+        if rows < 1 or cols < 1:
+            raise err(state["line"], "bad array size line")
+        a = np.zeros((rows, cols))
+        for j in range(cols):
+            for i in range(0 if sym == "general" else j, rows):
+                ln = next_data()
+                if ln is None:
+                    raise err(state["line"], "unexpected end of array data")
+                try:
+                    v = float(ln.split()[0])
+                except (IndexError, ValueError):
+                    raise err(state["line"], "bad array value")
+                a[i, j] = v
+                if sym == "symmetric":
+                    a[j, i] = v
+                if sym == "skew-symmetric":
+                    a[j, i] = -v
+        return ProblemMatrix(a)
+    if fmt != "coordinate":
+        raise err(1, f"unknown format '{fmt}'")
+    try:
+        rows, cols, nnz = ints(ln, 3)
+    except (TypeError, ValueError):
+        raise err(state["line"], "bad coordinate size line")
+    if rows < 1 or cols < 1 or nnz < 0:
+        raise err(state["line"], "bad coordinate size line")
+    trip = []
+    for _ in range(nnz):
+        ln = next_data()
+        if ln is None:
+            raise err(state["line"], "unexpected end of coordinate data")
+        parts = ln.split()
+        try:
+            i, j, v = int(parts[0]), int(parts[1]), float(parts[2])
+        except (IndexError, ValueError):
+            raise err(state["line"], "bad coordinate entry")
+        if i < 1 or i > rows or j < 1 or j > cols:
+            raise err(state["line"], "index out of range")
+        trip.append((i - 1, j - 1, v))
+        if sym != "general" and i != j:
+            trip.append((j - 1, i - 1, v if sym == "symmetric" else -v))
+    acc = {}
+    for i, j, v in trip:                       # setFromTriplets: duplicates summed in file order
+        acc[(i, j)] = acc[(i, j)] + v if (i, j) in acc else v
+    keys = sorted(acc, key=lambda ij: (ij[1], ij[0]))
+    data = np.array([acc[k] for k in keys], dtype=np.float64)
+    ri = np.array([k[0] for k in keys], dtype=np.int64)
+    ci = np.array([k[1] for k in keys], dtype=np.int64)
+    colptr = np.zeros(cols + 1, dtype=np.int64)
+    np.add.at(colptr, ci + 1, 1)
+    return ProblemMatrix(sp.csc_matrix((data, ri, np.cumsum(colptr)), shape=(rows, cols)))
 
 
 # ----------------------------------------------------------------------------- shifted solves

@@ -1,6 +1,7 @@
 // Launchers for the sm_100a kernels of the shifted-solve path (internal C++ interface).
 #pragma once
 #include <cstddef>
+#include <cstdint>
 #include <cuda_runtime.h>
 
 namespace sssvd_gpu {
@@ -77,5 +78,12 @@ cudaError_t gather_cols(const double* src, int lds, const int* perm, const doubl
                         int cols, double* dst, int ldd, cudaStream_t st);
 cudaError_t sumsq(const double* a, long long count, double* scratch, double* out, cudaStream_t s);
 cudaError_t pad_copy(const double* src, int rows, int cols, int lds, double* dst, int ldd, cudaStream_t s);
+// sparse ingest (sparse.cu): CSC validation (sets *bad) and densify into a zeroed operator
+cudaError_t csc_check(const int64_t* colptr, const int64_t* rowind, int64_t rows, int64_t cols, int64_t nnz,
+                      int* bad, cudaStream_t s);
+cudaError_t csc_scatter(const int64_t* colptr, const int64_t* rowind, const double* vals, int64_t cols,
+                        bool transposed, double* Ad, int64_t ldp, cudaStream_t s);
+// *bad |= 1 if any of a[0..count) is NaN / Inf (sparse.cu)
+cudaError_t any_nonfinite(const double* a, long long count, int* bad, cudaStream_t s);
 
 }  // namespace sssvd_gpu

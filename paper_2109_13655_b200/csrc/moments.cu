@@ -175,7 +175,7 @@ cudaError_t sumsq(const double* a, long long count, double* scratch /*>= 593 dou
   return cudaGetLastError();
 }
 
-// column-major (rows x cols, lda)  ->  row-major [rows][cols] complex with zero imaginary part
+// column-major rows x cols (leading dim lds) -> column-major with leading dim ldd >= rows, zero rows beyond
 __global__ void pad_copy_kernel(const double* __restrict__ src, int rows, int cols, int lds,
                                 double* __restrict__ dst, int ldd) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)ldd * cols;

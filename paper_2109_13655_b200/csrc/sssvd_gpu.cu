@@ -490,6 +490,25 @@ static void allreduce_S(sssvd_gpu_ctx* ctx, double* S, size_t count) {
   CKN(nccl().AllReduce(S, S, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
 }
 
+// common tail of set_operator / set_operator_csc: NaN / Inf check (problem.hpp:56-58, :29-33 for
+// sparse) and the operator bookkeeping
+static void finish_operator(sssvd_gpu_ctx* ctx, int64_t m, int64_t n, int64_t ldp, bool tr) {
+  cudaStream_t s = ctx->stream;
+  int* bad = ctx->scratch.as<int>(2048) + 2044;
+  CK(cudaMemsetAsync(bad, 0, sizeof(int), s));
+  CK(any_nonfinite(ctx->A.as<double>(0), (long long)ldp * n, bad, s));
+  int hbad = 0;
+  CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (hbad) throw Status(SSSVD_E_INVALID_ARGUMENT, "ProblemMatrix: NaN/Inf entry");
+  ctx->m = m;
+  ctx->n = n;
+  ctx->lda = ldp;
+  ctx->transposed = tr;
+  ctx->has_gram = false;
+  ctx->fact_valid = false;
+}
+
 // Gram of the current operator into ctx->G (row-major == column-major, symmetric) + max|G|
 static void ensure_gram(sssvd_gpu_ctx* ctx, int64_t cap) {
   if (ctx->n <= 0) throw Status(SSSVD_E_INVALID_ARGUMENT, "no operator set");
@@ -1166,19 +1185,50 @@ sssvd_status sssvd_gpu_set_operator(sssvd_gpu_ctx* ctx, const double* a, int64_t
                       tmp, (int)m));
       CK(pad_copy(tmp, (int)m, (int)n, (int)m, Ad, (int)ldp, s));
     }
-    // NaN / Inf check (problem.hpp:56-58): sum of squares is finite iff every entry is
-    double* scratch = ctx->scratch.as<double>(1024);
-    CK(sumsq(Ad, (long long)ldp * n, scratch, scratch + 1000, s));
-    double ss = 0;
-    CK(cudaMemcpyAsync(&ss, scratch + 1000, sizeof(double), cudaMemcpyDeviceToHost, s));
+    finish_operator(ctx, m, n, ldp, tr);
+  });
+}
+
+sssvd_status sssvd_gpu_set_operator_csc(sssvd_gpu_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz,
+                                        const int64_t* colptr, const int64_t* rowind, const double* values,
+                                        int on_device) {
+  return guarded(ctx, [&]() {
+    if (rows <= 0 || cols <= 0 || nnz < 0) throw Status(SSSVD_E_INVALID_ARGUMENT, "set_operator_csc: bad shape");
+    if (!colptr || (nnz > 0 && (!rowind || !values)))
+      throw Status(SSSVD_E_INVALID_ARGUMENT, "set_operator_csc: null array");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const bool tr = rows < cols;
+    const int64_t m = tr ? cols : rows, n = tr ? rows : cols;
+    const int64_t ldp = (m + 7) / 8 * 8;
+    // stage colptr | rowind | values in one device buffer (8-byte elements throughout)
+    const int64_t nz = std::max<int64_t>(nnz, 1);
+    const int64_t *cp = colptr, *ri = rowind;
+    const double* va = values;
+    if (!on_device) {
+      int64_t* st = ctx->t0.as<int64_t>((size_t)(cols + 1 + 2 * nz));
+      CK(cudaMemcpyAsync(st, colptr, sizeof(int64_t) * (cols + 1), cudaMemcpyHostToDevice, s));
+      if (nnz > 0) {
+        CK(cudaMemcpyAsync(st + cols + 1, rowind, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(st + cols + 1 + nz, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+      }
+      cp = st;
+      ri = st + cols + 1;
+      va = reinterpret_cast<const double*>(st + cols + 1 + nz);
+    }
+    int* bad = ctx->scratch.as<int>(2048) + 2040;   // past the doubles sumsq uses (<= index 1000)
+    CK(cudaMemsetAsync(bad, 0, sizeof(int), s));
+    CK(csc_check(cp, ri, rows, cols, nnz, bad, s));
+    int hbad = 0;
+    CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    if (!std::isfinite(ss)) throw Status(SSSVD_E_INVALID_ARGUMENT, "ProblemMatrix: NaN/Inf entry");
-    ctx->m = m;
-    ctx->n = n;
-    ctx->lda = ldp;
-    ctx->transposed = tr;
-    ctx->has_gram = false;
-    ctx->fact_valid = false;
+    if (hbad)
+      throw Status(SSSVD_E_INVALID_ARGUMENT,
+                   "set_operator_csc: not a compressed CSC matrix (colptr/rowind out of range or unsorted)");
+    double* Ad = ctx->A.as<double>((size_t)ldp * n);
+    CK(cudaMemsetAsync(Ad, 0, sizeof(double) * ldp * n, s));
+    CK(csc_scatter(cp, ri, va, cols, tr, Ad, ldp, s));
+    finish_operator(ctx, m, n, ldp, tr);
   });
 }
 

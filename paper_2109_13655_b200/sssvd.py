@@ -5,6 +5,7 @@ names, argument meanings and error behaviour for the shifted-solve path so the p
 like the reference's own tests:
 
     ProblemMatrix.from_dense   problem.hpp:20-25       form_gram            problem.hpp:81-95
+    ProblemMatrix.from_sparse  problem.hpp:27-35       read/write_matrix_market matrix_market.hpp:34-149
     ContourRule / build_contour contour.hpp:27-62     SpectralTransform     transform.hpp:16-45
     SsParams (+ validate)      moments.hpp:23-47       random_start         moments.hpp:84-94
     ShiftedFactorization       shifted_solver.hpp:20-40 (factor_shift / solve_block :77-87)
@@ -51,7 +52,11 @@ class CudaError(RuntimeError):
     pass
 
 
-SSSVD_OK, E_INVALID, E_DOMAIN, E_LENGTH, E_NUMERICAL, E_EMPTY, E_CUDA, E_NCCL, E_OOM = range(9)
+class MatrixMarketError(RuntimeError):
+    """matrix_market.hpp:17-21: "path:line: what"."""
+
+
+SSSVD_OK, E_INVALID, E_DOMAIN, E_LENGTH, E_NUMERICAL, E_EMPTY, E_CUDA, E_NCCL, E_OOM, E_FORMAT, E_IO = range(11)
 
 
 def _raise(code: int, msg: str):
@@ -65,6 +70,10 @@ def _raise(code: int, msg: str):
         raise NumericalError(msg)
     if code == E_EMPTY:
         raise EmptySubspaceError(msg)
+    if code == E_FORMAT:
+        raise MatrixMarketError(msg)
+    if code == E_IO:
+        raise RuntimeError(msg)
     raise CudaError(f"status {code}: {msg}")
 
 
@@ -109,7 +118,14 @@ EXPORTED_SYMBOLS = [
     "sssvd_result_free", "sssvd_contour", "sssvd_random_start", "sssvd_validate_params",
     "sssvd_moment_coefficients", "sssvd_build_info", "sssvd_gpu_launch_count", "sssvd_gpu_profile_gemm",
     "sssvd_gpu_profile_gemm_collect", "sssvd_debug_leaf_profile", "sssvd_debug_gram_part",
+    "sssvd_gpu_set_operator_csc", "sssvd_mm_read", "sssvd_mm_info_get", "sssvd_mm_values", "sssvd_mm_colptr",
+    "sssvd_mm_rowind", "sssvd_mm_free", "sssvd_mm_write", "sssvd_host_last_error",
 ]
+
+class _MmInfo(ctypes.Structure):
+    _fields_ = [("rows", ctypes.c_int64), ("cols", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("sparse", ctypes.c_int)]
+
 
 _lib = None
 
@@ -134,7 +150,18 @@ def lib():
     L.sssvd_shard_range.argtypes = [i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.sssvd_shard_range.restype = None
     L.sssvd_gpu_set_operator.argtypes = [vp, dp, i64, i64, i64, ip]
+    L.sssvd_gpu_set_operator_csc.argtypes = [vp, i64, i64, i64, dp, dp, dp, ip]
     L.sssvd_gpu_form_gram.argtypes = [vp, i64, dp]
+    L.sssvd_mm_read.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
+    L.sssvd_mm_info_get.argtypes = [vp, ctypes.POINTER(_MmInfo)]
+    L.sssvd_mm_info_get.restype = None
+    for f in ("sssvd_mm_values", "sssvd_mm_colptr", "sssvd_mm_rowind"):
+        getattr(L, f).argtypes = [vp]
+        getattr(L, f).restype = vp
+    L.sssvd_mm_free.argtypes = [vp]
+    L.sssvd_mm_free.restype = None
+    L.sssvd_mm_write.argtypes = [ctypes.c_char_p, i64, i64, i64, dp, dp, dp, ctypes.c_char_p]
+    L.sssvd_host_last_error.restype = ctypes.c_char_p
     L.sssvd_gpu_shifted_solve.argtypes = [vp, dp, i64, ctypes.c_double, ctypes.c_double, dp, i64, i64, dp]
     L.sssvd_gpu_moments.argtypes = [vp, i64, dp, dp, dp, dp, i64, i64, i64, dp]
     L.sssvd_gpu_run_solve.argtypes = [vp, ctypes.POINTER(_Config), ctypes.POINTER(vp)]
@@ -372,6 +399,25 @@ class Device:
         self.check(lib().sssvd_gpu_set_operator(self.h, _ptr(a), a.shape[0], a.shape[1], a.shape[0], 0))
         self._n = min(a.shape)
 
+    def set_operator_csc(self, rows: int, cols: int, colptr: np.ndarray, rowind: np.ndarray, values: np.ndarray):
+        """Sparse operator in the user orientation (problem.hpp:27-35), compressed CSC."""
+        colptr = np.ascontiguousarray(colptr, dtype=np.int64)
+        rowind = np.ascontiguousarray(rowind, dtype=np.int64)
+        values = np.ascontiguousarray(values, dtype=np.float64)
+        if colptr.size != cols + 1 or rowind.size != values.size:
+            raise ValueError("set_operator_csc: array sizes do not match the shape")
+        self.check(lib().sssvd_gpu_set_operator_csc(self.h, rows, cols, values.size, _ptr(colptr), _ptr(rowind),
+                                                    _ptr(values), 0))
+        self._n = min(rows, cols)
+
+    def set_problem(self, a: "ProblemMatrix"):
+        """Upload a ProblemMatrix (dense or sparse) in its user orientation."""
+        if a.is_sparse():
+            s = a.sparse().T.tocsc() if a.transposed() else a.sparse()
+            self.set_operator_csc(s.shape[0], s.shape[1], s.indptr, s.indices, s.data)
+        else:
+            self.set_operator(a.dense().T if a.transposed() else a.dense())
+
     def set_operator_device(self, ptr: int, rows: int, cols: int, lda: int):
         self.check(lib().sssvd_gpu_set_operator(self.h, ctypes.c_void_p(ptr), rows, cols, lda, 1))
         self._n = min(rows, cols)
@@ -403,11 +449,13 @@ def default_device() -> Device:
 
 # ----------------------------------------------------------------------------- problem / Gram
 class ProblemMatrix:
-    """problem.hpp:14-77 (dense). Auto-transpose and the NaN check also run in the library."""
+    """problem.hpp:14-77: dense or sparse (scipy CSC) storage, normalised so rows >= cols (wide
+    inputs stored transposed and flagged). The NaN/Inf check also runs in the library."""
 
-    def __init__(self, a: np.ndarray, transposed: bool):
+    def __init__(self, a, transposed: bool, sparse: bool = False):
         self._a = a
         self._transposed = transposed
+        self._sparse = sparse
 
     @staticmethod
     def from_dense(a) -> "ProblemMatrix":
@@ -417,10 +465,86 @@ class ProblemMatrix:
         tr = a.shape[0] < a.shape[1]
         return ProblemMatrix(np.asfortranarray(a.T if tr else a), tr)
 
+    @staticmethod
+    def from_sparse(a) -> "ProblemMatrix":
+        """problem.hpp:27-35. `a` is any scipy.sparse matrix/array; stored compressed CSC
+        (duplicates summed, row indices sorted, explicit zeros kept) like Eigen's SparseMatrix."""
+        import scipy.sparse as sp
+        s = sp.csc_matrix(a, dtype=np.float64, copy=True)
+        s.sum_duplicates()
+        s.sort_indices()
+        if not np.all(np.isfinite(s.data)):
+            raise ValueError("ProblemMatrix: NaN/Inf entry")
+        tr = s.shape[0] < s.shape[1]
+        if tr:
+            s = s.T.tocsc()
+            s.sort_indices()
+        return ProblemMatrix(s, tr, True)
+
     def rows(self): return self._a.shape[0]
     def cols(self): return self._a.shape[1]
     def transposed(self): return self._transposed
-    def dense(self): return self._a
+    def is_sparse(self): return self._sparse
+
+    def dense(self):
+        if self._sparse:
+            raise TypeError("ProblemMatrix: sparse storage (use sparse() or to_dense())")
+        return self._a
+
+    def sparse(self):
+        if not self._sparse:
+            raise TypeError("ProblemMatrix: dense storage")
+        return self._a
+
+    def to_dense(self):
+        """Densified copy regardless of storage (problem.hpp:60-64; tests only)."""
+        return np.asfortranarray(self._a.toarray()) if self._sparse else self._a
+
+
+def read_matrix_market(path: str) -> ProblemMatrix:
+    """matrix_market.hpp:34-119 through the library's C++ reader (sssvd_mm_read)."""
+    L = lib()
+    h = ctypes.c_void_p()
+    st = L.sssvd_mm_read(os.fsencode(path), ctypes.byref(h))
+    if st != SSSVD_OK:
+        _raise(st, L.sssvd_host_last_error().decode())
+    try:
+        info = _MmInfo()
+        L.sssvd_mm_info_get(h, ctypes.byref(info))
+
+        def arr(fn, count, ctype, dtype):
+            if count == 0:
+                return np.empty(0, dtype=dtype)
+            p = ctypes.cast(fn(h), ctypes.POINTER(ctype))
+            return np.ctypeslib.as_array(p, shape=(count,)).copy()
+
+        vals = arr(L.sssvd_mm_values, info.nnz, ctypes.c_double, np.float64)
+        if not info.sparse:
+            return ProblemMatrix.from_dense(vals.reshape((info.cols, info.rows)).T)
+        import scipy.sparse as sp
+        colptr = arr(L.sssvd_mm_colptr, info.cols + 1, ctypes.c_int64, np.int64)
+        rowind = arr(L.sssvd_mm_rowind, info.nnz, ctypes.c_int64, np.int64)
+        return ProblemMatrix.from_sparse(sp.csc_matrix((vals, rowind, colptr), shape=(info.rows, info.cols)))
+    finally:
+        L.sssvd_mm_free(h)
+
+
+def write_matrix_market(path: str, a: ProblemMatrix, comment: str = "") -> None:
+    """matrix_market.hpp:121-149: the caller's original orientation, 17 significant digits."""
+    L = lib()
+    if a.is_sparse():
+        s = a.sparse().T.tocsc() if a.transposed() else a.sparse()
+        cp = np.ascontiguousarray(s.indptr, dtype=np.int64)
+        ri = np.ascontiguousarray(s.indices, dtype=np.int64)
+        va = np.ascontiguousarray(s.data, dtype=np.float64)
+        st = L.sssvd_mm_write(os.fsencode(path), s.shape[0], s.shape[1], va.size, _ptr(cp), _ptr(ri), _ptr(va),
+                              comment.encode())
+    else:
+        d = np.asfortranarray(a.dense().T if a.transposed() else a.dense())
+        st = L.sssvd_mm_write(os.fsencode(path), d.shape[0], d.shape[1], d.size, None, None, _ptr(d),
+                              comment.encode())
+    if st != SSSVD_OK:
+        _raise(st, L.sssvd_host_last_error().decode())
 
 
 def form_gram(a: ProblemMatrix, size_cap: int = 8192, device: Optional[Device] = None) -> np.ndarray:
@@ -428,7 +552,7 @@ def form_gram(a: ProblemMatrix, size_cap: int = 8192, device: Optional[Device] =
     dev = device or default_device()
     if a.cols() > size_cap:
         raise LengthError("form_gram: column count exceeds the dense Gram cap")
-    dev.set_operator(a.dense())
+    dev.set_problem(a)
     return dev.form_gram(size_cap)
 
 
@@ -656,8 +780,7 @@ def run_solve(a, config: RunConfig, device: Optional[Device] = None) -> RunResul
     orientation); the library auto-transposes wide inputs like ProblemMatrix::from_dense."""
     dev = device or default_device()
     if isinstance(a, ProblemMatrix):
-        arr = a.dense().T if a.transposed() else a.dense()
+        dev.set_problem(a)
     else:
-        arr = np.asarray(a, dtype=np.float64)
-    dev.set_operator(arr)
+        dev.set_operator(np.asarray(a, dtype=np.float64))
     return dev.run_solve(config)
