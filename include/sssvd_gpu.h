@@ -185,6 +185,16 @@ sssvd_status sssvd_validate_params(const sssvd_params* p, int64_t n);
  * moments.hpp:138-144), complex interleaved, row k at offset 2*k*h. */
 sssvd_status sssvd_moment_coefficients(int64_t h, const double* weights, const double* nodes, int64_t M,
                                        double* coef_out);
+/* Model problems (problems.hpp:50-70): A = U diag(sigma) V^T from the model-seeded libstdc++ normal
+ * stream, Householder Q factors; which = 1 (sigma_i = 0.005 + 0.01 i) or 2 (10^(-10 + 0.05 i)).
+ * a_out rows x cols column-major, sigma_out[cols] ascending (may be NULL). rows >= cols. */
+sssvd_status sssvd_build_model(int which, int64_t rows, int64_t cols, uint64_t seed, double* a_out,
+                               double* sigma_out);
+/* filter_profile (filter.hpp:36-55): grid[points] and |f(sigma)| values[points] of the rational
+ * filter of the quadrature rule; log_spacing != 0 for a log grid. */
+sssvd_status sssvd_filter_profile(double a, double b, int64_t count, double aspect, int transform,
+                                  double sigma_min, double sigma_max, int64_t points, int log_spacing,
+                                  double* grid, double* values);
 /* Instrumentation: number of kernels this library launched so far (process-wide), and live
  * CUDA-event timing of the dominant kernel (the DMMA trailing update) while enabled. */
 uint64_t sssvd_gpu_launch_count(void);

@@ -31,6 +31,11 @@ class DeviceError : public std::runtime_error {
  public:
   explicit DeviceError(const std::string& w) : std::runtime_error(w) {}
 };
+// matrix_market.hpp:17-21 ("path:line: what")
+class MatrixMarketError : public std::runtime_error {
+ public:
+  explicit MatrixMarketError(const std::string& w) : std::runtime_error(w) {}
+};
 
 inline void check(sssvd_status st, const sssvd_gpu_ctx* ctx) {
   if (st == SSSVD_OK) return;
@@ -41,6 +46,8 @@ inline void check(sssvd_status st, const sssvd_gpu_ctx* ctx) {
     case SSSVD_E_LENGTH: throw std::length_error(msg);
     case SSSVD_E_NUMERICAL: throw NumericalError(msg);
     case SSSVD_E_EMPTY_SUBSPACE: throw EmptySubspaceError(msg);
+    case SSSVD_E_FORMAT: throw MatrixMarketError(msg);
+    case SSSVD_E_IO: throw std::runtime_error(msg);
     default: throw DeviceError(msg + " (status " + std::to_string(int(st)) + ")");
   }
 }
@@ -67,6 +74,11 @@ class Device {
   // ProblemMatrix::from_dense + upload (problem.hpp:20-25): column-major rows x cols
   void set_operator(const double* a, int64_t rows, int64_t cols, int64_t lda) {
     check(sssvd_gpu_set_operator(ctx_, a, rows, cols, lda, 0), ctx_);
+  }
+  // ProblemMatrix::from_sparse + upload (problem.hpp:27-35): compressed CSC, user orientation
+  void set_operator_csc(int64_t rows, int64_t cols, const int64_t* colptr, const int64_t* rowind,
+                        const double* values, int64_t nnz) {
+    check(sssvd_gpu_set_operator_csc(ctx_, rows, cols, nnz, colptr, rowind, values, 0), ctx_);
   }
   // form_gram (problem.hpp:81-95); g_out may be nullptr
   void form_gram(int64_t cap = 8192, double* g_out = nullptr) {
@@ -123,11 +135,57 @@ class Result {
     return out;
   }
   std::string note() const { return sssvd_result_note(r_); }
+  sssvd_gpu_result* raw() const { return r_; }
 
  private:
   sssvd_gpu_result* r_;
   sssvd_result_info info_{};
 };
+
+// Host-only calls report through sssvd_host_last_error().
+inline void check_host(sssvd_status st) {
+  if (st == SSSVD_OK) return;
+  const std::string msg = sssvd_host_last_error();
+  switch (st) {
+    case SSSVD_E_FORMAT: throw MatrixMarketError(msg);
+    case SSSVD_E_IO: throw std::runtime_error(msg);
+    case SSSVD_E_DOMAIN: throw std::domain_error(msg);
+    default: throw std::invalid_argument(msg);
+  }
+}
+
+// read_matrix_market (matrix_market.hpp:34-119) in the file's orientation: dense column-major
+// `values` (colptr/rowind empty) or compressed CSC.
+struct MarketMatrix {
+  int64_t rows = 0, cols = 0;
+  bool sparse = false;
+  std::vector<double> values;
+  std::vector<int64_t> colptr, rowind;
+};
+
+inline MarketMatrix read_matrix_market(const std::string& path) {
+  sssvd_mm_matrix* h = nullptr;
+  check_host(sssvd_mm_read(path.c_str(), &h));
+  sssvd_mm_info info{};
+  sssvd_mm_info_get(h, &info);
+  MarketMatrix m;
+  m.rows = info.rows;
+  m.cols = info.cols;
+  m.sparse = info.sparse != 0;
+  m.values.assign(sssvd_mm_values(h), sssvd_mm_values(h) + info.nnz);
+  if (m.sparse) {
+    m.colptr.assign(sssvd_mm_colptr(h), sssvd_mm_colptr(h) + info.cols + 1);
+    m.rowind.assign(sssvd_mm_rowind(h), sssvd_mm_rowind(h) + info.nnz);
+  }
+  sssvd_mm_free(h);
+  return m;
+}
+
+inline void write_matrix_market(const std::string& path, const MarketMatrix& m, const std::string& comment = {}) {
+  check_host(sssvd_mm_write(path.c_str(), m.rows, m.cols, (int64_t)m.values.size(),
+                            m.sparse ? m.colptr.data() : nullptr, m.sparse ? m.rowind.data() : nullptr,
+                            m.values.data(), comment.c_str()));
+}
 
 inline Result run_solve(Device& dev, const sssvd_config& cfg) {
   sssvd_gpu_result* r = nullptr;

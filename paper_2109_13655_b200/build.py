@@ -18,12 +18,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libsssvd_gpu.so")
+CLI = os.path.join(HERE, "sssvd-gpu")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
             "--expt-relaxed-constexpr", "-I", CSRC]
 CU_SOURCES = ["zgemm.cu", "lu.cu", "gram.cu", "moments.cu", "jacobi_svd.cu", "sparse.cu", "sssvd_gpu.cu"]
-CXX_SOURCES = ["host_mirror.cpp", "matrix_market.cpp"]
+CXX_SOURCES = ["host_mirror.cpp", "matrix_market.cpp", "problems.cpp"]
 
 
 def _run(cmd, log):
@@ -65,6 +66,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if force or jobs or _stale(LIB, objs):
         _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs +
              ["-lcublas", "-lcusolver", "-ldl"], os.path.join(BUILD, "link.log"))
+    # the command-line front end (proj/tools/sssvd.cpp) over the C ABI, rpath'ed to this directory
+    cli_src = os.path.join(CSRC, "cli.cpp")
+    hpp = os.path.join(HERE, "..", "include", "sssvd_gpu.hpp")
+    if force or _stale(CLI, [cli_src, LIB, hpp] + headers):
+        _run(["g++", "-O2", "-std=c++20", cli_src, "-o", CLI, "-L", HERE, "-lsssvd_gpu",
+              "-L/usr/local/cuda/lib64", "-Wl,-rpath,$ORIGIN"], os.path.join(BUILD, "cli.log"))
     if verbose:
         print(LIB)
     return LIB

@@ -119,7 +119,8 @@ EXPORTED_SYMBOLS = [
     "sssvd_moment_coefficients", "sssvd_build_info", "sssvd_gpu_launch_count", "sssvd_gpu_profile_gemm",
     "sssvd_gpu_profile_gemm_collect", "sssvd_debug_leaf_profile", "sssvd_debug_gram_part",
     "sssvd_gpu_set_operator_csc", "sssvd_mm_read", "sssvd_mm_info_get", "sssvd_mm_values", "sssvd_mm_colptr",
-    "sssvd_mm_rowind", "sssvd_mm_free", "sssvd_mm_write", "sssvd_host_last_error",
+    "sssvd_mm_rowind", "sssvd_mm_free", "sssvd_mm_write", "sssvd_host_last_error", "sssvd_build_model",
+    "sssvd_filter_profile",
 ]
 
 class _MmInfo(ctypes.Structure):
@@ -162,6 +163,9 @@ def lib():
     L.sssvd_mm_free.restype = None
     L.sssvd_mm_write.argtypes = [ctypes.c_char_p, i64, i64, i64, dp, dp, dp, ctypes.c_char_p]
     L.sssvd_host_last_error.restype = ctypes.c_char_p
+    L.sssvd_build_model.argtypes = [ctypes.c_int, i64, i64, ctypes.c_uint64, dp, dp]
+    L.sssvd_filter_profile.argtypes = [ctypes.c_double, ctypes.c_double, i64, ctypes.c_double, ctypes.c_int,
+                                       ctypes.c_double, ctypes.c_double, i64, ctypes.c_int, dp, dp]
     L.sssvd_gpu_shifted_solve.argtypes = [vp, dp, i64, ctypes.c_double, ctypes.c_double, dp, i64, i64, dp]
     L.sssvd_gpu_moments.argtypes = [vp, i64, dp, dp, dp, dp, i64, i64, i64, dp]
     L.sssvd_gpu_run_solve.argtypes = [vp, ctypes.POINTER(_Config), ctypes.POINTER(vp)]
@@ -499,6 +503,29 @@ class ProblemMatrix:
     def to_dense(self):
         """Densified copy regardless of storage (problem.hpp:60-64; tests only)."""
         return np.asfortranarray(self._a.toarray()) if self._sparse else self._a
+
+
+def build_model(which: int = 1, rows: int = 1000, cols: int = 200, seed: int = 7):
+    """problems.hpp:50-70 (host generator in the library): (ProblemMatrix, sigma ascending)."""
+    a = np.empty((rows, cols), order="F")
+    s = np.empty(cols)
+    st = lib().sssvd_build_model(which, rows, cols, seed, _ptr(a), _ptr(s))
+    if st != SSSVD_OK:
+        _raise(st, "build_model: needs rows >= cols and model 1 or 2")
+    return ProblemMatrix.from_dense(a), s
+
+
+def filter_profile(rule: "ContourRule", sigma_min: float, sigma_max: float, points: int, log_spacing: bool = False):
+    """filter.hpp:36-55: (grid, |f(grid)|)."""
+    if points < 1:
+        raise ValueError("filter_profile: need at least one point")
+    grid, vals = np.empty(points), np.empty(points)
+    st = lib().sssvd_filter_profile(rule.interval_a(), rule.interval_b(), rule.count(), rule.aspect(),
+                                    rule.transform().kind(), sigma_min, sigma_max, points, int(log_spacing),
+                                    _ptr(grid), _ptr(vals))
+    if st != SSSVD_OK:
+        _raise(st, "filter_profile: need 0 < sigma_min < sigma_max")
+    return grid, vals
 
 
 def read_matrix_market(path: str) -> ProblemMatrix:
