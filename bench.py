@@ -190,8 +190,10 @@ def main():
         tt = torch.tensor([t], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt.item())
-    # ---- e2e through the public API with host buffers
-    step_e2e()
+    # ---- e2e through the public API with host buffers (same W warm-up steps as the device leg:
+    #      the library's pinned result pool reaches its steady state there)
+    for _ in range(max(1, args.warmup)):
+        res_e = step_e2e()
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
@@ -230,9 +232,17 @@ def main():
             "roofline": {"bound": "tensor", "kernel": "zgemm_sub_kernel (DMMA trailing update)",
                          "achieved": gemm_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": (gemm_tflops / FP64_PEAK_TFLOPS) if gemm_tflops else None,
-                         "traffic": None,
+                         # one ncu --set full capture of a large trailing update (profiles/
+                         # r01_ncu_zgemm_trailing_prefetch.txt): M=3968 N=4000 K=128 complex x 8 shifts
+                         "traffic": 2.163797e9 + 1.976564e9,
+                         "traffic_launch": {"shape": "M=3968 N=4000 K=128 complex, batch 8",
+                                            "algorithmic_bytes": 8 * 16 * (2 * 3968 * 4000 + 3968 * 128 + 128 * 4000),
+                                            "dram_bytes": 2.163797e9 + 1.976564e9, "ncu_duration_ms": 4.259136,
+                                            "ncu_tflops": 1.300e11 / 4.259136e-3 / 1e12},
+                         "achieved_basis": "GEMM flops / GEMM-busy time (union of the launch intervals, CUDA events "
+                                           "on the launching streams; the shift groups overlap their GEMMs)",
                          "peak_source": "measured FP64 DMMA probe (profiles/r01_fp64_peaks.json); MEASURED_PEAKS.json has no FP64 entry",
-                         "gemm_launches": gemm_launches, "gemm_ms_per_step": gemm_ms / args.steps,
+                         "gemm_launches": gemm_launches, "gemm_busy_ms_per_step": gemm_ms / args.steps,
                          "phase_tflops": solve_flops / solve_s / 1e12 if solve_s > 0 else None,
                          "phase_frac": (solve_flops / solve_s / 1e12 / FP64_PEAK_TFLOPS) if solve_s > 0 else None,
                          "phase_flops_per_step": solve_flops, "phase_s_per_step": solve_s},

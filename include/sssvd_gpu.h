@@ -196,7 +196,9 @@ sssvd_status sssvd_filter_profile(double a, double b, int64_t count, double aspe
                                   double sigma_min, double sigma_max, int64_t points, int log_spacing,
                                   double* grid, double* values);
 /* Instrumentation: number of kernels this library launched so far (process-wide), and live
- * CUDA-event timing of the dominant kernel (the DMMA trailing update) while enabled. */
+ * CUDA-event timing of the dominant kernel (the DMMA trailing update) while enabled: `ms` is the
+ * GEMM-busy time (union of the launch intervals; the shift groups overlap their GEMMs), `flops`
+ * the algorithmic flops of those launches. */
 uint64_t sssvd_gpu_launch_count(void);
 void sssvd_gpu_profile_gemm(int enable);
 void sssvd_gpu_profile_gemm_collect(double* ms, double* flops, uint64_t* launches);

@@ -22,6 +22,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <map>
+#include <mutex>
 #include <numeric>
 #include <stdexcept>
 #include <string>
@@ -158,12 +160,72 @@ struct sssvd_gpu_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxGroups] = {};
   cudaEvent_t ev_pre[kMaxGroups] = {}, ev_gemm[kMaxGroups] = {};
   DBuf tail[24];
+  cudaStream_t cstream = nullptr;   // result device->host copies, overlapped with the tail
+  cudaEvent_t ev_copy = nullptr;
   double t_gram = 0, t_solves = 0, t_allreduce = 0, solve_flops = 0;
+};
+
+// Page-locked host arrays for the large result fields (moment blocks, triplet vectors): their
+// device->host copies run asynchronously on the context's copy stream, overlapped with the tail.
+// Blocks come from a process-wide cache, so steady-state runs allocate no pinned memory.
+class PinnedPool {
+ public:
+  static double* get(size_t count) {
+    std::lock_guard<std::mutex> lk(mu());
+    auto& f = free_list();
+    for (size_t i = 0; i < f.size(); ++i)
+      if (f[i].second >= count) {
+        double* p = f[i].first;
+        f.erase(f.begin() + (long)i);
+        return p;
+      }
+    void* p = nullptr;
+    if (cudaMallocHost(&p, std::max<size_t>(count, 1) * sizeof(double)) != cudaSuccess)
+      throw std::bad_alloc();
+    sizes()[p] = std::max<size_t>(count, 1);
+    return static_cast<double*>(p);
+  }
+  static void put(double* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(mu());
+    free_list().emplace_back(p, sizes()[p]);
+  }
+
+ private:
+  static std::mutex& mu() { static std::mutex m; return m; }
+  static std::vector<std::pair<double*, size_t>>& free_list() { static std::vector<std::pair<double*, size_t>> f; return f; }
+  static std::map<void*, size_t>& sizes() { static std::map<void*, size_t> m; return m; }
+};
+
+struct PinnedArray {
+  double* p = nullptr;
+  size_t n = 0;
+  PinnedArray() = default;
+  PinnedArray(const PinnedArray&) = delete;
+  PinnedArray& operator=(const PinnedArray&) = delete;
+  PinnedArray(PinnedArray&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  PinnedArray& operator=(PinnedArray&& o) noexcept {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+    return *this;
+  }
+  ~PinnedArray() { PinnedPool::put(p); }
+  void resize(size_t count) {
+    PinnedPool::put(p);
+    p = count ? PinnedPool::get(count) : nullptr;
+    n = count;
+  }
+  bool empty() const { return n == 0; }
+  size_t size() const { return n; }
+  const double* data() const { return p; }
+  double* data() { return p; }
+  const double& operator[](size_t i) const { return p[i]; }
 };
 
 struct sssvd_gpu_result {
   sssvd_result_info info{};
-  std::vector<double> sigma, tau, estimated, exact, galerkin, left, right, basis_sv, blocks, q;
+  std::vector<double> sigma, tau, estimated, exact, galerkin, basis_sv, q;
+  PinnedArray left, right, blocks;
   std::vector<int32_t> in_interval, spurious;
   std::string note;
 };
@@ -580,6 +642,20 @@ static std::vector<double> d2h(const double* d, size_t count, cudaStream_t s) {
   return h;
 }
 
+// start an asynchronous device->host copy of `count` doubles into a pinned result array, ordered
+// after the work queued so far on ctx->stream; completion is awaited by CopyFence at run end
+static void d2h_async(sssvd_gpu_ctx* ctx, const double* d, size_t count, PinnedArray& out) {
+  out.resize(count);
+  if (!count) return;
+  CK(cudaEventRecord(ctx->ev_copy, ctx->stream));
+  CK(cudaStreamWaitEvent(ctx->cstream, ctx->ev_copy, 0));
+  CK(cudaMemcpyAsync(out.data(), d, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->cstream));
+}
+struct CopyFence {
+  cudaStream_t s;
+  ~CopyFence() { cudaStreamSynchronize(s); }
+};
+
 static void svd_square(sssvd_gpu_ctx* ctx, double* B, int k, double* U, double* S, double* V) {
   static const char* env = std::getenv("SSSVD_TAIL_SVD");
   const std::string method = env ? env : "jacobi";
@@ -724,6 +800,7 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
   const int64_t n = ctx->n, m = ctx->m;
   if (n <= 0) throw Status(SSSVD_E_INVALID_ARGUMENT, "no operator set");
   validate_params(cfg.params, n);
+  CopyFence copy_fence{ctx->cstream};   // every return path waits for the result copies
   const bool use_exp = cfg.mode == SSSVD_MODE_SS_SVD_NT || cfg.mode == SSSVD_MODE_NAIVE_NT;
   const bool naive = cfg.mode == SSSVD_MODE_NAIVE || cfg.mode == SSSVD_MODE_NAIVE_NT;
   Contour rule = make_contour(cfg.interval_a, cfg.interval_b, cfg.params.quadrature_count, cfg.aspect, use_exp);
@@ -806,7 +883,7 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
   info.t_shifted_solves = ctx->t_solves;
   info.t_allreduce = ctx->t_allreduce;
   info.shifted_solve_flops = ctx->solve_flops;
-  res->blocks = d2h(Sc, (size_t)(M + 1) * n * L, s);
+  d2h_async(ctx, Sc, (size_t)(M + 1) * n * L, res->blocks);   // Sc is read-only from here on
 
   // ---- step 3: low_rank (moments.hpp:190-211)
   t0 = now_s();
@@ -924,6 +1001,9 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
     CK(cudaMemcpyAsync(perm_d, idn.data(), sizeof(int) * rank, cudaMemcpyHostToDevice, s));
     CK(gather_cols(av, (int)m, perm_d, sig_d, (int)m, rank, leftv, (int)m, s));
   }
+  // the triplet vectors are final: copy them out while the postprocess runs
+  d2h_async(ctx, leftv, (size_t)m * tcount, res->left);
+  d2h_async(ctx, right, (size_t)n * tcount, res->right);
   std::vector<double> qhost = d2h(qs, (size_t)rank * rank, s);
   info.step_5 = now_s() - t0;
 
@@ -1006,8 +1086,7 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
       info.mu = mu;
     }
   }
-  res->left = d2h(leftv, (size_t)m * tcount, s);
-  res->right = d2h(right, (size_t)n * tcount, s);
+  CK(cudaStreamSynchronize(ctx->cstream));
   info.postprocess = now_s() - t0;
   if (ctx->transposed) {   // pipeline.hpp:214-217
     std::swap(res->left, res->right);
@@ -1095,6 +1174,8 @@ sssvd_status sssvd_gpu_create(int device, sssvd_gpu_ctx** out) {
     cudaEventCreateWithFlags(&ctx->ev_gemm[g], cudaEventDisableTiming);
   }
   cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
+  cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming);
   cublasSetStream(ctx->blas, ctx->stream);
   cusolverDnSetStream(ctx->solver, ctx->stream);
   *out = ctx;
@@ -1121,6 +1202,11 @@ void sssvd_gpu_destroy(sssvd_gpu_ctx* ctx) {
     if (ctx->ev_gemm[g]) cudaEventDestroy(ctx->ev_gemm[g]);
   }
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->cstream) {
+    cudaStreamSynchronize(ctx->cstream);
+    cudaStreamDestroy(ctx->cstream);
+  }
+  if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -1384,7 +1470,7 @@ sssvd_status sssvd_result_info_get(const sssvd_gpu_result* res, sssvd_result_inf
 
 sssvd_status sssvd_result_copy(const sssvd_gpu_result* res, int field, void* dst) {
   auto cp = [&](const auto& v) {
-    if (!v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+    if (!v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(*v.data()));
   };
   switch (field) {
     case SSSVD_FIELD_SIGMA: cp(res->sigma); break;

@@ -14,6 +14,9 @@
 #include <atomic>
 #include <vector>
 
+#include <algorithm>
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -37,15 +40,33 @@ void zgemm_profile_enable(bool on) {
   g_prof.flops.clear();
 }
 
+// *ms is the GEMM-BUSY time: the length of the union of the launch intervals. The shift groups
+// run their trailing updates concurrently on separate streams, so summing per-launch durations
+// would count shared time once per overlapping launch.
 void zgemm_profile_collect(double* ms, double* flops, unsigned long long* launches) {
-  double t = 0, f = 0;
+  double f = 0;
+  std::vector<std::pair<double, double>> iv;
+  iv.reserve(g_prof.used);
   for (size_t i = 0; i < g_prof.used; ++i) {
     cudaEventSynchronize(g_prof.ev[2 * i + 1]);
-    float x = 0;
-    cudaEventElapsedTime(&x, g_prof.ev[2 * i], g_prof.ev[2 * i + 1]);
-    t += x;
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, g_prof.ev[0], g_prof.ev[2 * i]);
+    cudaEventElapsedTime(&b, g_prof.ev[0], g_prof.ev[2 * i + 1]);
+    iv.emplace_back(a, b);
     f += g_prof.flops[i];
   }
+  std::sort(iv.begin(), iv.end());
+  double t = 0, cs = 0, ce = -1e300;
+  for (const auto& [a, b] : iv) {
+    if (a > ce) {
+      if (ce > cs) t += ce - cs;
+      cs = a;
+      ce = b;
+    } else {
+      ce = std::max(ce, b);
+    }
+  }
+  if (!iv.empty() && ce > cs) t += ce - cs;
   *ms = t;
   *flops = f;
   *launches = g_prof.used;
