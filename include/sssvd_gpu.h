@@ -205,6 +205,14 @@ void sssvd_gpu_profile_gemm_collect(double* ms, double* flops, uint64_t* launche
 /* Debug: tile share `part` of `nparts` of form_gram (the multi-GPU Gram sharding), zeros
  * elsewhere; n x n column-major. */
 sssvd_status sssvd_debug_gram_part(sssvd_gpu_ctx* ctx, int part, int nparts, double* g_out);
+/* Debug: the tail's hand-written Householder QR (HouseholderQR, moments.hpp:195-198 / extract.hpp:
+ * 43-57) on host data: a (m x k column-major, m >= k) -> thin q_out (m x k) and upper r_out (k x k). */
+sssvd_status sssvd_debug_thin_qr(sssvd_gpu_ctx* ctx, const double* a, int64_t m, int64_t k, double* q_out,
+                                 double* r_out);
+/* Debug: the tail's one-sided Jacobi SVD of a square k x k matrix b (svd_small, extract.hpp:66-70):
+ * u_out, v_out (k x k column-major), s_out[k] descending. */
+sssvd_status sssvd_debug_svd_square(sssvd_gpu_ctx* ctx, const double* b, int64_t k, double* u_out, double* s_out,
+                                    double* v_out);
 /* Debug: cycles per leaf-kernel phase summed over columns (SSSVD_LEAF_PROF=1): out[0..3] phases,
  * out[4] columns, out[5] summed CTA lifetimes, out[6] leaves (7 entries). */
 void sssvd_debug_leaf_profile(uint64_t* out7);

@@ -23,7 +23,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
             "--expt-relaxed-constexpr", "-I", CSRC]
-CU_SOURCES = ["zgemm.cu", "lu.cu", "gram.cu", "moments.cu", "jacobi_svd.cu", "sparse.cu", "sssvd_gpu.cu"]
+CU_SOURCES = ["zgemm.cu", "lu.cu", "gram.cu", "moments.cu", "jacobi_svd.cu", "householder_qr.cu", "sparse.cu", "sssvd_gpu.cu"]
 CXX_SOURCES = ["host_mirror.cpp", "matrix_market.cpp", "problems.cpp"]
 
 

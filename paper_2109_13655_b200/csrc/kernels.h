@@ -83,6 +83,14 @@ cudaError_t csc_check(const int64_t* colptr, const int64_t* rowind, int64_t rows
                       int* bad, cudaStream_t s);
 cudaError_t csc_scatter(const int64_t* colptr, const int64_t* rowind, const double* vals, int64_t cols,
                         bool transposed, double* Ad, int64_t ldp, cudaStream_t s);
+// Householder QR of the tail (householder_qr.cu): cluster panel factorisation of A[j:m, j:j+w]
+// (w <= 32) writing R/v in place, explicit Y (rows j..m, ldy) and T (32 x 32 column-major)
+size_t qr_panel_smem(int rp, int w);
+int qr_panel_plan(int mp, int w, int* cluster);
+cudaError_t qr_panel(double* A, int lda, int m, int j, int w, double* Y, int ldy, double* T, double* tau,
+                     cudaStream_t s);
+cudaError_t eye(double* Q, int m, int k, int ldq, cudaStream_t s);
+cudaError_t copy_r(const double* A, int lda, int k, double* R, cudaStream_t s);
 // *bad |= 1 if any of a[0..count) is NaN / Inf (sparse.cu)
 cudaError_t any_nonfinite(const double* a, long long count, int* bad, cudaStream_t s);
 

@@ -541,6 +541,7 @@ cudaError_t build_moves(const int* ipiv, int n, int r0, int np, int* src, int* d
 // ----------------------------------------------------------------------------- L11^{-1}
 // Linv = L11^{-1} for the unit-lower np x np block at (r0, r0): one warp per column j; lanes
 // split each dot product, a warp reduction closes it. Row-major output with pitch np.
+template <int QMAX>   // np <= 32 QMAX
 __global__ void trinv_lower_kernel(const double2* __restrict__ mats, int ld, long long stride, int r0, int np,
                                    double2* __restrict__ linv, long long lstride) {
   const int b = blockIdx.y;
@@ -549,7 +550,6 @@ __global__ void trinv_lower_kernel(const double2* __restrict__ mats, int ld, lon
   if (j >= np) return;
   const double2* Mb = mats + b * stride + (size_t)r0 * ld + r0;
   double2* out = linv + (size_t)b * lstride;
-  constexpr int QMAX = 4;   // np <= 128
   double2 x[QMAX];
 #pragma unroll
   for (int q = 0; q < QMAX; ++q) x[q] = make_double2((lane + 32 * q) == j ? 1.0 : 0.0, 0.0);
@@ -602,10 +602,13 @@ __global__ void trinv_lower_kernel(const double2* __restrict__ mats, int ld, lon
 
 cudaError_t trinv_lower(const double2* mats, int ld, long long stride, int r0, int np, double2* linv,
                         long long lstride, int batch, cudaStream_t s) {
-  if (np > 128) return cudaErrorInvalidValue;
+  if (np > 256) return cudaErrorInvalidValue;
   const int wpb = 4;
   dim3 grid((np + wpb - 1) / wpb, batch);
-  trinv_lower_kernel<<<grid, 32 * wpb, 0, s>>>(mats, ld, stride, r0, np, linv, lstride);
+  if (np <= 128)
+    trinv_lower_kernel<4><<<grid, 32 * wpb, 0, s>>>(mats, ld, stride, r0, np, linv, lstride);
+  else
+    trinv_lower_kernel<8><<<grid, 32 * wpb, 0, s>>>(mats, ld, stride, r0, np, linv, lstride);
   note_launch();
   return cudaGetLastError();
 }
@@ -640,6 +643,7 @@ cudaError_t scatter_copy(double2* mats, int ld, long long stride, int r0, int np
 // ----------------------------------------------------------------------------- back substitution
 // Rows r0..r0+np of the columns [c0,c1): x = U11^{-1} y by substitution (backward stable), one
 // warp per (column, shift); lanes split each dot product; x stays distributed over the lanes.
+template <int QMAX>   // np <= 32 QMAX
 __global__ void trsm_upper_warp_kernel(double2* mats, int ld, long long stride, int r0, int np, int c0, int c1) {
   const int b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -647,7 +651,6 @@ __global__ void trsm_upper_warp_kernel(double2* mats, int ld, long long stride, 
   if (c >= c1) return;
   double2* Mb = mats + b * stride;
   const double2* U = Mb + (size_t)r0 * ld + r0;
-  constexpr int QMAX = 4;
   double2 x[QMAX], invd[QMAX];
 #pragma unroll
   for (int q = 0; q < QMAX; ++q) {
@@ -706,10 +709,13 @@ __global__ void trsm_upper_warp_kernel(double2* mats, int ld, long long stride, 
 cudaError_t trsm_upper_warp(double2* mats, int ld, long long stride, int r0, int np, int c0, int c1, int batch,
                             cudaStream_t s) {
   if (c1 <= c0 || np <= 0) return cudaSuccess;
-  if (np > 128) return cudaErrorInvalidValue;
+  if (np > 256) return cudaErrorInvalidValue;
   const int wpb = 4;
   dim3 grid((c1 - c0 + wpb - 1) / wpb, batch);
-  trsm_upper_warp_kernel<<<grid, 32 * wpb, 0, s>>>(mats, ld, stride, r0, np, c0, c1);
+  if (np <= 128)
+    trsm_upper_warp_kernel<4><<<grid, 32 * wpb, 0, s>>>(mats, ld, stride, r0, np, c0, c1);
+  else
+    trsm_upper_warp_kernel<8><<<grid, 32 * wpb, 0, s>>>(mats, ld, stride, r0, np, c0, c1);
   note_launch();
   return cudaGetLastError();
 }

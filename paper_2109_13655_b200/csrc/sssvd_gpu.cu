@@ -146,7 +146,7 @@ struct sssvd_gpu_ctx {
   bool has_gram = false;
   DBuf A, G, gmax, mats, ipiv, shifts, coef, S, V, status, minpiv, scratch;
   DBuf t0, t1, t2, t7, work, info;
-  DBuf lw_linv, lw_T, lw_src, lw_disp, jscr, jperm, jq, jr, jj;
+  DBuf lw_linv, lw_T, lw_src, lw_disp, jscr, jperm, jq, jr, jj, qy, qt, qw;
   // factor cache (moments.hpp:106-116): the last pass left shifts [fact_jb, fact_je) factored in
   // one resident batch of `mats`, so a later pass with the same operator/shifts/L only replays the
   // forward elimination of its new right-hand side and the back substitution
@@ -154,7 +154,7 @@ struct sssvd_gpu_ctx {
   int64_t fact_jb = 0, fact_je = 0;
   int fact_n = 0, fact_L = 0;
   std::vector<std::complex<double>> fact_shifts;
-  static constexpr int kMaxGroups = 4;
+  static constexpr int kMaxGroups = 8;
   cudaStream_t gstream[kMaxGroups] = {};      // high priority: panels, small kernels
   cudaStream_t gstream_lo[kMaxGroups] = {};   // low priority: the big trailing-update GEMMs
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxGroups] = {};
@@ -245,7 +245,10 @@ static LuPlan make_plan(int n, int L) {
   p.L = L;
   p.ld = ((n + L) + 7) / 8 * 8;
   p.stride = (long long)n * p.ld;
-  p.NB = 128;
+  // outer block: the trailing update runs K = NB deep (SSSVD_NB = 128 or 256; the 256-wide block
+  // recurses once more inside the panel)
+  static const char* nb_env = std::getenv("SSSVD_NB");
+  p.NB = (nb_env && std::atoi(nb_env) == 256) ? 256 : 128;
   // leaf width W and cluster size C: the leaf slab (ceil(n/C) x (W+1) complex) must fit ~200 KB
   const size_t budget = 200 * 1024;
   p.W = 8;
@@ -507,7 +510,7 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
     CK(assemble(ctx->G.as<double>(0), n, n, V_dev, L, dshift, mats, P.ld, P.stride, nb, s));
     {
       static const char* genv = std::getenv("SSSVD_GROUPS");
-      const int ng = std::max(1, std::min(nb / 2, genv ? std::atoi(genv) : 3));
+      const int ng = std::max(1, std::min({nb / 2, sssvd_gpu_ctx::kMaxGroups, genv ? std::atoi(genv) : 4}));
       if (ng <= 1) {
         lu_solve_batch(P, work, mats, ipiv, nb, s);
       } else {
@@ -613,26 +616,44 @@ static void dgemm(sssvd_gpu_ctx* ctx, bool ta, bool tb, int m, int n, int k, dou
 
 // thin QR: A (m x k, lda=m) is overwritten by Q; R (k x k upper, ldr = k) returned
 static void thin_qr(sssvd_gpu_ctx* ctx, double* A, int m, int k, double* R) {
-  double* tau = ctx->t7.as<double>(k);
-  int* dinfo = ctx->info.as<int>(1);
-  int lw1 = 0, lw2 = 0;
-  CKS(cusolverDnDgeqrf_bufferSize(ctx->solver, m, k, A, m, &lw1));
-  CKS(cusolverDnDorgqr_bufferSize(ctx->solver, m, k, k, A, m, tau, &lw2));
-  double* work = ctx->work.as<double>(std::max(lw1, lw2));
-  CKS(cusolverDnDgeqrf(ctx->solver, m, k, A, m, tau, work, std::max(lw1, lw2), dinfo));
-  // R = upper triangle of the first k rows
-  CK(cudaMemset2DAsync(R, sizeof(double) * k, 0, sizeof(double) * k, k, ctx->stream));
-  for (int j = 0; j < k; ++j)
-    CK(cudaMemcpyAsync(R + (size_t)j * k, A + (size_t)j * m, sizeof(double) * (j + 1), cudaMemcpyDeviceToDevice,
-                       ctx->stream));
-  CKS(cusolverDnDorgqr(ctx->solver, m, k, k, A, m, tau, work, std::max(lw1, lw2), dinfo));
+  // hand-written blocked Householder QR (householder_qr.cu): cluster panels + DGEMM updates
+  cudaStream_t s = ctx->stream;
+  // panel width: 32 columns, halved until the tallest panel's rows fit one cluster's shared memory
+  int w = 32, c = 0;
+  while (w > 1 && qr_panel_plan(m, w, &c) == 0) w /= 2;
+  if (qr_panel_plan(m, w, &c) == 0) throw Status(SSSVD_E_LENGTH, "thin_qr: operator too tall for the on-chip QR panel");
+  const int npanel = (k + w - 1) / w;
+  double* Y = ctx->qy.as<double>((size_t)m * k);
+  double* T = ctx->qt.as<double>((size_t)npanel * 1024);
+  double* Wt = ctx->qw.as<double>((size_t)2 * w * k + 64);
+  double* W2 = Wt + (size_t)w * k;
+  double* tau = ctx->t7.as<double>(k + 64);
+  for (int p = 0; p < npanel; ++p) {
+    const int j = p * w, wp = std::min(w, k - j), mp = m - j, nt = k - j - wp;
+    CK(qr_panel(A, m, m, j, wp, Y + (size_t)j * m + j, m, T + (size_t)p * 1024, tau + j, s));
+    if (nt > 0) {
+      // A[j:m, j+wp:k] -= Y (T^T (Y^T A[j:m, j+wp:k]))
+      dgemm(ctx, true, false, wp, nt, mp, 1.0, Y + (size_t)j * m + j, m, A + (size_t)(j + wp) * m + j, m, 0.0, Wt, wp);
+      dgemm(ctx, true, false, wp, nt, wp, 1.0, T + (size_t)p * 1024, 32, Wt, wp, 0.0, W2, wp);
+      dgemm(ctx, false, false, mp, nt, wp, -1.0, Y + (size_t)j * m + j, m, W2, wp, 1.0, A + (size_t)(j + wp) * m + j, m);
+    }
+  }
+  CK(copy_r(A, m, k, R, s));
+  // Q = H_0 ... H_{p-1} [I; 0], backward: Q[j:m, j:k] -= Y (T (Y^T Q[j:m, j:k]))
+  CK(eye(A, m, k, m, s));
+  for (int p = npanel - 1; p >= 0; --p) {
+    const int j = p * w, wp = std::min(w, k - j), mp = m - j, nq = k - j;
+    dgemm(ctx, true, false, wp, nq, mp, 1.0, Y + (size_t)j * m + j, m, A + (size_t)j * m + j, m, 0.0, Wt, wp);
+    dgemm(ctx, false, false, wp, nq, wp, 1.0, T + (size_t)p * 1024, 32, Wt, wp, 0.0, W2, wp);
+    dgemm(ctx, false, false, mp, nq, wp, -1.0, Y + (size_t)j * m + j, m, W2, wp, 1.0, A + (size_t)j * m + j, m);
+  }
 }
 
-// full SVD of a square k x k matrix B (destroyed): U (k x k), S (k, descending), V (k x k).
-// Method (round-1 interim, cuSOLVER): SSSVD_TAIL_SVD = gesvdj (default: Jacobi, like the
-// reference's JacobiSVD), gesvdp (polar decomposition; fastest: 12 ms vs 30 ms at 512 x 512, but
-// it resolves the roundoff-level singular values differently, which moves tau on degenerate
-// configs: cfg2 NT-off gives 20 non-spurious vs 0 for the reference restatement) or gesvd.
+// full SVD of a square k x k matrix B (destroyed): U (k x k), S (k, descending), V (k x k), by the
+// hand-written one-sided Jacobi SVD (jacobi_svd.cu) with dgejsv-style QR preconditioning (below).
+// Jacobi, like the reference's JacobiSVD, keeps the roundoff-level singular values that drive the
+// spurious index tau; a polar-decomposition SVD (measured: cuSOLVER gesvdp) moves tau on the
+// degenerate configs (cfg2 NT-off: 20 non-spurious vs 0 for the reference restatement).
 static std::vector<double> d2h(const double* d, size_t count, cudaStream_t s) {
   std::vector<double> h(count);
   if (count) {
@@ -659,7 +680,6 @@ struct CopyFence {
 static void svd_square(sssvd_gpu_ctx* ctx, double* B, int k, double* U, double* S, double* V) {
   static const char* env = std::getenv("SSSVD_TAIL_SVD");
   const std::string method = env ? env : "jacobi";
-  int* dinfo = ctx->info.as<int>(1);
   if (method == "jacobi" || method == "jacobi_n") {
     // hand-written one-sided Jacobi (jacobi_svd.cu); columns sorted by nonincreasing sigma.
     // Default: Jacobi on B^T (B is triangular: the transposed factor converges in far fewer
@@ -730,63 +750,8 @@ static void svd_square(sssvd_gpu_ctx* ctx, double* B, int k, double* U, double* 
     CK(cudaStreamSynchronize(ctx->stream));
     return;
   }
-  if (method == "gesvdp" || method == "gesvd") {
-    cusolverDnParams_t params;
-    CKS(cusolverDnCreateParams(&params));
-    size_t dws = 0, hws = 0;
-    if (method == "gesvdp") {
-      CKS(cusolverDnXgesvdp_bufferSize(ctx->solver, params, CUSOLVER_EIG_MODE_VECTOR, 0, k, k, CUDA_R_64F, B, k,
-                                       CUDA_R_64F, S, CUDA_R_64F, U, k, CUDA_R_64F, V, k, CUDA_R_64F, &dws, &hws));
-      void* dw = ctx->work.get(dws);
-      std::vector<char> hw(hws + 1);
-      double err = 0;
-      CKS(cusolverDnXgesvdp(ctx->solver, params, CUSOLVER_EIG_MODE_VECTOR, 0, k, k, CUDA_R_64F, B, k, CUDA_R_64F, S,
-                            CUDA_R_64F, U, k, CUDA_R_64F, V, k, CUDA_R_64F, dw, dws, hw.data(), hws, dinfo, &err));
-    } else {
-      // gesvd returns V^T; transpose into V afterwards
-      double* VT = ctx->t7.as<double>((size_t)k * k + 64);
-      CKS(cusolverDnXgesvd_bufferSize(ctx->solver, params, 'A', 'A', k, k, CUDA_R_64F, B, k, CUDA_R_64F, S,
-                                      CUDA_R_64F, U, k, CUDA_R_64F, VT, k, CUDA_R_64F, &dws, &hws));
-      void* dw = ctx->work.get(dws);
-      std::vector<char> hw(hws + 1);
-      CKS(cusolverDnXgesvd(ctx->solver, params, 'A', 'A', k, k, CUDA_R_64F, B, k, CUDA_R_64F, S, CUDA_R_64F, U, k,
-                           CUDA_R_64F, VT, k, CUDA_R_64F, dw, dws, hw.data(), hws, dinfo));
-      const double one = 1.0, zero = 0.0;
-      CKB(cublasDgeam(ctx->blas, CUBLAS_OP_T, CUBLAS_OP_N, k, k, &one, VT, k, &zero, V, k, V, k));
-    }
-    cusolverDnDestroyParams(params);
-    return;
-  }
-  if (method == "gesvdj_t") {
-    // one-sided Jacobi on B^T (lower triangular when B is the R of a QR): B^T = V S U^T, so the
-    // roles of the singular-vector outputs swap; converges in fewer sweeps on graded factors
-    double* BT = ctx->t7.as<double>((size_t)k * k + 64);
-    const double one = 1.0, zero = 0.0;
-    CKB(cublasDgeam(ctx->blas, CUBLAS_OP_T, CUBLAS_OP_N, k, k, &one, B, k, &zero, BT, k, BT, k));
-    gesvdjInfo_t pj;
-    CKS(cusolverDnCreateGesvdjInfo(&pj));
-    CKS(cusolverDnXgesvdjSetTolerance(pj, 1e-15));
-    CKS(cusolverDnXgesvdjSetMaxSweeps(pj, 100));
-    int lw = 0;
-    CKS(cusolverDnDgesvdj_bufferSize(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, 0, k, k, BT, k, S, V, k, U, k, &lw, pj));
-    double* wk = ctx->work.as<double>(lw);
-    CKS(cusolverDnDgesvdj(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, 0, k, k, BT, k, S, V, k, U, k, wk, lw, dinfo, pj));
-    cusolverDnDestroyGesvdjInfo(pj);
-    return;
-  }
-  gesvdjInfo_t params;
-  CKS(cusolverDnCreateGesvdjInfo(&params));
-  CKS(cusolverDnXgesvdjSetTolerance(params, 1e-15));
-  CKS(cusolverDnXgesvdjSetMaxSweeps(params, 100));
-  int lwork = 0;
-  CKS(cusolverDnDgesvdj_bufferSize(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, 0, k, k, B, k, S, U, k, V, k, &lwork,
-                                   params));
-  double* work = ctx->work.as<double>(lwork);
-  CKS(cusolverDnDgesvdj(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, 0, k, k, B, k, S, U, k, V, k, work, lwork, dinfo,
-                        params));
-  cusolverDnDestroyGesvdjInfo(params);
+  throw Status(SSSVD_E_INVALID_ARGUMENT, "SSSVD_TAIL_SVD: unknown method (jacobi | jacobi_n)");
 }
-
 
 static bool near_endpoint(double sigma, double endpoint) {
   return std::abs(sigma - endpoint) <= 1e-9 * std::max(std::abs(endpoint), sigma);
@@ -1188,7 +1153,8 @@ void sssvd_gpu_destroy(sssvd_gpu_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   DBuf* bufs[] = {&ctx->A, &ctx->G, &ctx->gmax, &ctx->mats, &ctx->ipiv, &ctx->shifts, &ctx->coef, &ctx->S, &ctx->V,
                   &ctx->status, &ctx->minpiv, &ctx->scratch, &ctx->t0, &ctx->t1, &ctx->t2, &ctx->t7, &ctx->work,
-                  &ctx->info, &ctx->lw_linv, &ctx->lw_T, &ctx->lw_src, &ctx->lw_disp, &ctx->jscr, &ctx->jperm, &ctx->jq, &ctx->jr, &ctx->jj};
+                  &ctx->info, &ctx->lw_linv, &ctx->lw_T, &ctx->lw_src, &ctx->lw_disp, &ctx->jscr, &ctx->jperm, &ctx->jq, &ctx->jr, &ctx->jj,
+                  &ctx->qy, &ctx->qt, &ctx->qw};
   for (DBuf* b : bufs) b->release();
   for (auto& b : ctx->tail) b.release();
   if (ctx->comm) nccl().CommDestroy(ctx->comm);
@@ -1340,6 +1306,48 @@ sssvd_status sssvd_debug_gram_part(sssvd_gpu_ctx* ctx, int part, int nparts, dou
     CK(cudaMemsetAsync(G, 0, sizeof(double) * ctx->n * ctx->n, ctx->stream));
     CK(gram(ctx->A.as<double>(0), (int)ctx->lda, (int)ctx->lda, (int)ctx->n, G, (int)ctx->n, part, nparts, ctx->stream));
     CK(cudaMemcpyAsync(g_out, G, sizeof(double) * ctx->n * ctx->n, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+sssvd_status sssvd_debug_thin_qr(sssvd_gpu_ctx* ctx, const double* a, int64_t m, int64_t k, double* q_out,
+                                 double* r_out) {
+  return guarded(ctx, [&]() {
+    if (m < 1 || k < 1 || m < k) throw Status(SSSVD_E_INVALID_ARGUMENT, "thin_qr: need m >= k >= 1");
+    CK(cudaSetDevice(ctx->device));
+    double* A = ctx->t1.as<double>((size_t)m * k);
+    double* R = ctx->t2.as<double>((size_t)k * k);
+    CK(cudaMemcpyAsync(A, a, sizeof(double) * m * k, cudaMemcpyHostToDevice, ctx->stream));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, ctx->stream));
+    thin_qr(ctx, A, (int)m, (int)k, R);
+    CK(cudaEventRecord(e1, ctx->stream));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (std::getenv("SSSVD_DEBUG")) std::fprintf(stderr, "[sssvd] thin_qr %lld x %lld: %.3f ms\n", (long long)m, (long long)k, ms);
+    CK(cudaMemcpyAsync(q_out, A, sizeof(double) * m * k, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(r_out, R, sizeof(double) * k * k, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+sssvd_status sssvd_debug_svd_square(sssvd_gpu_ctx* ctx, const double* b, int64_t k, double* u_out, double* s_out,
+                                    double* v_out) {
+  return guarded(ctx, [&]() {
+    if (k < 1) throw Status(SSSVD_E_INVALID_ARGUMENT, "svd_square: need k >= 1");
+    CK(cudaSetDevice(ctx->device));
+    double* B = ctx->t1.as<double>((size_t)3 * k * k + k);
+    double *U = B + (size_t)k * k, *V = U + (size_t)k * k, *S = V + (size_t)k * k;
+    CK(cudaMemcpyAsync(B, b, sizeof(double) * k * k, cudaMemcpyHostToDevice, ctx->stream));
+    svd_square(ctx, B, (int)k, U, S, V);
+    CK(cudaMemcpyAsync(u_out, U, sizeof(double) * k * k, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(v_out, V, sizeof(double) * k * k, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(s_out, S, sizeof(double) * k, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
   });
 }

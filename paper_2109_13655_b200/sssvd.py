@@ -120,7 +120,7 @@ EXPORTED_SYMBOLS = [
     "sssvd_gpu_profile_gemm_collect", "sssvd_debug_leaf_profile", "sssvd_debug_gram_part",
     "sssvd_gpu_set_operator_csc", "sssvd_mm_read", "sssvd_mm_info_get", "sssvd_mm_values", "sssvd_mm_colptr",
     "sssvd_mm_rowind", "sssvd_mm_free", "sssvd_mm_write", "sssvd_host_last_error", "sssvd_build_model",
-    "sssvd_filter_profile",
+    "sssvd_filter_profile", "sssvd_debug_thin_qr", "sssvd_debug_svd_square",
 ]
 
 class _MmInfo(ctypes.Structure):
@@ -163,6 +163,8 @@ def lib():
     L.sssvd_mm_free.restype = None
     L.sssvd_mm_write.argtypes = [ctypes.c_char_p, i64, i64, i64, dp, dp, dp, ctypes.c_char_p]
     L.sssvd_host_last_error.restype = ctypes.c_char_p
+    L.sssvd_debug_thin_qr.argtypes = [vp, dp, i64, i64, dp, dp]
+    L.sssvd_debug_svd_square.argtypes = [vp, dp, i64, dp, dp, dp]
     L.sssvd_build_model.argtypes = [ctypes.c_int, i64, i64, ctypes.c_uint64, dp, dp]
     L.sssvd_filter_profile.argtypes = [ctypes.c_double, ctypes.c_double, i64, ctypes.c_double, ctypes.c_int,
                                        ctypes.c_double, ctypes.c_double, i64, ctypes.c_int, dp, dp]
@@ -433,6 +435,22 @@ class Device:
         g = np.empty((self._n, self._n), order="F")
         self.check(lib().sssvd_gpu_form_gram(self.h, size_cap, _ptr(g)))
         return g
+
+    def thin_qr(self, a: np.ndarray):
+        """Debug: the tail's Householder QR (thin Q, R) of a tall matrix."""
+        a = np.asfortranarray(a, dtype=np.float64)
+        m, k = a.shape
+        q, r = np.empty((m, k), order="F"), np.empty((k, k), order="F")
+        self.check(lib().sssvd_debug_thin_qr(self.h, _ptr(a), m, k, _ptr(q), _ptr(r)))
+        return q, r
+
+    def svd_square(self, b: np.ndarray):
+        """Debug: the tail's Jacobi SVD (U, s descending, V) of a square matrix."""
+        b = np.asfortranarray(b, dtype=np.float64)
+        k = b.shape[0]
+        u, v, sv = np.empty((k, k), order="F"), np.empty((k, k), order="F"), np.empty(k)
+        self.check(lib().sssvd_debug_svd_square(self.h, _ptr(b), k, _ptr(u), _ptr(sv), _ptr(v)))
+        return u, sv, v
 
     def run_solve(self, config: RunConfig) -> "RunResult":
         c = config._c()
