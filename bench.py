@@ -167,12 +167,15 @@ def main():
         dev.check(lib.sssvd_gpu_set_operator(dev.h, sssvd.ctypes.c_void_p(a_pin.data_ptr()), w.m, w.n, w.m, 0))
         return [dev.run_solve(c) for c in cfgs]
 
+    # GEMM timing is on from the first warm-up step: the library captures the shifted-solve pass
+    # into a CUDA graph on its second run, keyed (among others) by the profiling state
+    sssvd.profile_gemm(True)
     for _ in range(args.warmup):
         res = step_device()
     barrier()
+    sssvd.profile_gemm_collect()   # discard the warm-up timings
     # ---- timed region (device events on the current stream bracket library work that is
     #      synchronised inside run_solve; CUDA events + synchronize on both sides)
-    sssvd.profile_gemm(True)
     launches0 = sssvd.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:

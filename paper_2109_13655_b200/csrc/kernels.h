@@ -2,6 +2,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <vector>
 #include <cuda_runtime.h>
 
 namespace sssvd_gpu {
@@ -12,8 +13,14 @@ cudaError_t cuda_fail(cudaError_t e, const char* expr, const char* file, int lin
 // brackets each launch with CUDA events on its stream (the dominant kernel's live timing)
 void note_launch(unsigned long long count = 1);
 unsigned long long launch_count();
+void unnote_launch(unsigned long long count);   // captured into a graph, not executed
 void zgemm_profile_enable(bool on);
 void zgemm_profile_collect(double* ms, double* flops, unsigned long long* launches);
+// GEMM stamps of one shifted-solve pass (zgemm.cu): begin resets the slots (stream-ordered, so it
+// is captured with a graph), end returns the per-slot flops, harvest folds a finished pass in
+cudaError_t zgemm_stamp_pass_begin(cudaStream_t s);
+std::vector<double> zgemm_stamp_pass_end();
+void zgemm_stamp_harvest(const std::vector<double>& flops);
 
 // K0 Gram (gram.cu): G = A^T A, A column-major (lda even, K = rows incl. zero padding)
 cudaError_t gram(const double* A, int lda, int K, int n, double* G, int ldg, int part, int nparts, cudaStream_t s);

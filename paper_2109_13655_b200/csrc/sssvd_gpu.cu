@@ -160,6 +160,16 @@ struct sssvd_gpu_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxGroups] = {};
   cudaEvent_t ev_pre[kMaxGroups] = {}, ev_gemm[kMaxGroups] = {};
   DBuf tail[24];
+  // CUDA graphs of the shifted-solve pass (assemble -> grouped LU -> pivot floor -> moments), keyed
+  // by the plan and every device pointer they bake in; captured on the second sighting of a key
+  struct LuGraph {
+    std::vector<uintptr_t> key;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<double> gemm_flops;   // per stamp slot
+    unsigned long long launches = 0;
+  };
+  std::vector<LuGraph> lu_graphs;
+  std::vector<uintptr_t> lu_warm_key;
   cudaStream_t cstream = nullptr;   // result device->host copies, overlapped with the tail
   cudaEvent_t ev_copy = nullptr;
   double t_gram = 0, t_solves = 0, t_allreduce = 0, solve_flops = 0;
@@ -271,6 +281,17 @@ static LuPlan make_plan(int n, int L) {
       }
   }
   if (!found) throw Status(SSSVD_E_LENGTH, "operator too large for the on-chip leaf panel");
+  {
+    // measurement overrides: leaf width / cluster size (used only if the slab fits)
+    static const char* wenv = std::getenv("SSSVD_LEAF_W");
+    static const char* cenv = std::getenv("SSSVD_LEAF_C");
+    const int w = wenv ? std::atoi(wenv) : p.W, c = cenv ? std::atoi(cenv) : p.cluster;
+    if ((w == 8 || w == 16 || w == 32) && (c == 1 || c == 2 || c == 4 || c == 8 || c == 16) &&
+        leaf_smem_bytes(n, w, c) <= budget) {
+      p.W = w;
+      p.cluster = c;
+    }
+  }
   // register-resident leaf (v2): rows per CTA <= threads x rows-per-thread of the variant
   p.leaf_variant = -1;
   // default: shared-memory leaf (v1); the register-resident v2 needs a whole SM register file
@@ -507,10 +528,14 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
       ctx->solve_flops += nb * (8.0 * (double)n * n * L);
       continue;
     }
-    CK(assemble(ctx->G.as<double>(0), n, n, V_dev, L, dshift, mats, P.ld, P.stride, nb, s));
-    {
-      static const char* genv = std::getenv("SSSVD_GROUPS");
-      const int ng = std::max(1, std::min({nb / 2, sssvd_gpu_ctx::kMaxGroups, genv ? std::atoi(genv) : 4}));
+    static const char* genv = std::getenv("SSSVD_GROUPS");
+    const int ng = std::max(1, std::min({nb / 2, sssvd_gpu_ctx::kMaxGroups, genv ? std::atoi(genv) : 4}));
+    // the whole pass on the device: the host issues ~5000 launches per pass, which at ~17 us each
+    // would make the GPU wait on the host; replaying a captured graph removes that
+    std::vector<double> pass_flops;
+    auto enqueue = [&](bool capturing) {
+      CK(zgemm_stamp_pass_begin(s));
+      CK(assemble(ctx->G.as<double>(0), n, n, V_dev, L, dshift, mats, P.ld, P.stride, nb, s));
       if (ng <= 1) {
         lu_solve_batch(P, work, mats, ipiv, nb, s);
       } else {
@@ -524,17 +549,77 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
                             ctx->gstream[g], ctx->gstream_lo[g], ctx->ev_pre[g], ctx->ev_gemm[g]});
           b0 += cnt;
         }
+        const double th0 = now_s();
         lu_solve_groups(P, groups);
+        const double th1 = now_s();
         for (int g = 0; g < ng; ++g) {
           CK(cudaEventRecord(ctx->ev_join[g], ctx->gstream[g]));
           CK(cudaStreamWaitEvent(s, ctx->ev_join[g], 0));
         }
+        static const bool dbg_issue = std::getenv("SSSVD_DEBUG_ISSUE") != nullptr;
+        if (dbg_issue && !capturing) {
+          CK(cudaStreamSynchronize(s));
+          std::fprintf(stderr, "[sssvd] LU host issue %.1f ms, host issue + device drain %.1f ms\n",
+                       (th1 - th0) * 1e3, (now_s() - th0) * 1e3);
+        }
+      }
+      CK(pivot_floor(mats, P.ld, P.stride, n, dshift, ctx->gmax.as<double>(1), dstatus, dmin, nb, s));
+      CK(moments(mats, P.ld, P.stride, n, n, L, nb, dcoef, M, S_dev, s));
+      pass_flops = zgemm_stamp_pass_end();
+    };
+    static const bool no_graph = std::getenv("SSSVD_NO_GRAPH") != nullptr;
+    sssvd_gpu_ctx::LuGraph* replayed = nullptr;
+    if (no_graph) {
+      enqueue(false);
+    } else {
+      const std::vector<uintptr_t> key = {
+          (uintptr_t)n, (uintptr_t)L, (uintptr_t)M, (uintptr_t)nb, (uintptr_t)ng, (uintptr_t)P.NB, (uintptr_t)P.W,
+          (uintptr_t)P.cluster, (uintptr_t)(P.leaf_variant + 1), (uintptr_t)P.ld, (uintptr_t)ctx->G.p,
+          (uintptr_t)V_dev, (uintptr_t)mats, (uintptr_t)ipiv, (uintptr_t)work.linv, (uintptr_t)work.T,
+          (uintptr_t)work.src, (uintptr_t)work.disp, (uintptr_t)dshift, (uintptr_t)dcoef, (uintptr_t)S_dev,
+          (uintptr_t)ctx->gmax.p, (uintptr_t)dstatus, (uintptr_t)dmin};
+      for (auto& g : ctx->lu_graphs)
+        if (g.key == key) replayed = &g;
+      if (replayed) {
+        CK(cudaGraphLaunch(replayed->exec, s));
+        note_launch(replayed->launches);
+      } else if (ctx->lu_warm_key == key) {
+        // second sighting: capture (the eager first run has set every kernel attribute)
+        sssvd_gpu_ctx::LuGraph g;
+        g.key = key;
+        const unsigned long long l0 = launch_count();
+        cudaGraph_t graph = nullptr;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        try {
+          enqueue(true);
+        } catch (...) {
+          cudaStreamEndCapture(s, &graph);
+          if (graph) cudaGraphDestroy(graph);
+          zgemm_stamp_pass_end();
+          throw;
+        }
+        g.gemm_flops = pass_flops;
+        CK(cudaStreamEndCapture(s, &graph));
+        g.launches = launch_count() - l0;
+        unnote_launch(g.launches);
+        CK(cudaGraphInstantiateWithFlags(&g.exec, graph, cudaGraphInstantiateFlagUseNodePriority));
+        CK(cudaGraphDestroy(graph));
+        if (ctx->lu_graphs.size() >= 4) {
+          if (ctx->lu_graphs.front().exec) cudaGraphExecDestroy(ctx->lu_graphs.front().exec);
+          ctx->lu_graphs.erase(ctx->lu_graphs.begin());
+        }
+        ctx->lu_graphs.push_back(g);
+        replayed = &ctx->lu_graphs.back();
+        CK(cudaGraphLaunch(replayed->exec, s));
+        note_launch(replayed->launches);
+      } else {
+        enqueue(false);
+        ctx->lu_warm_key = key;
       }
     }
-    CK(pivot_floor(mats, P.ld, P.stride, n, dshift, ctx->gmax.as<double>(1), dstatus, dmin, nb, s));
-    CK(moments(mats, P.ld, P.stride, n, n, L, nb, dcoef, M, S_dev, s));
     CK(cudaMemcpyAsync(hstatus.data(), dstatus, sizeof(int) * nb, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    zgemm_stamp_harvest(replayed ? replayed->gemm_flops : pass_flops);
     for (int b = 0; b < nb; ++b)
       if (hstatus[b]) throw Status(SSSVD_E_NUMERICAL, "ShiftedFactorization: shift numerically on the spectrum");
     ctx->solve_flops += nb * (8.0 * n * (double)n * n / 3.0 + 8.0 * (double)n * n * L);
@@ -1173,6 +1258,8 @@ void sssvd_gpu_destroy(sssvd_gpu_ctx* ctx) {
     cudaStreamDestroy(ctx->cstream);
   }
   if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
+  for (auto& g : ctx->lu_graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }

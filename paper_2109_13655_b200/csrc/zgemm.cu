@@ -24,54 +24,92 @@ namespace sssvd_gpu {
 
 static std::atomic<unsigned long long> g_launches{0};
 void note_launch(unsigned long long c) { g_launches += c; }
+void unnote_launch(unsigned long long c) { g_launches -= c; }
 unsigned long long launch_count() { return g_launches.load(); }
 
+// Live timing of the DMMA GEMMs without extra stream or graph nodes: inside a shifted-solve pass
+// every launch gets a stamp slot; thread 0 of each CTA folds %globaltimer into the slot's start
+// (atomicMin at entry) and end (atomicMax at exit). The slots are reset by two memsets at the
+// start of the pass (captured with it when the pass is a CUDA graph) and harvested after the
+// pass has synchronised, so graph replays and eager runs are timed alike.
 struct GemmProf {
   bool on = false;
-  std::vector<cudaEvent_t> ev;       // pairs
-  std::vector<double> flops;
-  size_t used = 0;
+  unsigned long long* d_stamp = nullptr;   // [cap] starts, then [cap] ends (ns)
+  int cap = 0;
+  bool in_pass = false;
+  std::vector<double> flops;               // per slot of the pass being enqueued
+  double acc_ms = 0, acc_flops = 0;
+  unsigned long long acc_launches = 0;
 };
 static GemmProf g_prof;
+constexpr int kStampSlots = 8192;
 
 void zgemm_profile_enable(bool on) {
   g_prof.on = on;
-  g_prof.used = 0;
-  g_prof.flops.clear();
+  g_prof.acc_ms = g_prof.acc_flops = 0;
+  g_prof.acc_launches = 0;
 }
 
-// *ms is the GEMM-BUSY time: the length of the union of the launch intervals. The shift groups
-// run their trailing updates concurrently on separate streams, so summing per-launch durations
-// would count shared time once per overlapping launch.
-void zgemm_profile_collect(double* ms, double* flops, unsigned long long* launches) {
+cudaError_t zgemm_stamp_pass_begin(cudaStream_t s) {
+  if (!g_prof.d_stamp) {
+    cudaError_t e = cudaMalloc(&g_prof.d_stamp, sizeof(unsigned long long) * 2 * kStampSlots);
+    if (e != cudaSuccess) return e;
+    g_prof.cap = kStampSlots;
+  }
+  g_prof.in_pass = true;
+  g_prof.flops.clear();
+  cudaError_t e = cudaMemsetAsync(g_prof.d_stamp, 0xff, sizeof(unsigned long long) * g_prof.cap, s);
+  if (e != cudaSuccess) return e;
+  return cudaMemsetAsync(g_prof.d_stamp + g_prof.cap, 0, sizeof(unsigned long long) * g_prof.cap, s);
+}
+
+std::vector<double> zgemm_stamp_pass_end() {
+  g_prof.in_pass = false;
+  return g_prof.flops;
+}
+
+// GEMM-BUSY time of one pass: the length of the union of its launch intervals (the shift groups
+// run their trailing updates concurrently, so summing per-launch durations would count shared
+// time once per overlapping launch); added to the running totals when profiling is on
+void zgemm_stamp_harvest(const std::vector<double>& flops) {
+  if (!g_prof.on || flops.empty() || !g_prof.d_stamp) return;
+  const size_t cnt = flops.size();
+  std::vector<unsigned long long> st(cnt), en(cnt);
+  cudaMemcpy(st.data(), g_prof.d_stamp, sizeof(unsigned long long) * cnt, cudaMemcpyDeviceToHost);
+  cudaMemcpy(en.data(), g_prof.d_stamp + g_prof.cap, sizeof(unsigned long long) * cnt, cudaMemcpyDeviceToHost);
+  std::vector<std::pair<unsigned long long, unsigned long long>> iv;
   double f = 0;
-  std::vector<std::pair<double, double>> iv;
-  iv.reserve(g_prof.used);
-  for (size_t i = 0; i < g_prof.used; ++i) {
-    cudaEventSynchronize(g_prof.ev[2 * i + 1]);
-    float a = 0, b = 0;
-    cudaEventElapsedTime(&a, g_prof.ev[0], g_prof.ev[2 * i]);
-    cudaEventElapsedTime(&b, g_prof.ev[0], g_prof.ev[2 * i + 1]);
-    iv.emplace_back(a, b);
-    f += g_prof.flops[i];
+  for (size_t i = 0; i < cnt; ++i) {
+    if (en[i] == 0 || st[i] == ~0ull) continue;   // empty launch
+    iv.emplace_back(st[i], en[i]);
+    f += flops[i];
   }
   std::sort(iv.begin(), iv.end());
-  double t = 0, cs = 0, ce = -1e300;
+  double t = 0;
+  unsigned long long cs = 0, ce = 0;
+  bool open = false;
   for (const auto& [a, b] : iv) {
-    if (a > ce) {
-      if (ce > cs) t += ce - cs;
+    if (!open || a > ce) {
+      if (open) t += (double)(ce - cs);
       cs = a;
       ce = b;
+      open = true;
     } else {
       ce = std::max(ce, b);
     }
   }
-  if (!iv.empty() && ce > cs) t += ce - cs;
-  *ms = t;
-  *flops = f;
-  *launches = g_prof.used;
-  g_prof.used = 0;
-  g_prof.flops.clear();
+  if (open) t += (double)(ce - cs);
+  g_prof.acc_ms += t * 1e-6;
+  g_prof.acc_flops += f;
+  g_prof.acc_launches += iv.size();
+}
+
+void zgemm_profile_collect(double* ms, double* flops, unsigned long long* launches) {
+  *ms = g_prof.acc_ms;
+  *flops = g_prof.acc_flops;
+  *launches = g_prof.acc_launches;
+  g_prof.acc_ms = g_prof.acc_flops = 0;
+  g_prof.acc_launches = 0;
 }
 
 namespace {
@@ -125,8 +163,13 @@ template <bool SET, bool GATHER>
 __global__ void __launch_bounds__(THREADS, 2)
 zgemm_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long long sA,
              const double2* __restrict__ B, int ldb, long long sB, const int* __restrict__ brow, int sR,
-             double2* C, int ldc, long long sC) {
+             double2* C, int ldc, long long sC, unsigned long long* __restrict__ stamp, int stamp_cap) {
   extern __shared__ __align__(16) double2 smem[];
+  if (stamp && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(stamp, t);
+  }
   // stage s occupies [s*(A_STAGE+B_STAGE), (s+1)*(A_STAGE+B_STAGE)): A tile then B tile
   double2* As = smem;
   double2* Bs = smem + A_STAGE;
@@ -243,6 +286,14 @@ zgemm_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long l
       }
     }
   }
+  if (stamp) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMax(stamp + stamp_cap, t);
+    }
+  }
 }
 
 size_t zgemm_sub_smem() { return (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double2); }
@@ -260,24 +311,14 @@ static cudaError_t launch(int M, int N, int K, const double2* A, int lda, long l
     configured = true;
   }
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch);
-  if (g_prof.on) {
-    if (2 * (g_prof.used + 1) > g_prof.ev.size()) {
-      for (int i = 0; i < 512; ++i) {
-        cudaEvent_t e;
-        cudaEventCreate(&e);
-        g_prof.ev.push_back(e);
-      }
-    }
-    cudaEventRecord(g_prof.ev[2 * g_prof.used], stream);
+  unsigned long long* stamp = nullptr;
+  if (g_prof.in_pass && (int)g_prof.flops.size() < g_prof.cap) {
+    stamp = g_prof.d_stamp + g_prof.flops.size();
+    g_prof.flops.push_back(8.0 * M * (double)N * K * batch);
   }
   zgemm_kernel<SET, GATHER><<<grid, THREADS, zgemm_sub_smem(), stream>>>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR,
-                                                                         C, ldc, sC);
+                                                                         C, ldc, sC, stamp, g_prof.cap);
   note_launch();
-  if (g_prof.on) {
-    cudaEventRecord(g_prof.ev[2 * g_prof.used + 1], stream);
-    g_prof.flops.push_back(8.0 * M * (double)N * K * batch);
-    ++g_prof.used;
-  }
   return cudaGetLastError();
 }
 
