@@ -245,6 +245,20 @@ cudaError_t jacobi_svd(double* W, double* V, int k, int ldw, double* S, double t
       configured = true;
     }
     unsigned int* rot = scratch + 2;      // [2], [3] rotation counts (ping-pong by sweep parity)
+    const int npairs = (k + (k & 1)) / 2;
+    if (npairs > 256) {
+      // large k (configs 3, 5: k = 1024, 2048): the whole GPU, one column pair per warp per round,
+      // rounds separated by a software grid barrier over co-resident CTAs (cooperative launch)
+      int ctas = std::min(148, (npairs + 7) / 8);
+      unsigned int* bar = scratch;         // [0] arrivals, [1] generation (zeroed above)
+      void* args[] = {&W, &V, &k, &ldw, &tol, &max_sweeps, &bar, &rot, &sweeps_out};
+      e = cudaLaunchCooperativeKernel((const void*)jacobi_svd_kernel, dim3(ctas), dim3(256), args, 0, s);
+      if (e != cudaSuccess) return e;
+      note_launch();
+      jacobi_finish_kernel<<<k, 256, 0, s>>>(W, k, ldw, S);
+      note_launch();
+      return cudaGetLastError();
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(16, 1, 1);
     cfg.blockDim = dim3(512, 1, 1);

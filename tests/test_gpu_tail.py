@@ -56,3 +56,16 @@ def test_svd_square_matches_lapack(dev, k):
     assert np.all(np.abs(s - s_ref) <= 1e-9 * s_ref + 1e-14 * s_ref[0])
     assert np.linalg.norm(u * s @ v.T - b) <= 1e-13 * np.linalg.norm(b)
     assert np.linalg.norm(v.T @ v - np.eye(k)) <= 1e-12
+
+
+@pytest.mark.parametrize("k", [1024, 1500])
+def test_svd_square_large_grid_kernel(dev, k):
+    """k > 512: the whole-GPU grid-barrier Jacobi (configs 3 and 5 have k = 1024 and 2048).
+    Rounding grows with the k - 1 rotations per column per sweep: bounds scale with k eps."""
+    b = np.triu(graded(k, k, k, decades=10.0))
+    u, s, v = dev.svd_square(b)
+    s_ref = np.linalg.svd(b, compute_uv=False)
+    assert np.all(np.diff(s) <= 0)
+    assert np.all(np.abs(s - s_ref) <= 1e-9 * s_ref + 1e-14 * s_ref[0])
+    assert np.linalg.norm(u * s @ v.T - b) <= 4e-15 * k * np.linalg.norm(b)
+    assert np.linalg.norm(v.T @ v - np.eye(k)) <= 2e-14 * k   # Frobenius: ~1e-14 per entry
