@@ -208,3 +208,15 @@ def test_config1_parity_with_oracle(dev):
         gap = 1e-3
         bound = max(1e-8, 10 * (res.exact[g] + ores.residuals.exact[o]) / gap)
         assert min(np.linalg.norm(v - vo), np.linalg.norm(v + vo)) <= bound
+
+
+def test_run_solve_repeatable_across_graph_capture(dev):
+    """run_solve x3 on the same operator (eager, capture + replay, replay): identical results."""
+    from paper_2109_13655_b200 import sssvd
+    a, _, sigma, _ = orc.build_model(1, 300, 120, 7)
+    cfg = sssvd.RunConfig(0.2, 0.6, params=sssvd.SsParams(block_size=8, moment_degree=4, quadrature_count=32))
+    res = [sssvd.run_solve(a.dense, cfg, dev) for _ in range(3)]
+    for r in res[1:]:
+        assert np.array_equal(r.triplets.sigma, res[0].triplets.sigma)
+        assert np.array_equal(r.tau, res[0].tau) and np.array_equal(r.exact, res[0].exact)
+        assert np.array_equal(r.triplets.left, res[0].triplets.left)
