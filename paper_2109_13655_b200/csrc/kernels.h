@@ -75,6 +75,10 @@ cudaError_t jacobi_svd(double* W, double* V, int k, int ldw, double* S, double t
 cudaError_t jacobi_svd_block(double* W, double* V, int k, int ldw, double* S, double tol, int max_sweeps,
                              unsigned int* scratch, int* sweeps_out, cudaStream_t s);
 size_t jacobi_block_smem(int k);
+// k > 512: block Jacobi over the whole GPU (one block pair per SM per outer round)
+cudaError_t jacobi_svd_grid_block(double* W, double* V, int k, int ldw, double* S, double tol, int max_sweeps,
+                                  unsigned int* scratch, int* sweeps_out, cudaStream_t s);
+bool jacobi_grid_block_plan(int k, int sms, int* b, int* nbe, int* rpl, size_t* smem);
 // K7 (moments.cu)
 cudaError_t moments(const double2* mats, int ld, long long stride, int xcol, int n, int L, int nb,
                     const double2* coef, int M, double* S, cudaStream_t s);

@@ -793,10 +793,17 @@ static void svd_square(sssvd_gpu_ctx* ctx, double* B, int k, double* U, double* 
       }
       // block Jacobi (shared-memory inner sweeps) where the block pair fits, else the scalar one
       static const char* jb = std::getenv("SSSVD_JACOBI");
-      const bool use_block = !(jb && std::string(jb) == "scalar") && k <= 512 && k >= 64 &&
+      const std::string jmode = jb ? jb : "";
+      const bool use_block = jmode != "scalar" && jmode != "grid" && k <= 512 && k >= 64 &&
                              jacobi_block_smem(k) <= 220 * 1024;
+      int gb_b, gb_nbe, gb_tw;
+      size_t gb_smem;
+      const bool use_grid_block = !use_block && jmode != "scalar" &&
+                                  jacobi_grid_block_plan(k, 148, &gb_b, &gb_nbe, &gb_tw, &gb_smem);
       if (use_block)
         CK(jacobi_svd_block(U, J, k, k, S, tol, 60, scr, sweeps, ctx->stream));
+      else if (use_grid_block)
+        CK(jacobi_svd_grid_block(U, J, k, k, S, tol, 60, scr, sweeps, ctx->stream));
       else
         CK(jacobi_svd(U, J, k, k, S, tol, 60, scr, sweeps, ctx->stream));   // U <- W S^-1, S
       if (dbg) {

@@ -58,9 +58,9 @@ def test_svd_square_matches_lapack(dev, k):
     assert np.linalg.norm(v.T @ v - np.eye(k)) <= 1e-12
 
 
-@pytest.mark.parametrize("k", [1024, 1500])
+@pytest.mark.parametrize("k", [777, 1024, 1500, 2048])
 def test_svd_square_large_grid_kernel(dev, k):
-    """k > 512: the whole-GPU grid-barrier Jacobi (configs 3 and 5 have k = 1024 and 2048).
+    """k > 512: the whole-GPU block Jacobi (configs 3 and 5 have k = 1024 and 2048).
     Rounding grows with the k - 1 rotations per column per sweep: bounds scale with k eps."""
     b = np.triu(graded(k, k, k, decades=10.0))
     u, s, v = dev.svd_square(b)
