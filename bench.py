@@ -177,13 +177,14 @@ def main():
     # ---- timed region (device events on the current stream bracket library work that is
     #      synchronised inside run_solve; CUDA events + synchronize on both sides)
     launches0 = sssvd.launch_count()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    ev0, ev1 = evs[0], evs[-1]
     with Clocks(local) as clk:
         barrier()
         ev0.record()
-        for _ in range(args.steps):
+        for i in range(args.steps):
             res = step_device()
-        ev1.record()
+            evs[i + 1].record()
         barrier()
     launches = sssvd.launch_count() - launches0
     gemm_ms, gemm_flops, gemm_launches = sssvd.profile_gemm_collect()
@@ -257,6 +258,7 @@ def main():
             "truth_in_interval": int(np.sum((sigma >= w.a) & (sigma <= w.b))),
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
+            "step_ms": [round(evs[i].elapsed_time(evs[i + 1]), 3) for i in range(args.steps)],
             "gpu_launches": int(launches // max(1, args.steps)),
             "gpu_launches_timed_region": int(launches),
             "input_sha256": workloads.sha256(a),

@@ -250,6 +250,43 @@ cudaError_t qr_panel(double* A, int lda, int m, int j, int w, double* Y, int ldy
   return e;
 }
 
+// Block reflector factor of an outer block (LAPACK dlarft, forward / columnwise): H_0 ... H_{kb-1}
+// = I - Y T Y^T with T upper triangular, T_ii = tau_i and T[0:i, i] = -tau_i T[0:i, 0:i] G[0:i, i],
+// where G = Y^T Y (kb x kb, column-major, from one DGEMM). One CTA, T in shared memory.
+__global__ void __launch_bounds__(128, 1)
+larft_kernel(const double* __restrict__ G, int kb, const double* __restrict__ tau, double* __restrict__ T) {
+  extern __shared__ double ts[];   // [kb][kb] column-major
+  const int r = threadIdx.x;
+  for (int e = r; e < kb * kb; e += blockDim.x) ts[e] = 0.0;
+  __syncthreads();
+  for (int i = 0; i < kb; ++i) {
+    const double ti = tau[i];
+    if (r < i) {
+      double z = 0.0;
+      for (int c = r; c < i; ++c) z = fma(ts[(size_t)c * kb + r], G[(size_t)i * kb + c], z);
+      ts[(size_t)i * kb + r] = -ti * z;
+    } else if (r == i) {
+      ts[(size_t)i * kb + i] = ti;
+    }
+    __syncthreads();
+  }
+  for (int e = r; e < kb * kb; e += blockDim.x) T[e] = ts[e];
+}
+
+cudaError_t larft(const double* G, int kb, const double* tau, double* T, cudaStream_t s) {
+  if (kb < 1 || kb > 128) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)kb * kb * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 128 * 8);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  larft_kernel<<<1, 128, smem, s>>>(G, kb, tau, T);
+  note_launch();
+  return cudaGetLastError();
+}
+
 // [I_k; 0] into the m x k column-major Q
 __global__ void eye_kernel(double* __restrict__ Q, int m, int k, int ldq) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)ldq * k;

@@ -674,8 +674,8 @@ namespace sssvd_gpu {
 // 148 SMs, 229 KB; k = 1024: b = 8, 64 pairs): nb - 1 grid barriers per sweep instead of the
 // scalar kernel's k - 1, and the column traffic of the inner rounds stays on chip.
 //
-// Inner rounds: one warp owns one pair; lane t holds rows t + 32 i (i < RPL, RPL = 32 for
-// k <= 1024, 64 for k <= 2048) of the resident column x in registers and streams the partner
+// Inner rounds: one warp owns one pair; lane t holds rows t + 32 i (i < RPL, RPL = 16 / 32 / 64
+// for k <= 512 / 1024 / 2048) of the resident column x in registers and streams the partner
 // column y from shared memory twice (dot products, then the rotation), so only x occupies
 // registers (256 threads per CTA: up to 255 registers per thread).
 constexpr int GB_THREADS = 256;
@@ -1019,7 +1019,7 @@ jacobi_grid_block_kernel(double* __restrict__ Wm, double* __restrict__ Vm, int k
 // false when the shape does not fit (callers fall back to the scalar grid kernel)
 bool jacobi_grid_block_plan(int k, int sms, int* b_out, int* nbe_out, int* rpl_out, size_t* smem_out) {
   if (k < 64 || k > 32 * 64) return false;
-  const int rpl = k <= 32 * 32 ? 32 : 64;
+  const int rpl = k <= 32 * 16 ? 16 : k <= 32 * 32 ? 32 : 64;
   // widest block (fewest outer rounds, i.e. grid barriers, per sweep) with one warp per resident
   // column and the pair in shared memory; at least enough blocks to cover the SMs once
   int b = GB_THREADS / 32;
@@ -1052,10 +1052,12 @@ cudaError_t jacobi_svd_grid_block(double* W, double* V, int k, int ldw, double* 
   static unsigned long long* dprof = nullptr;
   if (prof_on && !dprof) cudaMalloc(&dprof, 8 * sizeof(unsigned long long));
   if (prof_on) cudaMemsetAsync(dprof, 0, 8 * sizeof(unsigned long long), s);
-  const void* fn = rpl == 32 ? (prof_on ? (const void*)jacobi_grid_block_kernel<32, true>
-                                        : (const void*)jacobi_grid_block_kernel<32, false>)
-                             : (prof_on ? (const void*)jacobi_grid_block_kernel<64, true>
-                                        : (const void*)jacobi_grid_block_kernel<64, false>);
+  const void* fn = rpl == 16   ? (prof_on ? (const void*)jacobi_grid_block_kernel<16, true>
+                                          : (const void*)jacobi_grid_block_kernel<16, false>)
+                   : rpl == 32 ? (prof_on ? (const void*)jacobi_grid_block_kernel<32, true>
+                                          : (const void*)jacobi_grid_block_kernel<32, false>)
+                               : (prof_on ? (const void*)jacobi_grid_block_kernel<64, true>
+                                          : (const void*)jacobi_grid_block_kernel<64, false>);
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;

@@ -85,6 +85,8 @@ cudaError_t moments(const double2* mats, int ld, long long stride, int xcol, int
 cudaError_t blocks_to_colmajor(const double* S, int n, int L, int nblk, double* out, cudaStream_t s);
 cudaError_t colnorm_diff(const double* X, int ldx, const double* Y, int ldy, const double* s, int rows,
                          int cols, double* out, cudaStream_t st);
+cudaError_t tau_scale(const double* q, int rank, int tcount, const double* sv, const double* inv, double* tau,
+                      double* qsc, cudaStream_t st);
 cudaError_t gather_cols(const double* src, int lds, const int* perm, const double* scale, int rows,
                         int cols, double* dst, int ldd, cudaStream_t st);
 cudaError_t sumsq(const double* a, long long count, double* scratch, double* out, cudaStream_t s);
@@ -101,6 +103,8 @@ int qr_panel_plan(int mp, int w, int* cluster);
 cudaError_t qr_panel(double* A, int lda, int m, int j, int w, double* Y, int ldy, double* T, double* tau,
                      cudaStream_t s);
 cudaError_t eye(double* Q, int m, int k, int ldq, cudaStream_t s);
+// T (kb x kb) of the block reflector H_0..H_{kb-1} = I - Y T Y^T from G = Y^T Y and tau (kb <= 128)
+cudaError_t larft(const double* G, int kb, const double* tau, double* T, cudaStream_t s);
 cudaError_t copy_r(const double* A, int lda, int k, double* R, cudaStream_t s);
 // *bad |= 1 if any of a[0..count) is NaN / Inf (sparse.cu)
 cudaError_t any_nonfinite(const double* a, long long count, int* bad, cudaStream_t s);

@@ -120,6 +120,55 @@ cudaError_t colnorm_diff(const double* X, int ldx, const double* Y, int ldy, con
   return cudaGetLastError();
 }
 
+// Spurious index and estimator coefficients of triplet i (one CTA per column of q, column-major
+// rank x tcount), postprocess.hpp:56-60 and :86-93:
+//   tau_i = ||q_i||^2 / sum_l q_li^2 / Sigma_l ,   qsc[:, i] = Sigma^+ q_i  (inv = Sigma^+ diagonal)
+// (the sums are CTA reductions; the reference's order is Eigen's vectorised one, parity is by
+// tolerance)
+__global__ void tau_scale_kernel(const double* __restrict__ q, int rank, const double* __restrict__ sv,
+                                 const double* __restrict__ inv, double* __restrict__ tau,
+                                 double* __restrict__ qsc) {
+  const int i = blockIdx.x;
+  const double* qi = q + (size_t)i * rank;
+  double num = 0.0, den = 0.0;
+  for (int l = threadIdx.x; l < rank; l += blockDim.x) {
+    const double v = qi[l], v2 = v * v;
+    num += v2;
+    den += v2 / sv[l];
+    qsc[(size_t)i * rank + l] = inv[l] * v;
+  }
+  __shared__ double red[2][32];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    num += __shfl_xor_sync(0xffffffffu, num, off);
+    den += __shfl_xor_sync(0xffffffffu, den, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = num;
+    red[1][threadIdx.x >> 5] = den;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const bool in = threadIdx.x < (blockDim.x >> 5);
+    num = in ? red[0][threadIdx.x] : 0.0;
+    den = in ? red[1][threadIdx.x] : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      num += __shfl_xor_sync(0xffffffffu, num, off);
+      den += __shfl_xor_sync(0xffffffffu, den, off);
+    }
+    if (threadIdx.x == 0) tau[i] = num / den;
+  }
+}
+
+cudaError_t tau_scale(const double* q, int rank, int tcount, const double* sv, const double* inv, double* tau,
+                      double* qsc, cudaStream_t st) {
+  if (tcount <= 0) return cudaSuccess;
+  tau_scale_kernel<<<tcount, 256, 0, st>>>(q, rank, sv, inv, tau, qsc);
+  note_launch();
+  return cudaGetLastError();
+}
+
 // dst[:, j] = src[:, perm[j]] * (scale ? scale[j] : 1)   (column gather, column-major)
 __global__ void gather_cols_kernel(const double* __restrict__ src, int lds, const int* __restrict__ perm,
                                    const double* __restrict__ scale, int rows, double* __restrict__ dst,

@@ -23,6 +23,7 @@
 #include <cstring>
 #include <limits>
 #include <map>
+#include <future>
 #include <mutex>
 #include <numeric>
 #include <stdexcept>
@@ -124,12 +125,27 @@ static double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+// SSSVD_TAIL_PROF=1: synchronised checkpoints through the tail (stderr), for measurement only
+struct TailProf {
+  cudaStream_t s;
+  bool on;
+  double t;
+  explicit TailProf(cudaStream_t st) : s(st), on(std::getenv("SSSVD_TAIL_PROF") != nullptr), t(now_s()) {}
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const double t1 = now_s();
+    std::fprintf(stderr, "[sssvd] tail %-28s %8.2f ms\n", what, (t1 - t) * 1e3);
+    t = t1;
+  }
+};
+
 }  // namespace sssvd_gpu
 
 using namespace sssvd_gpu;
 
 enum TailBuf { T_SC, T_Q, T_R, T_UR, T_VR, T_SV, T_US1, T_QM, T_LEFT, T_RIGHT, T_PERM, T_UT, T_BM, T_PM, T_PHI,
-               T_QS, T_SIG, T_PS, T_QSC, T_COEFF, T_X, T_IMG, T_NRM, T_COUNT };
+               T_QS, T_SIG, T_PS, T_QSC, T_COEFF, T_X, T_IMG, T_NRM, T_INV, T_TAU, T_Y, T_COUNT };
 
 struct sssvd_gpu_ctx {
   int device = 0;
@@ -159,7 +175,7 @@ struct sssvd_gpu_ctx {
   cudaStream_t gstream_lo[kMaxGroups] = {};   // low priority: the big trailing-update GEMMs
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxGroups] = {};
   cudaEvent_t ev_pre[kMaxGroups] = {}, ev_gemm[kMaxGroups] = {};
-  DBuf tail[24];
+  DBuf tail[T_COUNT];
   // CUDA graphs of the shifted-solve pass (assemble -> grouped LU -> pivot floor -> moments), keyed
   // by the plan and every device pointer they bake in; captured on the second sighting of a key
   struct LuGraph {
@@ -234,8 +250,8 @@ struct PinnedArray {
 
 struct sssvd_gpu_result {
   sssvd_result_info info{};
-  std::vector<double> sigma, tau, estimated, exact, galerkin, basis_sv, q;
-  PinnedArray left, right, blocks;
+  std::vector<double> sigma, tau, estimated, exact, galerkin, basis_sv;
+  PinnedArray left, right, blocks, q;
   std::vector<int32_t> in_interval, spurious;
   std::string note;
 };
@@ -701,36 +717,72 @@ static void dgemm(sssvd_gpu_ctx* ctx, bool ta, bool tb, int m, int n, int k, dou
 
 // thin QR: A (m x k, lda=m) is overwritten by Q; R (k x k upper, ldr = k) returned
 static void thin_qr(sssvd_gpu_ctx* ctx, double* A, int m, int k, double* R) {
-  // hand-written blocked Householder QR (householder_qr.cu): cluster panels + DGEMM updates
+  // hand-written blocked Householder QR (householder_qr.cu), two levels: cluster panels of w
+  // columns, whose updates stay inside an outer block of NBO columns; the outer block's reflectors
+  // are merged into one compact-WY factor (T from G = Y^T Y, larft) and applied to the trailing
+  // matrix and in the Q formation as K = NBO DGEMMs (the rank-w updates re-read the whole trailing
+  // matrix once per panel)
   cudaStream_t s = ctx->stream;
   // panel width: 32 columns, halved until the tallest panel's rows fit one cluster's shared memory
   int w = 32, c = 0;
   while (w > 1 && qr_panel_plan(m, w, &c) == 0) w /= 2;
   if (qr_panel_plan(m, w, &c) == 0) throw Status(SSSVD_E_LENGTH, "thin_qr: operator too tall for the on-chip QR panel");
+  static const char* nbo_env = std::getenv("SSSVD_QR_NB");
+  // measured (tools/qr_time.py): the merged factor pays off from k ~ 1024 (16384 x 2048: 52 -> 35
+  // ms); below, the larft + Y^T Y overhead outweighs the saved re-reads (4096 x 512: 4.4 vs 4.8 ms)
+  const int nbo_default = k >= 1024 ? 128 : w;
+  const int NBO = std::max(w, std::min(128, nbo_env ? std::atoi(nbo_env) / w * w : nbo_default));
   const int npanel = (k + w - 1) / w;
+  const int nblock = (k + NBO - 1) / NBO;
   double* Y = ctx->qy.as<double>((size_t)m * k);
-  double* T = ctx->qt.as<double>((size_t)npanel * 1024);
-  double* Wt = ctx->qw.as<double>((size_t)2 * w * k + 64);
-  double* W2 = Wt + (size_t)w * k;
+  double* T = ctx->qt.as<double>((size_t)npanel * 1024 + (size_t)nblock * NBO * NBO + (size_t)NBO * NBO);
+  double* Tb = T + (size_t)npanel * 1024;                 // [nblock][NBO][NBO]
+  double* Gb = Tb + (size_t)nblock * NBO * NBO;            // [NBO][NBO]
+  double* Wt = ctx->qw.as<double>((size_t)2 * NBO * k + 64);
+  double* W2 = Wt + (size_t)NBO * k;
   double* tau = ctx->t7.as<double>(k + 64);
-  for (int p = 0; p < npanel; ++p) {
-    const int j = p * w, wp = std::min(w, k - j), mp = m - j, nt = k - j - wp;
-    CK(qr_panel(A, m, m, j, wp, Y + (size_t)j * m + j, m, T + (size_t)p * 1024, tau + j, s));
+  // the block reflector Y_b spans rows jb..m: the rows above each panel's diagonal must be zero
+  CK(cudaMemsetAsync(Y, 0, sizeof(double) * m * k, s));
+  for (int jb = 0; jb < k; jb += NBO) {
+    const int kb = std::min(NBO, k - jb), mb = m - jb;
+    for (int j = jb; j < jb + kb; j += w) {
+      const int p = j / w, wp = std::min(w, jb + kb - j), mp = m - j, ntb = jb + kb - j - wp;
+      CK(qr_panel(A, m, m, j, wp, Y + (size_t)j * m + j, m, T + (size_t)p * 1024, tau + j, s));
+      if (ntb > 0) {
+        // inside the outer block: A[j:m, j+wp:jb+kb] -= Y (T^T (Y^T A[j:m, j+wp:jb+kb]))
+        dgemm(ctx, true, false, wp, ntb, mp, 1.0, Y + (size_t)j * m + j, m, A + (size_t)(j + wp) * m + j, m, 0.0, Wt, wp);
+        dgemm(ctx, true, false, wp, ntb, wp, 1.0, T + (size_t)p * 1024, 32, Wt, wp, 0.0, W2, wp);
+        dgemm(ctx, false, false, mp, ntb, wp, -1.0, Y + (size_t)j * m + j, m, W2, wp, 1.0,
+              A + (size_t)(j + wp) * m + j, m);
+      }
+    }
+    double* Yb = Y + (size_t)jb * m + jb;
+    double* Tbb = Tb + (size_t)(jb / NBO) * NBO * NBO;
+    if (kb > w) {
+      dgemm(ctx, true, false, kb, kb, mb, 1.0, Yb, m, Yb, m, 0.0, Gb, kb);
+      CK(larft(Gb, kb, tau + jb, Tbb, s));
+    }
+    const int nt = k - jb - kb;
     if (nt > 0) {
-      // A[j:m, j+wp:k] -= Y (T^T (Y^T A[j:m, j+wp:k]))
-      dgemm(ctx, true, false, wp, nt, mp, 1.0, Y + (size_t)j * m + j, m, A + (size_t)(j + wp) * m + j, m, 0.0, Wt, wp);
-      dgemm(ctx, true, false, wp, nt, wp, 1.0, T + (size_t)p * 1024, 32, Wt, wp, 0.0, W2, wp);
-      dgemm(ctx, false, false, mp, nt, wp, -1.0, Y + (size_t)j * m + j, m, W2, wp, 1.0, A + (size_t)(j + wp) * m + j, m);
+      // trailing columns: A[jb:m, jb+kb:k] -= Y_b (T_b^T (Y_b^T A[jb:m, jb+kb:k]))
+      const double* Tuse = kb > w ? Tbb : T + (size_t)(jb / w) * 1024;
+      const int ldt = kb > w ? kb : 32;
+      dgemm(ctx, true, false, kb, nt, mb, 1.0, Yb, m, A + (size_t)(jb + kb) * m + jb, m, 0.0, Wt, kb);
+      dgemm(ctx, true, false, kb, nt, kb, 1.0, Tuse, ldt, Wt, kb, 0.0, W2, kb);
+      dgemm(ctx, false, false, mb, nt, kb, -1.0, Yb, m, W2, kb, 1.0, A + (size_t)(jb + kb) * m + jb, m);
     }
   }
   CK(copy_r(A, m, k, R, s));
-  // Q = H_0 ... H_{p-1} [I; 0], backward: Q[j:m, j:k] -= Y (T (Y^T Q[j:m, j:k]))
+  // Q = H_0 ... H_{p-1} [I; 0], backward over the outer blocks: Q[jb:m, jb:k] -= Y_b (T_b (Y_b^T Q[jb:m, jb:k]))
   CK(eye(A, m, k, m, s));
-  for (int p = npanel - 1; p >= 0; --p) {
-    const int j = p * w, wp = std::min(w, k - j), mp = m - j, nq = k - j;
-    dgemm(ctx, true, false, wp, nq, mp, 1.0, Y + (size_t)j * m + j, m, A + (size_t)j * m + j, m, 0.0, Wt, wp);
-    dgemm(ctx, false, false, wp, nq, wp, 1.0, T + (size_t)p * 1024, 32, Wt, wp, 0.0, W2, wp);
-    dgemm(ctx, false, false, mp, nq, wp, -1.0, Y + (size_t)j * m + j, m, W2, wp, 1.0, A + (size_t)j * m + j, m);
+  for (int jb = (nblock - 1) * NBO; jb >= 0; jb -= NBO) {
+    const int kb = std::min(NBO, k - jb), mb = m - jb, nq = k - jb;
+    double* Yb = Y + (size_t)jb * m + jb;
+    const double* Tuse = kb > w ? Tb + (size_t)(jb / NBO) * NBO * NBO : T + (size_t)(jb / w) * 1024;
+    const int ldt = kb > w ? kb : 32;
+    dgemm(ctx, true, false, kb, nq, mb, 1.0, Yb, m, A + (size_t)jb * m + jb, m, 0.0, Wt, kb);
+    dgemm(ctx, false, false, kb, nq, kb, 1.0, Tuse, ldt, Wt, kb, 0.0, W2, kb);
+    dgemm(ctx, false, false, mb, nq, kb, -1.0, Yb, m, W2, kb, 1.0, A + (size_t)jb * m + jb, m);
   }
 }
 
@@ -791,15 +843,18 @@ static void svd_square(sssvd_gpu_ctx* ctx, double* B, int k, double* U, double* 
         cudaEventCreate(&je1);
         cudaEventRecord(je0, ctx->stream);
       }
-      // block Jacobi (shared-memory inner sweeps) where the block pair fits, else the scalar one
+      // default: the grid-wide block Jacobi (one block pair per SM per outer round); the
+      // one-cluster block kernel (SSSVD_JACOBI=cluster, k <= 512) and the scalar grid kernel
+      // (SSSVD_JACOBI=scalar, also the fallback where no block plan fits) stay selectable
       static const char* jb = std::getenv("SSSVD_JACOBI");
       const std::string jmode = jb ? jb : "";
-      const bool use_block = jmode != "scalar" && jmode != "grid" && k <= 512 && k >= 64 &&
-                             jacobi_block_smem(k) <= 220 * 1024;
-      int gb_b, gb_nbe, gb_tw;
+      const bool use_block = jmode == "cluster" && k <= 512 && k >= 64 && jacobi_block_smem(k) <= 220 * 1024;
+      int gb_b, gb_nbe, gb_rpl;
       size_t gb_smem;
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
       const bool use_grid_block = !use_block && jmode != "scalar" &&
-                                  jacobi_grid_block_plan(k, 148, &gb_b, &gb_nbe, &gb_tw, &gb_smem);
+                                  jacobi_grid_block_plan(k, sms, &gb_b, &gb_nbe, &gb_rpl, &gb_smem);
       if (use_block)
         CK(jacobi_svd_block(U, J, k, k, S, tol, 60, scr, sweeps, ctx->stream));
       else if (use_grid_block)
@@ -876,9 +931,11 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
   // ---- steps 1-2 (form_gram is part of steps 1-2 in every run, pipeline.hpp:124-125); the factor
   // cache lives only inside one solve, like the reference's per-accumulator cache
   double t0 = now_s();
+  TailProf tp12(s);
   ctx->has_gram = false;
   ctx->fact_valid = false;
   ensure_gram(ctx, cfg.gram_cap > 0 ? cfg.gram_cap : 8192);
+  tp12.mark("form_gram");
   std::vector<double> v0 = random_start(n, L, cfg.params.seed);
   double start_norm2 = 0;
   for (double x : v0) start_norm2 += x * x;
@@ -889,6 +946,14 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
   std::vector<std::complex<double>> t(rule.nodes.begin(), rule.nodes.begin() + h);
   int64_t jb = 0, je = h;
   shard_range(h, ctx->nranks, ctx->rank, &jb, &je);
+  {
+    // measurement only (tools/scale_estimate.py): SSSVD_SIM_RANKS="G:r" factors just rank r's
+    // shard of a G-rank run on this single GPU (no collective; the moments are partial sums)
+    static const char* sim = std::getenv("SSSVD_SIM_RANKS");
+    int sg = 0, sr = 0;
+    if (sim && std::sscanf(sim, "%d:%d", &sg, &sr) == 2 && sg > 0 && sr >= 0 && sr < sg)
+      shard_range(h, sg, sr, &jb, &je);
+  }
   double* Vd = ctx->V.as<double>((size_t)n * L);
   CK(cudaMemcpyAsync(Vd, v0.data(), sizeof(double) * n * L, cudaMemcpyHostToDevice, s));
   double* S = ctx->S.as<double>((size_t)(M + 1) * n * L);
@@ -913,12 +978,26 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
     CK(blocks_to_colmajor(S, (int)n, L, 1, Vd, s));
   }
   auto coef = moment_coefficients(w, t, h, M);
+  tp12.mark("start block + contour (host)");
+  // while the shifted-solve pass runs, a helper thread takes the pinned result buffers from the
+  // pool at their largest sizes (page-locking hundreds of MB costs ~0.3 s per GB when the pool
+  // has to grow)
+  auto reserve = std::async(std::launch::async, [res, m, n, L, M] {
+    const size_t rmax = (size_t)L * M;
+    res->left.resize((size_t)m * rmax);
+    res->right.resize((size_t)n * rmax);
+    res->blocks.resize((size_t)(M + 1) * n * L);
+    res->q.resize(rmax * rmax);
+  });
   CK(cudaEventRecord(e0, s));
   moment_pass(ctx, shifts, coef, h, jb, je, Vd, L, M, S);
   CK(cudaEventRecord(e1, s));
   allreduce_S(ctx, S, (size_t)(M + 1) * n * L);
   CK(cudaEventRecord(e2, s));
   CK(cudaEventSynchronize(e2));
+  tp12.mark("shifted solves + moments");
+  reserve.get();
+  tp12.mark("result buffer reservation");
   {
     float a = 0, b = 0;
     CK(cudaEventElapsedTime(&a, e0, e1));
@@ -935,6 +1014,7 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
   double* Sc = B[T_SC].as<double>((size_t)(M + 1) * n * L);
   CK(blocks_to_colmajor(S, (int)n, L, M + 1, Sc, s));
   CK(cudaStreamSynchronize(s));
+  tp12.mark("moment blocks layout");
   info.steps_1_2 = now_s() - t0;
   info.t_gram = ctx->t_gram;
   info.t_shifted_solves = ctx->t_solves;
@@ -950,21 +1030,30 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
   if (!(snorm > 1e-12 * starting_norm)) {   // pipeline.hpp:141-148
     info.empty = 1;
     res->note = kEmptyNote;
+    res->left.resize(0);
+    res->right.resize(0);
+    res->q.resize(0);
     info.step_3 = now_s() - t0;
     return;
   }
+  TailProf tp(s);
   double* Q = B[T_Q].as<double>((size_t)n * r);
   CK(cudaMemcpyAsync(Q, Sc, sizeof(double) * n * r, cudaMemcpyDeviceToDevice, s));
   double* R = B[T_R].as<double>((size_t)r * r);
   thin_qr(ctx, Q, (int)n, r, R);
+  tp.mark("low_rank thin_qr");
   double* UR = B[T_UR].as<double>((size_t)r * r);
   double* VR = B[T_VR].as<double>((size_t)r * r);   // W_S1 = VR[:, :rank]
   double* SV = B[T_SV].as<double>(r);
   svd_square(ctx, R, r, UR, SV, VR);
+  tp.mark("low_rank svd_square");
   std::vector<double> sv = d2h(SV, r, s);
   if (sv.empty() || !(sv[0] > 0)) {   // EmptySubspaceError caught at pipeline.hpp:151-156
     info.empty = 1;
     res->note = kEmptyNote;
+    res->left.resize(0);
+    res->right.resize(0);
+    res->q.resize(0);
     info.step_3 = now_s() - t0;
     return;
   }
@@ -975,6 +1064,7 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
   double* US1 = B[T_US1].as<double>((size_t)n * rank);
   dgemm(ctx, false, false, (int)n, rank, r, 1.0, Q, (int)n, UR, r, 0.0, US1, (int)n);
   CK(cudaStreamSynchronize(s));
+  tp.mark("U_S1 gemm");
   info.step_3 = now_s() - t0;
 
   const double* Ad = ctx->A.as<double>(0);
@@ -990,23 +1080,33 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
   int* perm_d = B[T_PERM].as<int>(rank);
   double* Ut = nullptr;
   double* Pm = nullptr;
+  double* Yk = nullptr;
   if (!naive) {
     // ---- step 4: project_qr (extract.hpp:43-57)
     t0 = now_s();
     Ut = B[T_UT].as<double>((size_t)m * rank);
     dgemm(ctx, false, false, (int)m, rank, (int)n, 1.0, Ad, lda, US1, (int)n, 0.0, Ut, (int)m);
+    Yk = B[T_Y].as<double>((size_t)m * rank);   // Y = A U_S1, kept for the Galerkin residuals
+    CK(cudaMemcpyAsync(Yk, Ut, sizeof(double) * m * rank, cudaMemcpyDeviceToDevice, s));
     double* Bm = B[T_BM].as<double>((size_t)rank * rank);
+    tp.mark("project gemm");
     thin_qr(ctx, Ut, (int)m, rank, Bm);
-    std::vector<double> bd = d2h(Bm, (size_t)rank * rank, s);
+    tp.mark("project thin_qr");
+    std::vector<double> bd(rank);   // the diagonal of B only (a strided copy)
+    CK(cudaMemcpy2DAsync(bd.data(), sizeof(double), Bm, sizeof(double) * (rank + 1), sizeof(double), rank,
+                         cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
     const double lead = std::abs(bd[0]);
     for (int i = 0; i < rank; ++i)
-      if (std::abs(bd[(size_t)i * rank + i]) <= 1e-14 * lead) info.rank_deficient_qr = 1;
+      if (std::abs(bd[i]) <= 1e-14 * lead) info.rank_deficient_qr = 1;
+    tp.mark("project rank flag d2h");
     info.step_4 = now_s() - t0;
     // ---- step 5: svd_small + assemble_triplets (extract.hpp:66-102)
     t0 = now_s();
     Pm = B[T_PM].as<double>((size_t)rank * rank);
     double* phi_d = B[T_PHI].as<double>(rank);
     svd_square(ctx, Bm, rank, Pm, phi_d, Qm);
+    tp.mark("svd_small svd_square");
     std::vector<double> phi = d2h(phi_d, rank, s);
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return phi[a] < phi[b]; });
     for (int i = 0; i < rank; ++i) sigma[i] = phi[order[i]];
@@ -1041,6 +1141,9 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
   CK(cudaMemcpyAsync(perm_d, order.data(), sizeof(int) * rank, cudaMemcpyHostToDevice, s));
   double* qs = B[T_QS].as<double>((size_t)rank * rank);           // q = Q[:, order]
   CK(gather_cols(Qm, rank, perm_d, nullptr, rank, rank, qs, rank, s));
+  // q (part of the result) goes out first, ahead of the triplet vectors on the copy engine
+  res->q.resize((size_t)rank * rank);
+  CK(cudaMemcpyAsync(res->q.data(), qs, sizeof(double) * rank * rank, cudaMemcpyDeviceToHost, s));
   dgemm(ctx, false, false, (int)n, rank, rank, 1.0, US1, (int)n, qs, rank, 0.0, right, (int)n);
   double* sig_d = B[T_SIG].as<double>(rank);
   if (!naive) {
@@ -1061,14 +1164,13 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
   // the triplet vectors are final: copy them out while the postprocess runs
   d2h_async(ctx, leftv, (size_t)m * tcount, res->left);
   d2h_async(ctx, right, (size_t)n * tcount, res->right);
-  std::vector<double> qhost = d2h(qs, (size_t)rank * rank, s);
+  tp.mark("assemble gemms");
   info.step_5 = now_s() - t0;
 
   // ---- postprocess (pipeline.hpp:179-208)
   t0 = now_s();
   info.count = tcount;
   res->sigma = sigma;
-  res->q = qhost;
   res->in_interval.resize(tcount);
   for (int i = 0; i < tcount; ++i) res->in_interval[i] = (sigma[i] >= cfg.interval_a && sigma[i] <= cfg.interval_b);
   // detect_spurious (postprocess.hpp:47-62)
@@ -1076,30 +1178,24 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
   for (double x : res->basis_sv)
     if (!(x > 0)) throw Status(SSSVD_E_INVALID_ARGUMENT, "detect_spurious: Sigma_S1 must be positive");
   info.spurious_threshold = cfg.params.spurious_threshold * sv_max;
-  res->tau.resize(tcount);
+  // tau (postprocess.hpp:56-60) and the estimator's Sigma^+ q (:86-93) in one pass over q on the
+  // device; transformed residual norms (postprocess.hpp:76-97):
+  //   ||S+ W Sigma^+ q_i - img_i U_S1 q_i|| / sigma_i
+  const double rcond = use_exp ? cfg.estimator_rcond_exp : cfg.estimator_rcond_identity;
+  std::vector<double> inv(rank);
+  for (int l = 0; l < rank; ++l) inv[l] = res->basis_sv[l] >= rcond * sv_max ? 1.0 / res->basis_sv[l] : 0.0;
+  double* inv_d = B[T_INV].as<double>(rank);
+  double* tau_d = B[T_TAU].as<double>(tcount);
+  double* qsc_d = B[T_QSC].as<double>((size_t)rank * tcount);
+  CK(cudaMemcpyAsync(inv_d, inv.data(), sizeof(double) * rank, cudaMemcpyHostToDevice, s));
+  CK(tau_scale(qs, rank, tcount, SV, inv_d, tau_d, qsc_d, s));
+  res->tau = d2h(tau_d, tcount, s);
   res->spurious.resize(tcount);
-  for (int i = 0; i < tcount; ++i) {
-    double num = 0, den = 0;
-    for (int l = 0; l < rank; ++l) {
-      const double v = qhost[(size_t)i * rank + l];
-      num += v * v;
-      den += v * v / res->basis_sv[l];
-    }
-    res->tau[i] = num / den;
-    res->spurious[i] = (res->tau[i] < info.spurious_threshold) || invalid[i];
-  }
-  // transformed residual norms (postprocess.hpp:76-97): ||S+ W Sigma^+ q_i - img_i U_S1 q_i|| / sigma_i
+  for (int i = 0; i < tcount; ++i) res->spurious[i] = (res->tau[i] < info.spurious_threshold) || invalid[i];
+  tp.mark("tau + Sigma^+ q");
   {
-    const double rcond = use_exp ? cfg.estimator_rcond_exp : cfg.estimator_rcond_identity;
-    std::vector<double> qsc(qhost.size());
-    for (int l = 0; l < rank; ++l) {
-      const double inv = res->basis_sv[l] >= rcond * sv_max ? 1.0 / res->basis_sv[l] : 0.0;
-      for (int i = 0; i < tcount; ++i) qsc[(size_t)i * rank + l] = inv * qhost[(size_t)i * rank + l];
-    }
-    double* qsc_d = B[T_QSC].as<double>((size_t)rank * tcount);
     double* coeff = B[T_COEFF].as<double>((size_t)r * tcount);
     double* X = B[T_X].as<double>((size_t)std::max(n, m) * tcount);
-    CK(cudaMemcpyAsync(qsc_d, qsc.data(), sizeof(double) * rank * tcount, cudaMemcpyHostToDevice, s));
     dgemm(ctx, false, false, r, tcount, rank, 1.0, VR, r, qsc_d, rank, 0.0, coeff, r);
     dgemm(ctx, false, false, (int)n, tcount, r, 1.0, Sc + (size_t)n * L, (int)n, coeff, r, 0.0, X, (int)n);
     std::vector<double> images(tcount);
@@ -1111,13 +1207,21 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
     CK(cudaMemcpyAsync(img_d, images.data(), sizeof(double) * tcount, cudaMemcpyHostToDevice, s));
     double* out_d = B[T_NRM].as<double>(3 * (size_t)tcount);
     CK(colnorm_diff(X, (int)n, right, (int)n, img_d, (int)n, tcount, out_d, s));
+    tp.mark("transformed residual");
     // exact residual ||A^T u - sigma v|| (postprocess.hpp:34-41), Galerkin ||A v - sigma u||
     CK(cudaMemcpyAsync(sig_d, sigma.data(), sizeof(double) * tcount, cudaMemcpyHostToDevice, s));
     dgemm(ctx, true, false, (int)n, tcount, (int)m, 1.0, Ad, lda, leftv, (int)m, 0.0, X, (int)n);
     CK(colnorm_diff(X, (int)n, right, (int)n, sig_d, (int)n, tcount, out_d + tcount, s));
-    dgemm(ctx, false, false, (int)m, tcount, (int)n, 1.0, Ad, lda, right, (int)n, 0.0, X, (int)m);
+    if (Yk) {
+      // A v_i = A U_S1 q_i = Y q_i with Y = A U_S1 kept from project_qr: an m x r x r product
+      // instead of m x n x r (equal up to rounding)
+      dgemm(ctx, false, false, (int)m, tcount, rank, 1.0, Yk, (int)m, qs, rank, 0.0, X, (int)m);
+    } else {
+      dgemm(ctx, false, false, (int)m, tcount, (int)n, 1.0, Ad, lda, right, (int)n, 0.0, X, (int)m);
+    }
     CK(colnorm_diff(X, (int)m, leftv, (int)m, sig_d, (int)m, tcount, out_d + 2 * tcount, s));
     std::vector<double> norms = d2h(out_d, 3 * (size_t)tcount, s);
+    tp.mark("exact + galerkin residuals");
     res->estimated.assign(norms.begin(), norms.begin() + tcount);
     for (int i = 0; i < tcount; ++i)
       res->estimated[i] = sigma[i] <= 1e-30 ? std::numeric_limits<double>::infinity() : res->estimated[i] / sigma[i];
@@ -1144,6 +1248,7 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
     }
   }
   CK(cudaStreamSynchronize(ctx->cstream));
+  tp.mark("calibration + result copies");
   info.postprocess = now_s() - t0;
   if (ctx->transposed) {   // pipeline.hpp:214-217
     std::swap(res->left, res->right);

@@ -1,4 +1,5 @@
-"""Two run_solve calls of one config in one process: first-call vs steady-state step timings."""
+"""Three run_solve calls of one config in one process: first call (eager), second (captures the
+shifted-solve pass as a CUDA graph) and steady state (graph replay)."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2109_13655_b200 import sssvd, workloads
@@ -6,7 +7,7 @@ c = int(sys.argv[1])
 w = workloads.CONFIGS[c]
 a, _ = workloads.make_operator(c)
 dev = sssvd.Device(0)
-for it in range(2):
+for it in range(3):
     for mode in w.modes:
         cfg = sssvd.RunConfig(w.a, w.b, mode=mode, params=sssvd.SsParams(block_size=w.L, moment_degree=w.M, quadrature_count=w.N), gram_cap=1 << 30)
         t0 = time.time(); r = sssvd.run_solve(a, cfg, dev); wall = time.time() - t0
