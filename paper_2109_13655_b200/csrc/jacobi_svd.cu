@@ -733,15 +733,19 @@ __device__ __forceinline__ bool gb_visit_smem(double* x, double* y, int k, doubl
 template <int RPL>
 __device__ __forceinline__ bool gb_visit(double (&x)[RPL], double* y, int k, double tol, int lane, double& cs,
                                          double& sn) {
-  double a = 0.0, bb = 0.0, g = 0.0;
+  // four partial sums per product: 4x shorter FMA dependency chains
+  double a4[4] = {0.0, 0.0, 0.0, 0.0}, b4[4] = {0.0, 0.0, 0.0, 0.0}, g4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
   for (int i = 0; i < RPL; ++i) {
     const int r = lane + 32 * i;
     const double yv = r < k ? y[r] : 0.0;
-    a = fma(x[i], x[i], a);
-    bb = fma(yv, yv, bb);
-    g = fma(x[i], yv, g);
+    a4[i & 3] = fma(x[i], x[i], a4[i & 3]);
+    b4[i & 3] = fma(yv, yv, b4[i & 3]);
+    g4[i & 3] = fma(x[i], yv, g4[i & 3]);
   }
+  double a = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+  double bb = (b4[0] + b4[1]) + (b4[2] + b4[3]);
+  double g = (g4[0] + g4[1]) + (g4[2] + g4[3]);
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     a += __shfl_xor_sync(0xffffffffu, a, off);
