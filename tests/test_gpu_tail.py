@@ -17,7 +17,7 @@ def graded(m, k, seed, decades=17.0):
 
 
 @pytest.mark.parametrize("m,k", [(700, 300), (4096, 512), (512, 512), (2000, 33), (13000, 64), (40, 1),
-                                 (32768, 40)])
+                                 (32768, 40), (2500, 1030), (1100, 1100)])
 def test_thin_qr_matches_lapack(dev, m, k):
     rng = np.random.default_rng(m + k)
     a = rng.standard_normal((m, k))

@@ -5,5 +5,6 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc $?" >> gpurun_out/smoke.log
 timeout 600 python bench.py --steps 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc $?" >> gpurun_out/bench.err
-timeout 900 python tools/scale_estimate.py --config 5 > gpurun_out/scale_cfg5.jsonl 2> gpurun_out/scale_cfg5.err; echo "scale rc $?" >> gpurun_out/scale_cfg5.err
+timeout 600 python bench.py --steps 5 --no-cpu-baseline > gpurun_out/bench2.json 2> gpurun_out/bench2.err
+timeout 1200 python tools/scale_estimate.py --config 5 > gpurun_out/scale_cfg5.jsonl 2> gpurun_out/scale_cfg5.err; echo "scale rc $?" >> gpurun_out/scale_cfg5.err
 tail -n 3 gpurun_out/pytest_gpu.log; tail -n 2 gpurun_out/smoke.log; cat gpurun_out/scale_cfg5.jsonl

@@ -22,7 +22,7 @@ for mode in modes:
     gthr, othr = g.spurious_threshold, o.verdict.threshold
     def near(s): return any(abs(s - e) <= 1e-9 * max(abs(e), s) for e in (w.a, w.b))
     def firm(s, tau, thr): return not near(s) and not (0.5 <= tau / thr <= 2.0)
-    matched, worst_sigma, worst_res_ratio, mism = 0, 0.0, 0.0, []
+    matched, worst_sigma, worst_res_ratio, mism, worst_vec = 0, 0.0, 0.0, [], 0.0
     for i in range(o.triplets.count()):
         if not o.triplets.in_interval[i] or o.verdict.spurious[i] or not firm(os_[i], o.verdict.tau[i], othr):
             continue
@@ -32,11 +32,18 @@ for mode in modes:
         if ok:
             matched += 1
             worst_sigma = max(worst_sigma, rel)
+            for gv, ov in ((g.triplets.left[:, j], o.triplets.left[:, i]), (g.triplets.right[:, j], o.triplets.right[:, i])):
+                worst_vec = max(worst_vec, min(np.linalg.norm(gv - ov), np.linalg.norm(gv + ov)))
             worst_res_ratio = max(worst_res_ratio, g.exact[j] / max(1e-9 * sigma.max(), 10 * o.residuals.exact[i]))
         else:
             mism.append({"oracle_sigma": float(os_[i]), "gpu_sigma": float(gs[j]), "rel": float(rel),
                          "gpu_tau_ratio": float(g.tau[j] / gthr), "oracle_tau_ratio": float(o.verdict.tau[i] / othr)})
+    # every oracle candidate inside [a, b] (converged or not): relative distance to the nearest GPU value
+    cand = [abs(gs[int(np.argmin(np.abs(gs - x)))] - x) / x for x, f in zip(os_, o.triplets.in_interval) if f]
     out = {"cfg": c, "mode": mode, "gpu_s": tg, "oracle_s": to, "cores": os.cpu_count(),
+           "in_interval_sigma_reldiff_median": float(np.median(cand)) if cand else None,
+           "in_interval_sigma_reldiff_max": float(np.max(cand)) if cand else None,
+           "firm_matched_vector_max_diff": worst_vec,
            "gpu_nonspurious": g.count_nonspurious_in_interval, "oracle_nonspurious": o.count_nonspurious_in_interval,
            "gpu_in_interval": g.count_in_interval, "oracle_in_interval": o.count_in_interval,
            "gpu_boundary": g.count_boundary, "oracle_boundary": o.count_boundary,
