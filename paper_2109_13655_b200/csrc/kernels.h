@@ -83,8 +83,10 @@ bool jacobi_grid_block_plan(int k, int sms, int* b, int* nbe, int* rpl, size_t* 
 cudaError_t moments(const double2* mats, int ld, long long stride, int xcol, int n, int L, int nb,
                     const double2* coef, int M, double* S, cudaStream_t s);
 cudaError_t blocks_to_colmajor(const double* S, int n, int L, int nblk, double* out, cudaStream_t s);
+// part: colnorm_scratch(rows, cols) doubles of per-chunk partial sums
+size_t colnorm_scratch(int rows, int cols);
 cudaError_t colnorm_diff(const double* X, int ldx, const double* Y, int ldy, const double* s, int rows,
-                         int cols, double* out, cudaStream_t st);
+                         int cols, double* out, double* part, cudaStream_t st);
 cudaError_t tau_scale(const double* q, int rank, int tcount, const double* sv, const double* inv, double* tau,
                       double* qsc, cudaStream_t st);
 cudaError_t gather_cols(const double* src, int lds, const int* perm, const double* scale, int rows,

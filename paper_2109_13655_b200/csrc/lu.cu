@@ -17,6 +17,7 @@
 // The trailing updates are zgemm_sub (zgemm.cu, DMMA).
 #include <cooperative_groups.h>
 #include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -26,28 +27,44 @@ namespace sssvd_gpu {
 // ----------------------------------------------------------------------------- K1 assembly
 // Mj[i][c] = -G[i][c] + (i == c ? z_j : 0) for c < n ; V[i][c-n] for n <= c < n+L.
 // G is symmetric, so reading it row-major is reading it column-major (shifted_solver.hpp:24-25).
-__global__ void assemble_kernel(const double* __restrict__ G, int n, int ldg,
-                                const double* __restrict__ V, int L, const double2* __restrict__ shifts,
-                                double2* __restrict__ out, int ld, long long stride) {
-  const int b = blockIdx.y;
-  double2* M = out + b * stride;
-  const double2 z = shifts[b];
-  const long long total = (long long)n * (n + L);
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(e / (n + L)), c = (int)(e % (n + L));
-    double2 v;
-    if (c < n) {
-      v = make_double2(-G[(size_t)i * ldg + c], 0.0);
-      if (c == i) {
-        v.x += z.x;
-        v.y += z.y;
-      }
+// One CTA per row i; each thread reads two consecutive entries of the row ONCE and writes them to
+// every shift of the batch (HBM: 8 n (n + L) bytes read, 16 B n (n + L) written per launch).
+constexpr int ASM_THREADS = 256;
+constexpr int ASM_MAXB = 64;
+__global__ void __launch_bounds__(ASM_THREADS)
+assemble_kernel(const double* __restrict__ G, int n, int ldg, const double* __restrict__ V, int L,
+                const double2* __restrict__ shifts, double2* __restrict__ out, int ld, long long stride, int nb) {
+  __shared__ double2 zs[ASM_MAXB];
+  for (int b = threadIdx.x; b < nb; b += ASM_THREADS) zs[b] = shifts[b];
+  __syncthreads();
+  const int i = blockIdx.x;
+  const int ncols = n + L;
+  const double* grow = G + (size_t)i * ldg;
+  for (int c = threadIdx.x; c < ncols; c += ASM_THREADS) {
+    const double v = c < n ? -grow[c] : V[(size_t)(c - n) * n + i];
+    double2* dst = out + (size_t)i * ld + c;
+    if (c == i) {
+      for (int b = 0; b < nb; ++b, dst += stride) __stcs(dst, make_double2(v + zs[b].x, zs[b].y));
     } else {
-      // V is column-major n x L (moments.hpp:84-94 fill order)
-      v = make_double2(V[(size_t)(c - n) * n + i], 0.0);
+      for (int b = 0; b < nb; ++b, dst += stride) __stcs(dst, make_double2(v, 0.0));
     }
-    M[(size_t)i * ld + c] = v;
+  }
+}
+
+// the per-shift variant (grid.y = shift): G is re-read once per shift (SSSVD_ASM=pershift)
+__global__ void __launch_bounds__(ASM_THREADS)
+assemble_pershift_kernel(const double* __restrict__ G, int n, int ldg, const double* __restrict__ V, int L,
+                         const double2* __restrict__ shifts, double2* __restrict__ out, int ld, long long stride) {
+  const int b = blockIdx.y;
+  const double2 z = shifts[b];
+  const int ncols = n + L;
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const double* grow = G + (size_t)i * ldg;
+    double2* dst = out + b * stride + (size_t)i * ld;
+    for (int c = threadIdx.x; c < ncols; c += ASM_THREADS) {
+      const double v = c < n ? -grow[c] : V[(size_t)(c - n) * n + i];
+      dst[c] = c == i ? make_double2(v + z.x, z.y) : make_double2(v, 0.0);
+    }
   }
 }
 
@@ -72,10 +89,19 @@ cudaError_t load_rhs(const double* V, int n, int L, double2* out, int ld, long l
 
 cudaError_t assemble(const double* G, int n, int ldg, const double* V, int L, const double2* shifts,
                      double2* out, int ld, long long stride, int batch, cudaStream_t s) {
-  long long total = (long long)n * (n + L);
-  int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 8);
-  assemble_kernel<<<dim3(blocks, batch), 256, 0, s>>>(G, n, ldg, V, L, shifts, out, ld, stride);
-  note_launch();
+  static const char* env = std::getenv("SSSVD_ASM");
+  if (env && std::string(env) == "pershift") {
+    assemble_pershift_kernel<<<dim3(std::min(n, 148 * 4), batch), ASM_THREADS, 0, s>>>(G, n, ldg, V, L, shifts, out,
+                                                                                      ld, stride);
+    note_launch();
+    return cudaGetLastError();
+  }
+  for (int b0 = 0; b0 < batch; b0 += ASM_MAXB) {
+    const int nbb = std::min(ASM_MAXB, batch - b0);
+    assemble_kernel<<<n, ASM_THREADS, 0, s>>>(G, n, ldg, V, L, shifts + b0, out + (size_t)b0 * stride, ld, stride,
+                                              nbb);
+    note_launch();
+  }
   return cudaGetLastError();
 }
 

@@ -12,9 +12,10 @@
 
 namespace sssvd_gpu {
 
-constexpr int MMAX = 32;
 
 // S is row-major [(M+1)][n][L]; X_j = rows 0..n-1, columns xcol..xcol+L-1 of mats[j].
+// MMAX: compile-time bound on M (accumulators in registers), instantiated for 8, 16 and 32.
+template <int MMAX>
 __global__ void __launch_bounds__(256)
 moments_kernel(const double2* __restrict__ mats, int ld, long long stride, int xcol, int n, int L,
                int nb, const double2* __restrict__ coef, int M, double* __restrict__ S) {
@@ -29,14 +30,26 @@ moments_kernel(const double2* __restrict__ mats, int ld, long long stride, int x
 #pragma unroll
     for (int k = 0; k <= MMAX; ++k)
       if (k <= M) acc[k] = S[k * nl + e];
-    for (int j = 0; j < nb; ++j) {
-      const double2 x = mats[j * stride + (size_t)i * ld + xcol + c];
+    // X_j loads in chunks of MCH shifts, all in flight before the (ascending-j) accumulation
+    constexpr int MCH = 8;
+    const double2* xp = mats + (size_t)i * ld + xcol + c;
+    for (int j0 = 0; j0 < nb; j0 += MCH) {
+      double2 xs[MCH];
 #pragma unroll
-      for (int k = 0; k <= MMAX; ++k) {
-        if (k <= M) {
-          const double2 w = cs[k * nb + j];
-          const double re = __dsub_rn(__dmul_rn(w.x, x.x), __dmul_rn(w.y, x.y));
-          acc[k] = __dadd_rn(acc[k], 2.0 * re);
+      for (int u = 0; u < MCH; ++u) xs[u] = j0 + u < nb ? __ldcs(xp + (j0 + u) * stride) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < MCH; ++u) {
+        if (j0 + u < nb) {
+          const double2 x = xs[u];
+          const int j = j0 + u;
+#pragma unroll
+          for (int k = 0; k <= MMAX; ++k) {
+            if (k <= M) {
+              const double2 w = cs[k * nb + j];
+              const double re = __dsub_rn(__dmul_rn(w.x, x.x), __dmul_rn(w.y, x.y));
+              acc[k] = __dadd_rn(acc[k], 2.0 * re);
+            }
+          }
         }
       }
     }
@@ -48,11 +61,16 @@ moments_kernel(const double2* __restrict__ mats, int ld, long long stride, int x
 
 cudaError_t moments(const double2* mats, int ld, long long stride, int xcol, int n, int L, int nb,
                     const double2* coef, int M, double* S, cudaStream_t s) {
-  if (M > MMAX) return cudaErrorInvalidValue;
+  if (M > 32) return cudaErrorInvalidValue;
   const long long nl = (long long)n * L;
   int blocks = (int)std::min<long long>((nl + 255) / 256, 148 * 8);
-  moments_kernel<<<blocks, 256, (size_t)(M + 1) * nb * sizeof(double2), s>>>(mats, ld, stride, xcol, n,
-                                                                           L, nb, coef, M, S);
+  const size_t smem = (size_t)(M + 1) * nb * sizeof(double2);
+  if (M <= 8)
+    moments_kernel<8><<<blocks, 256, smem, s>>>(mats, ld, stride, xcol, n, L, nb, coef, M, S);
+  else if (M <= 16)
+    moments_kernel<16><<<blocks, 256, smem, s>>>(mats, ld, stride, xcol, n, L, nb, coef, M, S);
+  else
+    moments_kernel<32><<<blocks, 256, smem, s>>>(mats, ld, stride, xcol, n, L, nb, coef, M, S);
   note_launch();
   return cudaGetLastError();
 }
@@ -85,38 +103,64 @@ cudaError_t blocks_to_colmajor(const double* S, int n, int L, int nblk, double* 
 }
 
 // out[j] = || X[:, j] - s_j * Y[:, j] ||_2 for column-major X (ldx), Y (ldy), rows x cols.
-// One CTA per column; s == nullptr means s_j = 0. The residual kernel of the tail
-// (postprocess.hpp:36-39 exact residual, pipeline.hpp:205-207 Galerkin, :91-95 estimate).
-__global__ void colnorm_diff_kernel(const double* __restrict__ X, int ldx, const double* __restrict__ Y,
-                                    int ldy, const double* __restrict__ s, int rows,
-                                    double* __restrict__ out) {
-  const int j = blockIdx.x;
+// s == nullptr means s_j = 0. The residual kernel of the tail (postprocess.hpp:36-39 exact
+// residual, pipeline.hpp:205-207 Galerkin, :91-95 estimate). HBM-bound: grid (column, row chunk
+// of CN_ROWS), 8 independent loads in flight per thread, per-chunk partial sums, then one warp
+// per column adds its chunks in a fixed order (deterministic) and takes the root.
+constexpr int CN_THREADS = 256, CN_UNROLL = 8, CN_ROWS = CN_THREADS * CN_UNROLL;
+__global__ void __launch_bounds__(CN_THREADS)
+colnorm_partial_kernel(const double* __restrict__ X, int ldx, const double* __restrict__ Y, int ldy,
+                       const double* __restrict__ s, int rows, double* __restrict__ part) {
+  const int j = blockIdx.x, ch = blockIdx.y;
   const double sj = s ? s[j] : 0.0;
   const double* x = X + (size_t)j * ldx;
   const double* y = Y ? Y + (size_t)j * ldy : nullptr;
+  const int r0 = ch * CN_ROWS + threadIdx.x;
+  double xv[CN_UNROLL], yv[CN_UNROLL];
+#pragma unroll
+  for (int u = 0; u < CN_UNROLL; ++u) {
+    const int r = r0 + u * CN_THREADS;
+    xv[u] = r < rows ? __ldcs(x + r) : 0.0;
+    yv[u] = (y && r < rows) ? __ldcs(y + r) : 0.0;
+  }
   double acc = 0.0;
-  for (int i = threadIdx.x; i < rows; i += blockDim.x) {
-    double v = x[i] - (y ? sj * y[i] : 0.0);
+#pragma unroll
+  for (int u = 0; u < CN_UNROLL; ++u) {
+    const double v = xv[u] - sj * yv[u];
     acc += v * v;
   }
-  __shared__ double red[32];
+  __shared__ double red[CN_THREADS / 32];
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
   if (threadIdx.x < 32) {
-    acc = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    acc = threadIdx.x < CN_THREADS / 32 ? red[threadIdx.x] : 0.0;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (threadIdx.x == 0) out[j] = sqrt(acc);
+    if (threadIdx.x == 0) part[(size_t)j * gridDim.y + ch] = acc;
   }
 }
 
+__global__ void colnorm_finish_kernel(const double* __restrict__ part, int chunks, int cols, double* __restrict__ out) {
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (j >= cols) return;
+  double acc = 0.0;
+  for (int c = lane; c < chunks; c += 32) acc += part[(size_t)j * chunks + c];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) out[j] = sqrt(acc);
+}
+
+size_t colnorm_scratch(int rows, int cols) { return (size_t)cols * ((rows + CN_ROWS - 1) / CN_ROWS); }
+
 cudaError_t colnorm_diff(const double* X, int ldx, const double* Y, int ldy, const double* s, int rows,
-                         int cols, double* out, cudaStream_t st) {
+                         int cols, double* out, double* part, cudaStream_t st) {
   if (cols <= 0) return cudaSuccess;
-  colnorm_diff_kernel<<<cols, 256, 0, st>>>(X, ldx, Y, ldy, s, rows, out);
-  note_launch();
+  const int chunks = (rows + CN_ROWS - 1) / CN_ROWS;
+  colnorm_partial_kernel<<<dim3(cols, chunks), CN_THREADS, 0, st>>>(X, ldx, Y, ldy, s, rows, part);
+  colnorm_finish_kernel<<<(cols + 7) / 8, 256, 0, st>>>(part, chunks, cols, out);
+  note_launch(2);
   return cudaGetLastError();
 }
 

@@ -145,7 +145,7 @@ struct TailProf {
 using namespace sssvd_gpu;
 
 enum TailBuf { T_SC, T_Q, T_R, T_UR, T_VR, T_SV, T_US1, T_QM, T_LEFT, T_RIGHT, T_PERM, T_UT, T_BM, T_PM, T_PHI,
-               T_QS, T_SIG, T_PS, T_QSC, T_COEFF, T_X, T_IMG, T_NRM, T_INV, T_TAU, T_Y, T_COUNT };
+               T_QS, T_SIG, T_PS, T_QSC, T_COEFF, T_X, T_IMG, T_NRM, T_INV, T_TAU, T_Y, T_CNP, T_COUNT };
 
 struct sssvd_gpu_ctx {
   int device = 0;
@@ -1203,12 +1203,13 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
     double* img_d = B[T_IMG].as<double>(tcount);
     CK(cudaMemcpyAsync(img_d, images.data(), sizeof(double) * tcount, cudaMemcpyHostToDevice, s));
     double* out_d = B[T_NRM].as<double>(3 * (size_t)tcount);
-    CK(colnorm_diff(X, (int)n, right, (int)n, img_d, (int)n, tcount, out_d, s));
+    B[T_CNP].as<double>(colnorm_scratch((int)std::max(n, m), tcount));   // sized once for the three norms
+    CK(colnorm_diff(X, (int)n, right, (int)n, img_d, (int)n, tcount, out_d, B[T_CNP].as<double>(colnorm_scratch((int)n, tcount)), s));
     tp.mark("transformed residual");
     // exact residual ||A^T u - sigma v|| (postprocess.hpp:34-41), Galerkin ||A v - sigma u||
     CK(cudaMemcpyAsync(sig_d, sigma.data(), sizeof(double) * tcount, cudaMemcpyHostToDevice, s));
     dgemm(ctx, true, false, (int)n, tcount, (int)m, 1.0, Ad, lda, leftv, (int)m, 0.0, X, (int)n);
-    CK(colnorm_diff(X, (int)n, right, (int)n, sig_d, (int)n, tcount, out_d + tcount, s));
+    CK(colnorm_diff(X, (int)n, right, (int)n, sig_d, (int)n, tcount, out_d + tcount, B[T_CNP].as<double>(colnorm_scratch((int)n, tcount)), s));
     if (Yk) {
       // A v_i = A U_S1 q_i = Y q_i with Y = A U_S1 kept from project_qr: an m x r x r product
       // instead of m x n x r (equal up to rounding)
@@ -1216,7 +1217,7 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
     } else {
       dgemm(ctx, false, false, (int)m, tcount, (int)n, 1.0, Ad, lda, right, (int)n, 0.0, X, (int)m);
     }
-    CK(colnorm_diff(X, (int)m, leftv, (int)m, sig_d, (int)m, tcount, out_d + 2 * tcount, s));
+    CK(colnorm_diff(X, (int)m, leftv, (int)m, sig_d, (int)m, tcount, out_d + 2 * tcount, B[T_CNP].as<double>(colnorm_scratch((int)m, tcount)), s));
     // one small read-back at the end: the copy engine is busy with the triplet vectors meanwhile
     std::vector<double> norms = d2h(out_d, 3 * (size_t)tcount, s);
     res->tau = d2h(tau_d, tcount, s);
