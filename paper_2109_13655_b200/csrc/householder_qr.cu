@@ -250,6 +250,222 @@ cudaError_t qr_panel(double* A, int lda, int m, int j, int w, double* Y, int ldy
   return e;
 }
 
+// ----------------------------------------------------------------------------- register panel
+// Same panel factorisation with the panel held in REGISTERS: 256 threads per CTA, thread t owns
+// rows lo + t + 256 r (r < RPT = 64 / W) of all W columns (64 doubles per thread). Per column: one
+// CTA + cluster reduction for the tail norm, then one for the W dot products v^T A[:, q] (which
+// also yield the Gram column y_q^T y_c for q < c), then the rank-1 update in registers. The
+// shared-memory panel kernel above re-read the whole panel from shared memory for every column
+// and was instruction-bound (ncu: IPC 1.64, ~1.4K instructions per warp per column).
+constexpr int QR_THREADS = 256;
+
+// lane l ends with the warp sum of acc[l % W] (transpose-reduce, W - 1 shuffles + log2(32 / W))
+template <int W>
+__device__ __forceinline__ double warp_transpose_reduce(double (&acc)[W], int lane) {
+#pragma unroll
+  for (int h = W / 2; h >= 1; h >>= 1) {
+    const bool upper = (lane & h) != 0;
+#pragma unroll
+    for (int q = 0; q < h; ++q) {
+      const double send = upper ? acc[q] : acc[q + h];
+      const double keep = upper ? acc[q + h] : acc[q];
+      acc[q] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+    }
+  }
+  double v = acc[0];
+#pragma unroll
+  for (int h = W; h < 32; h <<= 1) v += __shfl_xor_sync(0xffffffffu, v, h);
+  return v;
+}
+
+template <int W, bool CLUSTER>
+__global__ void __launch_bounds__(QR_THREADS, 1)
+qr_panel_reg_kernel(double* __restrict__ A, int lda, int m, int j, int w, int rp, double* __restrict__ Y, int ldy,
+                    double* __restrict__ Tout, double* __restrict__ tau_out) {
+  constexpr int RPT = 64 / W;
+  constexpr int NW = QR_THREADS / 32;
+  __shared__ double red1[2];          // tail-norm partial, alpha (CTA 0 only)
+  __shared__ double red2[W];          // dot partials of this CTA
+  __shared__ double wred1[NW];
+  __shared__ double wred2[NW][W];
+  __shared__ double wsum[W];
+  __shared__ double taus[32];
+  __shared__ double gram[32 * 32];    // G[a][b] = y_a . y_b (a < b)
+  __shared__ double Ts[32 * 32];
+  const int C = CLUSTER ? gridDim.x : 1;
+  const unsigned crank = CLUSTER ? cluster_ctarank() : 0u;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int mp = m - j;
+  const int lo = (int)crank * rp, hi = min(lo + rp, mp);
+  double x[RPT][W];
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int gi = lo + tid + QR_THREADS * r;
+#pragma unroll
+    for (int q = 0; q < W; ++q) x[r][q] = (gi < hi && q < w) ? A[(size_t)(j + q) * lda + j + gi] : 0.0;
+  }
+#pragma unroll
+  for (int c = 0; c < W; ++c) {
+    // ---- tail norm below the diagonal; alpha = A[c][c] (relative row c: CTA 0, thread c, r = 0)
+    double ss = 0.0;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int gi = lo + tid + QR_THREADS * r;
+      if (gi > c && gi < hi) ss = fma(x[r][c], x[r][c], ss);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    if (lane == 0) wred1[warp] = ss;
+    if (crank == 0 && tid == c) red1[1] = x[0][c];
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < NW; ++q) t += wred1[q];
+      red1[0] = t;
+    }
+    qp_sync<CLUSTER>();
+    double tail2 = 0.0;
+    for (int q = 0; q < C; ++q) tail2 += qp_ld<CLUSTER>(red1, q);
+    const double alpha = qp_ld<CLUSTER>(red1 + 1, 0);
+    double tau = 0.0, beta = alpha, scale = 0.0;
+    if (tail2 > 0.0) {
+      beta = -copysign(sqrt(fma(alpha, alpha, tail2)), alpha);
+      tau = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    if (tid == 0) taus[c] = tau;
+    // ---- v = x / (alpha - beta) below the diagonal, v_c = 1; one reduction gives v^T A[:, q]
+    //      for q > c and the Gram column G[q][c] = y_q . y_c for q < c
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int gi = lo + tid + QR_THREADS * r;
+      if (gi > c && gi < hi) x[r][c] *= scale;
+    }
+    // in groups of at most 16 columns (bounds the accumulator registers next to the panel)
+    constexpr int WG = W < 16 ? W : 16;
+#pragma unroll
+    for (int g0 = 0; g0 < W; g0 += WG) {
+      double acc[WG];
+#pragma unroll
+      for (int q = 0; q < WG; ++q) acc[q] = 0.0;
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const int gi = lo + tid + QR_THREADS * r;
+        if (gi >= c && gi < hi) {
+          double v = x[r][c];   // (a select of the constant against the element would make the
+          v = gi == c ? 1.0 : v; //  front end address the panel array: it would leave registers)
+#pragma unroll
+          for (int q = 0; q < WG; ++q)
+            if (g0 + q != c) acc[q] = fma(v, x[r][g0 + q], acc[q]);
+        }
+      }
+      const double part = warp_transpose_reduce<WG>(acc, lane);
+      if (lane < WG) wred2[warp][g0 + lane] = part;
+    }
+    __syncthreads();
+    if (tid < W) {
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < NW; ++q) t += wred2[q][tid];
+      red2[tid] = t;
+    }
+    qp_sync<CLUSTER>();
+    if (tid < W && tid != c) {
+      double t = 0.0;
+      for (int q = 0; q < C; ++q) t += qp_ld<CLUSTER>(red2 + tid, q);
+      if (tid > c) wsum[tid] = tau * t;
+      else gram[tid * 32 + c] = t;
+    }
+    __syncthreads();
+    // ---- rank-1 update of rows >= c of the columns q > c (registers); R[c][c] = beta
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int gi = lo + tid + QR_THREADS * r;
+      if (gi >= c && gi < hi) {
+        double v = x[r][c];   // (a select of the constant against the element would make the
+          v = gi == c ? 1.0 : v; //  front end address the panel array: it would leave registers)
+#pragma unroll
+        for (int q = c + 1; q < W; ++q) x[r][q] = fma(-wsum[q], v, x[r][q]);
+        if (gi == c) x[r][c] = beta;
+      }
+    }
+  }
+  // ---- write back: A holds R on/above the diagonal and v below; Y explicit (unit diagonal, zeros)
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int gi = lo + tid + QR_THREADS * r;
+    if (gi < hi) {
+#pragma unroll
+      for (int q = 0; q < W; ++q)
+        if (q < w) {
+          A[(size_t)(j + q) * lda + j + gi] = x[r][q];
+          Y[(size_t)q * ldy + gi] = gi < q ? 0.0 : (gi == q ? 1.0 : x[r][q]);
+        }
+    }
+  }
+  // red2 may still be read remotely by slower CTAs of the last column
+  qp_sync<CLUSTER>();
+  if (crank == 0 && warp == 0) {
+    // dlarft (forward, columnwise) over the w columns, lane a owns row a
+    for (int b = 0; b < 32; ++b) {
+      const double tb = b < w ? taus[b] : 0.0;
+      double t = 0.0;
+      if (lane < b && b < w)
+        for (int q = lane; q < b; ++q) t = fma(Ts[q * 32 + lane], gram[q * 32 + b], t);
+      Ts[b * 32 + lane] = lane < b ? -tb * t : (lane == b ? tb : 0.0);
+      __syncwarp();
+    }
+    for (int e = lane; e < 32 * 32; e += 32) Tout[e] = Ts[e];
+    if (lane < w) tau_out[lane] = taus[lane];
+  }
+}
+
+// rows capacity of one register panel CTA for width W: 256 threads x 64 / W rows
+int qr_panel_reg_rows(int W) { return QR_THREADS * (64 / W); }
+
+cudaError_t qr_panel_reg(double* A, int lda, int m, int j, int w, int W, double* Y, int ldy, double* T, double* tau,
+                         cudaStream_t s) {
+  if (w < 1 || w > W || (W != 8 && W != 16 && W != 32)) return cudaErrorInvalidValue;
+  const int mp = m - j, cap = qr_panel_reg_rows(W);
+  int C = 1;
+  while (C < 16 && (mp + C - 1) / C > cap) C *= 2;
+  const int rp = (mp + C - 1) / C;
+  if (rp > cap) return cudaErrorInvalidValue;
+  static bool configured = false;
+  if (!configured) {
+    for (auto fn : {qr_panel_reg_kernel<8, true>, qr_panel_reg_kernel<16, true>, qr_panel_reg_kernel<32, true>}) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    configured = true;
+  }
+  cudaError_t e;
+  if (C == 1) {
+    if (W == 8) qr_panel_reg_kernel<8, false><<<1, QR_THREADS, 0, s>>>(A, lda, m, j, w, rp, Y, ldy, T, tau);
+    else if (W == 16) qr_panel_reg_kernel<16, false><<<1, QR_THREADS, 0, s>>>(A, lda, m, j, w, rp, Y, ldy, T, tau);
+    else qr_panel_reg_kernel<32, false><<<1, QR_THREADS, 0, s>>>(A, lda, m, j, w, rp, Y, ldy, T, tau);
+    e = cudaGetLastError();
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C, 1, 1);
+    cfg.blockDim = dim3(QR_THREADS, 1, 1);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (W == 8) e = cudaLaunchKernelEx(&cfg, qr_panel_reg_kernel<8, true>, A, lda, m, j, w, rp, Y, ldy, T, tau);
+    else if (W == 16) e = cudaLaunchKernelEx(&cfg, qr_panel_reg_kernel<16, true>, A, lda, m, j, w, rp, Y, ldy, T, tau);
+    else e = cudaLaunchKernelEx(&cfg, qr_panel_reg_kernel<32, true>, A, lda, m, j, w, rp, Y, ldy, T, tau);
+  }
+  note_launch();
+  return e;
+}
+
 // Block reflector factor of an outer block (LAPACK dlarft, forward / columnwise): H_0 ... H_{kb-1}
 // = I - Y T Y^T with T upper triangular, T_ii = tau_i and T[0:i, i] = -tau_i T[0:i, 0:i] G[0:i, i],
 // where G = Y^T Y (kb x kb, column-major, from one DGEMM). One CTA, T in shared memory.

@@ -104,6 +104,10 @@ size_t qr_panel_smem(int rp, int w);
 int qr_panel_plan(int mp, int w, int* cluster);
 cudaError_t qr_panel(double* A, int lda, int m, int j, int w, double* Y, int ldy, double* T, double* tau,
                      cudaStream_t s);
+// register-resident panel (householder_qr.cu): W in {8, 16, 32}, up to 16 x qr_panel_reg_rows(W) rows
+int qr_panel_reg_rows(int W);
+cudaError_t qr_panel_reg(double* A, int lda, int m, int j, int w, int W, double* Y, int ldy, double* T, double* tau,
+                         cudaStream_t s);
 cudaError_t eye(double* Q, int m, int k, int ldq, cudaStream_t s);
 // T (kb x kb) of the block reflector H_0..H_{kb-1} = I - Y T Y^T from G = Y^T Y and tau (kb <= 128)
 cudaError_t larft(const double* G, int kb, const double* tau, double* T, cudaStream_t s);

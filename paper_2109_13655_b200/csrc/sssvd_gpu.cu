@@ -723,10 +723,21 @@ static void thin_qr(sssvd_gpu_ctx* ctx, double* A, int m, int k, double* R) {
   // matrix and in the Q formation as K = NBO DGEMMs (the rank-w updates re-read the whole trailing
   // matrix once per panel)
   cudaStream_t s = ctx->stream;
-  // panel width: 32 columns, halved until the tallest panel's rows fit one cluster's shared memory
+  // panel width: 32 columns, halved until the tallest panel's rows fit one cluster (register panel:
+  // 16 CTAs x 256 threads x 64 / w rows; shared-memory panel: its slab budget, the fallback and
+  // SSSVD_QR_PANEL=smem)
+  static const char* pe = std::getenv("SSSVD_QR_PANEL");
+  const bool reg_panel = !(pe && std::string(pe) == "smem");
   int w = 32, c = 0;
-  while (w > 1 && qr_panel_plan(m, w, &c) == 0) w /= 2;
-  if (qr_panel_plan(m, w, &c) == 0) throw Status(SSSVD_E_LENGTH, "thin_qr: operator too tall for the on-chip QR panel");
+  if (reg_panel) {
+    while (w > 8 && m > 16 * qr_panel_reg_rows(w)) w /= 2;
+  }
+  const bool use_reg = reg_panel && m <= 16 * qr_panel_reg_rows(w);
+  if (!use_reg) {
+    w = 32;
+    while (w > 1 && qr_panel_plan(m, w, &c) == 0) w /= 2;
+    if (qr_panel_plan(m, w, &c) == 0) throw Status(SSSVD_E_LENGTH, "thin_qr: operator too tall for the on-chip QR panel");
+  }
   static const char* nbo_env = std::getenv("SSSVD_QR_NB");
   // measured (tools/qr_time.py): the merged factor pays off from k ~ 1024 (16384 x 2048: 52 -> 35
   // ms); below, the larft + Y^T Y overhead outweighs the saved re-reads (4096 x 512: 4.4 vs 4.8 ms)
@@ -747,7 +758,10 @@ static void thin_qr(sssvd_gpu_ctx* ctx, double* A, int m, int k, double* R) {
     const int kb = std::min(NBO, k - jb), mb = m - jb;
     for (int j = jb; j < jb + kb; j += w) {
       const int p = j / w, wp = std::min(w, jb + kb - j), mp = m - j, ntb = jb + kb - j - wp;
-      CK(qr_panel(A, m, m, j, wp, Y + (size_t)j * m + j, m, T + (size_t)p * 1024, tau + j, s));
+      if (use_reg)
+        CK(qr_panel_reg(A, m, m, j, wp, w, Y + (size_t)j * m + j, m, T + (size_t)p * 1024, tau + j, s));
+      else
+        CK(qr_panel(A, m, m, j, wp, Y + (size_t)j * m + j, m, T + (size_t)p * 1024, tau + j, s));
       if (ntb > 0) {
         // inside the outer block: A[j:m, j+wp:jb+kb] -= Y (T^T (Y^T A[j:m, j+wp:jb+kb]))
         dgemm(ctx, true, false, wp, ntb, mp, 1.0, Y + (size_t)j * m + j, m, A + (size_t)(j + wp) * m + j, m, 0.0, Wt, wp);

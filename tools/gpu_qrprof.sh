@@ -1,5 +1,7 @@
 mkdir -p gpurun_out
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/qr_launches.csv python tools/qr_launches.py 16384 2048 > gpurun_out/qr_ncu.log 2>&1
-python tools/launch_summary.py gpurun_out/qr_launches.csv > gpurun_out/qr_launch_summary.txt 2>&1
-SSSVD_DEBUG=1 SSSVD_TAIL_PROF=1 timeout 600 python tools/cfg_twice.py 5 > gpurun_out/tailprof_cfg5.log 2>&1; echo "rc $?" >> gpurun_out/tailprof_cfg5.log
-cat gpurun_out/qr_launch_summary.txt; grep -v "jacobi_svd k\|gram " gpurun_out/tailprof_cfg5.log | tail -28
+for shape in "4096 512" "512 512"; do
+set -- $shape
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/qr_launches_$1x$2.csv python tools/qr_launches.py $1 $2 > /dev/null 2>&1
+python tools/launch_summary.py gpurun_out/qr_launches_$1x$2.csv > gpurun_out/qr_launch_summary_$1x$2.txt 2>&1
+cat gpurun_out/qr_launch_summary_$1x$2.txt
+done

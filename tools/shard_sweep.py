@@ -33,19 +33,25 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--sim", default="")
     ap.add_argument("--groups", type=int, nargs="*", default=[4])
+    ap.add_argument("--env", nargs="*", default=[""], help="extra VAR=value settings, one run each")
     ap.add_argument("--child", action="store_true")
     a = ap.parse_args()
     if a.child:
         child(a.config)
         return
-    for grp in a.groups:
-        env = dict(os.environ, SSSVD_GROUPS=str(grp))
-        if a.sim:
-            env["SSSVD_SIM_RANKS"] = a.sim
-        p = subprocess.run([sys.executable, __file__, "--child", "--config", str(a.config)], env=env,
-                           capture_output=True, text=True)
-        line = p.stdout.strip().splitlines()[-1] if p.stdout.strip() else p.stderr[-400:]
-        print(f"config {a.config} sim {a.sim or '1:0'} groups {grp}: {line}", flush=True)
+    for extra in a.env:
+        for grp in a.groups:
+            env = dict(os.environ, SSSVD_GROUPS=str(grp))
+            if a.sim:
+                env["SSSVD_SIM_RANKS"] = a.sim
+            for kv in extra.split(","):
+                if "=" in kv:
+                    k, v = kv.split("=", 1)
+                    env[k] = v
+            p = subprocess.run([sys.executable, __file__, "--child", "--config", str(a.config)], env=env,
+                               capture_output=True, text=True)
+            line = p.stdout.strip().splitlines()[-1] if p.stdout.strip() else p.stderr[-400:]
+            print(f"config {a.config} sim {a.sim or '1:0'} groups {grp} {extra}: {line}", flush=True)
 
 
 if __name__ == "__main__":
