@@ -271,10 +271,13 @@ static LuPlan make_plan(int n, int L) {
   p.L = L;
   p.ld = ((n + L) + 7) / 8 * 8;
   p.stride = (long long)n * p.ld;
-  // outer block: the trailing update runs K = NB deep (SSSVD_NB = 128 or 256; the 256-wide block
-  // recurses once more inside the panel)
+  // outer block: the trailing update runs K = NB deep (the 256-wide block recurses once more inside
+  // the panel). Measured (tools/shard_sweep.py): n >= 8192 prefers 256 (config 4 1.72 -> 1.60 s,
+  // config-5 shard 3.23 -> 3.08 s: the K = 256 trailing GEMM halves the C traffic per flop), n = 4096
+  // prefers 128 (0.125 vs 0.138 s: the wider panel's latency is no longer hidden). SSSVD_NB overrides.
   static const char* nb_env = std::getenv("SSSVD_NB");
-  p.NB = (nb_env && std::atoi(nb_env) == 256) ? 256 : 128;
+  p.NB = n >= 8192 ? 256 : 128;
+  if (nb_env && (std::atoi(nb_env) == 128 || std::atoi(nb_env) == 256)) p.NB = std::atoi(nb_env);
   // leaf width W and cluster size C: the leaf slab (ceil(n/C) x (W+1) complex) must fit ~200 KB
   const size_t budget = 200 * 1024;
   p.W = 8;
