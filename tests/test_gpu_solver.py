@@ -48,7 +48,7 @@ def test_diagonal_closed_form(dev):
     assert abs(x[1, 1] - complex(-0.4, -0.2)) <= 1e-15
 
 
-@pytest.mark.parametrize("n,L", [(20, 5), (100, 7), (600, 16), (1500, 32), (3000, 20)])
+@pytest.mark.parametrize("n,L", [(20, 5), (100, 7), (600, 16), (1500, 32), (3000, 20), (8192, 4)])   # 8192: NB = 256
 def test_residual_bound_random_symmetric(dev, n, L):
     from paper_2109_13655_b200 import sssvd
     g = sym(n, 7)
