@@ -1570,6 +1570,77 @@ sssvd_status sssvd_debug_svd_square(sssvd_gpu_ctx* ctx, const double* b, int64_t
   });
 }
 
+namespace {
+__global__ void debug_fill_kernel(double* p, long long cnt, unsigned long long seed) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt; i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long x = (i + 1) * 0x9E3779B97F4A7C15ull ^ seed;
+    x ^= x >> 31; x *= 0xBF58476D1CE4E5B9ull; x ^= x >> 29;
+    p[i] = (double)(x >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+  }
+}
+__global__ void debug_diff_kernel(const unsigned long long* a, const unsigned long long* b, long long cnt,
+                                  unsigned long long* out) {
+  unsigned long long c = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt; i += (long long)gridDim.x * blockDim.x)
+    c += a[i] != b[i];
+  if (c) atomicAdd(out, c);
+}
+}  // namespace
+
+sssvd_status sssvd_debug_zgemm(sssvd_gpu_ctx* ctx, int variant, int64_t m, int64_t n, int64_t k, int64_t batch,
+                               int reps, double* ms_out, int64_t* mismatches_out) {
+  return guarded(ctx, [&]() {
+    if (m < 1 || n < 1 || k < 1 || batch < 1 || reps < 1 || variant < 0 || variant > 3)
+      throw Status(SSSVD_E_INVALID_ARGUMENT, "debug_zgemm: bad arguments");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const size_t na = (size_t)batch * m * k, nb = (size_t)batch * k * n, nc = (size_t)batch * m * n;
+    double2 *A = nullptr, *B = nullptr, *C0 = nullptr, *C1 = nullptr;
+    unsigned long long* cnt = nullptr;
+    auto release = [&]() { cudaFree(A); cudaFree(B); cudaFree(C0); cudaFree(C1); cudaFree(cnt); };
+    try {
+      CK(cudaMalloc(&A, na * sizeof(double2)));
+      CK(cudaMalloc(&B, nb * sizeof(double2)));
+      CK(cudaMalloc(&C0, nc * sizeof(double2)));
+      CK(cudaMalloc(&C1, nc * sizeof(double2)));
+      CK(cudaMalloc(&cnt, sizeof(unsigned long long)));
+      debug_fill_kernel<<<1184, 256, 0, s>>>((double*)A, 2 * (long long)na, 1);
+      debug_fill_kernel<<<1184, 256, 0, s>>>((double*)B, 2 * (long long)nb, 2);
+      debug_fill_kernel<<<1184, 256, 0, s>>>((double*)C0, 2 * (long long)nc, 3);
+      CK(cudaMemcpyAsync(C1, C0, nc * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+      zgemm_set_variant(0);
+      CK(zgemm_sub((int)m, (int)n, (int)k, A, (int)k, m * k, B, (int)n, k * n, C0, (int)n, m * n, (int)batch, s));
+      zgemm_set_variant(variant);
+      CK(zgemm_sub((int)m, (int)n, (int)k, A, (int)k, m * k, B, (int)n, k * n, C1, (int)n, m * n, (int)batch, s));
+      CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
+      debug_diff_kernel<<<1184, 256, 0, s>>>((const unsigned long long*)C0, (const unsigned long long*)C1,
+                                             2 * (long long)nc, cnt);
+      unsigned long long h = 0;
+      CK(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
+      cudaEvent_t e0, e1;
+      CK(cudaEventCreate(&e0));
+      CK(cudaEventCreate(&e1));
+      CK(cudaEventRecord(e0, s));
+      for (int r = 0; r < reps; ++r)
+        CK(zgemm_sub((int)m, (int)n, (int)k, A, (int)k, m * k, B, (int)n, k * n, C1, (int)n, m * n, (int)batch, s));
+      CK(cudaEventRecord(e1, s));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      *ms_out = ms / reps;
+      *mismatches_out = (int64_t)h;
+    } catch (...) {
+      zgemm_set_variant(-1);
+      release();
+      throw;
+    }
+    zgemm_set_variant(-1);
+    release();
+  });
+}
+
 sssvd_status sssvd_gpu_shifted_solve(sssvd_gpu_ctx* ctx, const double* g, int64_t n, double zr, double zi,
                                      const double* rhs, int64_t rhs_rows, int64_t L, double* x_out) {
   return guarded(ctx, [&]() {

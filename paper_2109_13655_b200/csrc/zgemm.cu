@@ -11,10 +11,9 @@
 // CTA tile 64x64 (4 warps, 32x32 each), K staged 16 at a time through a 3-deep cp.async ring.
 // Shared-memory row pitches are padded (A: 20, B: 66 double2) so every fragment load is one
 // conflict-free LDS.128 per quarter-warp.
-#include <atomic>
-#include <vector>
-
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -113,14 +112,18 @@ void zgemm_profile_collect(double* ms, double* flops, unsigned long long* launch
 }
 
 namespace {
+// CTA tile BM x BN = 64 x 64 complex, K staged BK = 16 at a time through a STAGES-deep cp.async
+// ring. The warp tile is (8 WI) x (8 WJ): WI x WJ DMMA sub-tiles; (64 / 8WI) x (64 / 8WJ) warps.
+//   <4,4>:  4 warps of 32x32 (the original tile)      <4,2>: 8 warps of 32x16
+//   <2,4>:  8 warps of 16x32                           <2,2>: 16 warps of 16x16
+// More warps per SM shorten the gaps in the DMMA pipe left by one warp's fixed-latency waits.
 constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3;
 constexpr int LDA_S = BK + 4;   // 20 double2: row pitch of the A tile (== 4 mod 8)
 constexpr int LDB_S = BN + 2;   // 66 double2: row pitch of the B tile (== 2 mod 8)
 constexpr int A_STAGE = BM * LDA_S;
 constexpr int B_STAGE = BK * LDB_S;
-constexpr int THREADS = 128;
 
-template <bool GATHER>
+template <int THREADS, bool GATHER>
 __device__ __forceinline__ void load_stage(double2* As, double2* Bs, const double2* A, int lda,
                                            const double2* B, int ldb, const int* brow, int M, int N, int K,
                                            int m0, int n0, int k0, int tid) {
@@ -145,6 +148,7 @@ __device__ __forceinline__ void load_stage(double2* As, double2* Bs, const doubl
 // C half-tile h (rows 32h..32h+32 of the 64x64 tile) -> a free pipeline stage, pitch CP
 constexpr int CP = BN + 1;   // 65 double2: conflict-free fragment-pattern reads in the epilogue
 static_assert(32 * CP <= A_STAGE + B_STAGE, "C half-tile must fit one pipeline stage");
+template <int THREADS>
 __device__ __forceinline__ void load_c_half(double2* dst, const double2* C, int ldc, int M, int N, int m0,
                                             int n0, int h, int tid) {
 #pragma unroll
@@ -159,11 +163,13 @@ __device__ __forceinline__ void load_c_half(double2* dst, const double2* C, int 
 
 // SET: C = A B (C is not read); otherwise C -= A B. GATHER: row k of B is row brow[k] of the
 // B matrix (the pivoted rows of the panel block, read straight from their pre-interchange place).
-template <bool SET, bool GATHER>
-__global__ void __launch_bounds__(THREADS, 2)
+template <int WI, int WJ, bool SET, bool GATHER>
+__global__ void __launch_bounds__((64 / (8 * WI)) * (64 / (8 * WJ)) * 32, WI * WJ >= 8 ? 2 : 1)
 zgemm_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long long sA,
              const double2* __restrict__ B, int ldb, long long sB, const int* __restrict__ brow, int sR,
              double2* C, int ldc, long long sC, unsigned long long* __restrict__ stamp, int stamp_cap) {
+  constexpr int WARPS_N = 64 / (8 * WJ);
+  constexpr int THREADS = (64 / (8 * WI)) * WARPS_N * 32;
   extern __shared__ __align__(16) double2 smem[];
   if (stamp && threadIdx.x == 0) {
     unsigned long long t;
@@ -175,18 +181,18 @@ zgemm_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long l
   double2* Bs = smem + A_STAGE;
   constexpr int SSTRIDE = A_STAGE + B_STAGE;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1;
+  const int wm = warp / WARPS_N, wn = warp % WARPS_N;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   A += blockIdx.z * sA;
   B += blockIdx.z * sB;
   C += blockIdx.z * sC;
   if (GATHER) brow += blockIdx.z * sR;
 
-  double acc_re[4][4][2], acc_im[4][4][2];
+  double acc_re[WI][WJ][2], acc_im[WI][WJ][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < WI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < WJ; ++j) {
       acc_re[i][j][0] = acc_re[i][j][1] = 0.0;
       acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
     }
@@ -197,10 +203,11 @@ zgemm_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long l
   auto c_stage = [&](int h) { return smem + ((KT + h) % STAGES) * (A_STAGE + B_STAGE); };
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) load_stage<GATHER>(As + s * SSTRIDE, Bs + s * SSTRIDE, A, lda, B, ldb, brow, M, N, K, m0, n0, s * BK, tid);
+    if (s < KT)
+      load_stage<THREADS, GATHER>(As + s * SSTRIDE, Bs + s * SSTRIDE, A, lda, B, ldb, brow, M, N, K, m0, n0, s * BK, tid);
     if (!SET) {
       for (int h = 0; h < 2; ++h)
-        if (KT - 2 + h < 0 && s == 0) load_c_half(c_stage(h), C, ldc, M, N, m0, n0, h, tid);
+        if (KT - 2 + h < 0 && s == 0) load_c_half<THREADS>(c_stage(h), C, ldc, M, N, m0, n0, h, tid);
     }
     cp_async_commit();
   }
@@ -212,74 +219,76 @@ zgemm_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long l
       int nk = kt + STAGES - 1;
       if (nk < KT) {
         int st = nk % STAGES;
-        load_stage<GATHER>(As + st * SSTRIDE, Bs + st * SSTRIDE, A, lda, B, ldb, brow, M, N, K, m0, n0, nk * BK, tid);
+        load_stage<THREADS, GATHER>(As + st * SSTRIDE, Bs + st * SSTRIDE, A, lda, B, ldb, brow, M, N, K, m0, n0,
+                                    nk * BK, tid);
       } else if (!SET) {
         const int h = kt - (KT - 2);
-        if (h >= 0 && h < 2) load_c_half(c_stage(h), C, ldc, M, N, m0, n0, h, tid);
+        if (h >= 0 && h < 2) load_c_half<THREADS>(c_stage(h), C, ldc, M, N, m0, n0, h, tid);
       }
       cp_async_commit();
     }
-    const double2* as = As + (kt % STAGES) * SSTRIDE + (wm * 32 + fr) * LDA_S + fc;
-    const double2* bs = Bs + (kt % STAGES) * SSTRIDE + fc * LDB_S + wn * 32 + fr;
+    const double2* as = As + (kt % STAGES) * SSTRIDE + (wm * 8 * WI + fr) * LDA_S + fc;
+    const double2* bs = Bs + (kt % STAGES) * SSTRIDE + fc * LDB_S + wn * 8 * WJ + fr;
 #pragma unroll
     for (int kq = 0; kq < BK / 4; ++kq) {
-      double2 a[4], b[4];
+      double2 a[WI], b[WJ];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = as[i * 8 * LDA_S + kq * 4];
+      for (int i = 0; i < WI; ++i) a[i] = as[i * 8 * LDA_S + kq * 4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = bs[kq * 4 * LDB_S + j * 8];
-      double nai[4];
+      for (int j = 0; j < WJ; ++j) b[j] = bs[kq * 4 * LDB_S + j * 8];
+      double nai[WI];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) nai[i] = -a[i].y;
-      // four passes over the 16 independent (i, j) accumulators: the two DMMAs feeding the
-      // same accumulator are 32 instructions apart, so the fixed-latency pipe never waits
+      for (int i = 0; i < WI; ++i) nai[i] = -a[i].y;
+      // four passes over the WI x WJ independent accumulators: the two DMMAs feeding the same
+      // accumulator are 2 WI WJ instructions apart
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < WI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma884(acc_re[i][j][0], acc_re[i][j][1], a[i].x, b[j].x);
+        for (int j = 0; j < WJ; ++j) dmma884(acc_re[i][j][0], acc_re[i][j][1], a[i].x, b[j].x);
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < WI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma884(acc_im[i][j][0], acc_im[i][j][1], a[i].x, b[j].y);
+        for (int j = 0; j < WJ; ++j) dmma884(acc_im[i][j][0], acc_im[i][j][1], a[i].x, b[j].y);
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < WI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma884(acc_re[i][j][0], acc_re[i][j][1], nai[i], b[j].y);
+        for (int j = 0; j < WJ; ++j) dmma884(acc_re[i][j][0], acc_re[i][j][1], nai[i], b[j].y);
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < WI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma884(acc_im[i][j][0], acc_im[i][j][1], a[i].y, b[j].x);
+        for (int j = 0; j < WJ; ++j) dmma884(acc_im[i][j][0], acc_im[i][j][1], a[i].y, b[j].x);
     }
   }
   cp_async_wait<0>();
   __syncthreads();
 
-  // epilogue: C -= acc (fragment rows fr, cols 2*fc, 2*fc+1 of each 8x8 sub-tile). The 8 C
-  // values of a row block are loaded together before any store, so their latencies overlap.
+  // epilogue: C -= acc (fragment rows fr, cols 2*fc, 2*fc+1 of each 8x8 sub-tile). The C values
+  // of a row block are loaded together before any store, so their latencies overlap.
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int r = m0 + wm * 32 + i * 8 + fr;
+  for (int i = 0; i < WI; ++i) {
+    const int rt = wm * 8 * WI + i * 8 + fr;   // row inside the 64-row tile
+    const int r = m0 + rt;
     if (r >= M) continue;
-    double2* crow = C + (size_t)r * ldc + n0 + wn * 32 + 2 * fc;
-    const int cbase = n0 + wn * 32 + 2 * fc;
+    double2* crow = C + (size_t)r * ldc + n0 + wn * 8 * WJ + 2 * fc;
+    const int cbase = n0 + wn * 8 * WJ + 2 * fc;
     if (SET) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < WJ; ++j) {
         const int c = cbase + j * 8;
         if (c < N) crow[j * 8] = make_double2(acc_re[i][j][0], acc_im[i][j][0]);
         if (c + 1 < N) crow[j * 8 + 1] = make_double2(acc_re[i][j][1], acc_im[i][j][1]);
       }
     } else {
-      // C rows of this warp live in the prefetched half-tile wm (row i*8+fr, pitch CP)
-      const double2* cs = c_stage(wm) + (i * 8 + fr) * CP + wn * 32 + 2 * fc;
-      double2 v[4][2];
+      // the row lives in the prefetched half-tile rt / 32 (row rt % 32, pitch CP)
+      const double2* cs = c_stage(rt >> 5) + (rt & 31) * CP + wn * 8 * WJ + 2 * fc;
+      double2 v[WJ][2];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < WJ; ++j) {
         v[j][0] = cs[j * 8];
         v[j][1] = cs[j * 8 + 1];
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < WJ; ++j) {
         const int c = cbase + j * 8;
         if (c < N) crow[j * 8] = make_double2(v[j][0].x - acc_re[i][j][0], v[j][0].y - acc_im[i][j][0]);
         if (c + 1 < N) crow[j * 8 + 1] = make_double2(v[j][1].x - acc_re[i][j][1], v[j][1].y - acc_im[i][j][1]);
@@ -298,28 +307,54 @@ zgemm_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long l
 
 size_t zgemm_sub_smem() { return (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double2); }
 
+// warp-tile variant of the trailing-update GEMM: SSSVD_ZGEMM_V (0: 32x32, 1: 32x16, 2: 16x32,
+// 3: 16x16) or zgemm_set_variant (measurement hook)
+static int g_variant = -1;
+void zgemm_set_variant(int v) { g_variant = v; }
+static int zgemm_variant() {
+  if (g_variant < 0) {
+    const char* e = std::getenv("SSSVD_ZGEMM_V");
+    g_variant = e ? std::atoi(e) : 0;
+    if (g_variant < 0 || g_variant > 3) g_variant = 0;
+  }
+  return g_variant;
+}
+
+template <int WI, int WJ, bool SET, bool GATHER>
+static cudaError_t launch_v(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B, int ldb,
+                            long long sB, const int* brow, int sR, double2* C, int ldc, long long sC, int batch,
+                            cudaStream_t stream, unsigned long long* stamp) {
+  constexpr int THREADS = (64 / (8 * WI)) * (64 / (8 * WJ)) * 32;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(zgemm_kernel<WI, WJ, SET, GATHER>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zgemm_sub_smem());
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch);
+  zgemm_kernel<WI, WJ, SET, GATHER><<<grid, THREADS, zgemm_sub_smem(), stream>>>(
+      M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, stamp, g_prof.cap);
+  return cudaGetLastError();
+}
+
 template <bool SET, bool GATHER>
 static cudaError_t launch(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B, int ldb,
                           long long sB, const int* brow, int sR, double2* C, int ldc, long long sC, int batch,
                           cudaStream_t stream) {
   if (M <= 0 || N <= 0 || K <= 0 || batch <= 0) return cudaSuccess;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(zgemm_kernel<SET, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)zgemm_sub_smem());
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch);
   unsigned long long* stamp = nullptr;
   if (g_prof.in_pass && (int)g_prof.flops.size() < g_prof.cap) {
     stamp = g_prof.d_stamp + g_prof.flops.size();
     g_prof.flops.push_back(8.0 * M * (double)N * K * batch);
   }
-  zgemm_kernel<SET, GATHER><<<grid, THREADS, zgemm_sub_smem(), stream>>>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR,
-                                                                         C, ldc, sC, stamp, g_prof.cap);
   note_launch();
-  return cudaGetLastError();
+  switch (zgemm_variant()) {
+    case 1: return launch_v<4, 2, SET, GATHER>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stream, stamp);
+    case 2: return launch_v<2, 4, SET, GATHER>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stream, stamp);
+    case 3: return launch_v<2, 2, SET, GATHER>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stream, stamp);
+    default: return launch_v<4, 4, SET, GATHER>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stream, stamp);
+  }
 }
 
 cudaError_t zgemm_sub(int M, int N, int K, const double2* A, int lda, long long sA,

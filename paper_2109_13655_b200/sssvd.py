@@ -120,7 +120,7 @@ EXPORTED_SYMBOLS = [
     "sssvd_gpu_profile_gemm_collect", "sssvd_debug_leaf_profile", "sssvd_debug_gram_part",
     "sssvd_gpu_set_operator_csc", "sssvd_mm_read", "sssvd_mm_info_get", "sssvd_mm_values", "sssvd_mm_colptr",
     "sssvd_mm_rowind", "sssvd_mm_free", "sssvd_mm_write", "sssvd_host_last_error", "sssvd_build_model",
-    "sssvd_filter_profile", "sssvd_debug_thin_qr", "sssvd_debug_svd_square",
+    "sssvd_filter_profile", "sssvd_debug_thin_qr", "sssvd_debug_svd_square", "sssvd_debug_zgemm",
 ]
 
 class _MmInfo(ctypes.Structure):
@@ -165,6 +165,8 @@ def lib():
     L.sssvd_host_last_error.restype = ctypes.c_char_p
     L.sssvd_debug_thin_qr.argtypes = [vp, dp, i64, i64, dp, dp]
     L.sssvd_debug_svd_square.argtypes = [vp, dp, i64, dp, dp, dp]
+    L.sssvd_debug_zgemm.argtypes = [vp, ctypes.c_int, i64, i64, i64, i64, ctypes.c_int, dp,
+                                    ctypes.POINTER(ctypes.c_int64)]
     L.sssvd_build_model.argtypes = [ctypes.c_int, i64, i64, ctypes.c_uint64, dp, dp]
     L.sssvd_filter_profile.argtypes = [ctypes.c_double, ctypes.c_double, i64, ctypes.c_double, ctypes.c_int,
                                        ctypes.c_double, ctypes.c_double, i64, ctypes.c_int, dp, dp]

@@ -161,3 +161,15 @@ def test_gram_sharding_is_exact(dev):
         parts.append(out)
     assert np.array_equal(parts[0] + parts[1] + parts[2], g)
     assert all(np.count_nonzero(p) > 0 for p in parts)
+
+
+@pytest.mark.parametrize("variant", [1, 2, 3])
+@pytest.mark.parametrize("m,n,k,batch", [(200, 136, 128, 3), (64, 64, 16, 1), (77, 35, 9, 2), (1000, 1016, 64, 2)])
+def test_zgemm_warp_tile_variants_bitwise(dev, variant, m, n, k, batch):
+    """Every warp-tile variant of the trailing-update GEMM issues the same DMMA chain per entry of
+    C, so it must reproduce the 32x32 kernel bit for bit (ragged edges included)."""
+    import ctypes
+    from paper_2109_13655_b200 import sssvd
+    ms, mism = ctypes.c_double(), ctypes.c_int64()
+    dev.check(sssvd.lib().sssvd_debug_zgemm(dev.h, variant, m, n, k, batch, 1, ctypes.byref(ms), ctypes.byref(mism)))
+    assert mism.value == 0
