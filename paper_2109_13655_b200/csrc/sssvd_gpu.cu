@@ -162,7 +162,7 @@ struct sssvd_gpu_ctx {
   bool has_gram = false;
   DBuf A, G, gmax, mats, ipiv, shifts, coef, S, V, status, minpiv, scratch;
   DBuf t0, t1, t2, t7, work, info;
-  DBuf lw_linv, lw_T, lw_src, lw_disp, jscr, jperm, jq, jr, jj, qy, qt, qw;
+  DBuf lw_linv, lw_T, lw_src, lw_disp, lw2_linv, lw2_T, lw2_src, lw2_disp, jscr, jperm, jq, jr, jj, qy, qt, qw;
   // factor cache (moments.hpp:106-116): the last pass left shifts [fact_jb, fact_je) factored in
   // one resident batch of `mats`, so a later pass with the same operator/shifts/L only replays the
   // forward elimination of its new right-hand side and the back substitution
@@ -441,6 +441,7 @@ struct LuGroup {
   cudaStream_t s;      // high priority
   cudaStream_t s_lo;   // low priority (trailing GEMMs)
   cudaEvent_t ev_pre, ev_gemm;
+  LuWork Wb;           // look-ahead: workspace of the far trailing update on s_lo
 };
 
 static void lu_solve_groups(const LuPlan& P, std::vector<LuGroup>& G) {
@@ -464,6 +465,51 @@ static void lu_solve_groups(const LuPlan& P, std::vector<LuGroup>& G) {
   }
 }
 
+// Look-ahead (depth 1) version of lu_solve_groups. Block k's trailing update is split into the
+// next block's columns A(k) = [kb+NB, kb+2NB) and the far columns B(k) = [kb+2NB, n+L):
+//   s    (high priority): panel(k) -> [wait B(k-1)] -> A(k) -> panel(k+1) -> [wait B(k)] -> A(k+1) ...
+//   s_lo (low priority) :   [wait panel(k)] -> B(k) -> [wait panel(k+1)] -> B(k+1) ...
+// so panel k+1 factors while B(k) -- the big GEMM -- runs, instead of after it. A(k) and B(k)
+// read panel k and write disjoint columns; B(k-1) precedes A(k) because both update block k+1's
+// columns (blocks k-1 then k, the reference's order). Every column still receives every update
+// in the same order through the same kernels, so the factors are bitwise those of
+// lu_solve_groups. B(k) keeps its own interchange map / L11^-1 / U12 staging (Wb) because the
+// panel recursion on s reuses W meanwhile.
+static void lu_solve_groups_lookahead(const LuPlan& P, std::vector<LuGroup>& G) {
+  const int n = P.n, ncols = n + P.L;
+  for (int kb = 0; kb < n; kb += P.NB) {
+    const int nbk = std::min(P.NB, n - kb);
+    const int a_lo = kb + nbk;
+    const int a_hi = a_lo < n ? std::min(a_lo + P.NB, n) : a_lo;
+    for (auto& g : G) {
+      factor_rec(P, g.W, g.mats, g.ipiv, g.nb, g.s, kb, nbk, kb);
+      CK(cudaEventRecord(g.ev_pre, g.s));                       // panel k done
+      if (kb > 0) CK(cudaStreamWaitEvent(g.s, g.ev_gemm, 0));   // B(k-1) done
+      if (a_hi > a_lo) apply_panel(P, g.W, g.mats, g.ipiv, g.nb, g.s, kb, nbk, a_lo, a_hi);
+      CK(cudaStreamWaitEvent(g.s_lo, g.ev_pre, 0));
+      apply_panel(P, g.Wb, g.mats, g.ipiv, g.nb, g.s_lo, kb, nbk, a_hi, ncols);
+      CK(cudaEventRecord(g.ev_gemm, g.s_lo));
+    }
+  }
+  for (auto& g : G) CK(cudaStreamWaitEvent(g.s, g.ev_gemm, 0));   // the last B (the right-hand side)
+  const int nblocks = (n + P.NB - 1) / P.NB;
+  for (int bi = nblocks - 1; bi >= 0; --bi) {
+    const int kb = bi * P.NB, nbk = std::min(P.NB, n - kb);
+    for (auto& g : G) {
+      CK(trsm_upper_warp(g.mats, P.ld, P.stride, kb, nbk, n, ncols, g.nb, g.s));
+      if (kb > 0)
+        CK(zgemm_sub(kb, P.L, nbk, g.mats + kb, P.ld, P.stride, g.mats + (size_t)kb * P.ld + n, P.ld, P.stride,
+                     g.mats + n, P.ld, P.stride, g.nb, g.s));
+    }
+  }
+}
+
+// SSSVD_LOOKAHEAD=0 selects the plain grouped schedule (read per pass, so tests can compare both)
+static bool lookahead_on() {
+  const char* e = std::getenv("SSSVD_LOOKAHEAD");
+  return !(e && std::string(e) == "0");
+}
+
 static LuWork make_work(sssvd_gpu_ctx* ctx, const LuPlan& P, int B) {
   LuWork W;
   W.tstride = (long long)P.NB * (P.n + P.L);
@@ -471,6 +517,17 @@ static LuWork make_work(sssvd_gpu_ctx* ctx, const LuPlan& P, int B) {
   W.T = ctx->lw_T.as<double2>((size_t)B * W.tstride);
   W.src = ctx->lw_src.as<int>((size_t)B * P.NB);
   W.disp = ctx->lw_disp.as<int>((size_t)B * (2 * P.NB + 1));
+  return W;
+}
+
+// the second workspace of the look-ahead far update (same shapes)
+static LuWork make_work2(sssvd_gpu_ctx* ctx, const LuPlan& P, int B) {
+  LuWork W;
+  W.tstride = (long long)P.NB * (P.n + P.L);
+  W.linv = ctx->lw2_linv.as<double2>((size_t)B * P.NB * P.NB);
+  W.T = ctx->lw2_T.as<double2>((size_t)B * W.tstride);
+  W.src = ctx->lw2_src.as<int>((size_t)B * P.NB);
+  W.disp = ctx->lw2_disp.as<int>((size_t)B * (2 * P.NB + 1));
   return W;
 }
 
@@ -485,15 +542,17 @@ static LuWork work_slice(const LuWork& W, const LuPlan& P, int b0) {
 }
 
 static size_t bytes_per_shift(const LuPlan& P) {
+  // mats + ipiv + two LU workspaces (the look-ahead far update keeps its own)
   return (size_t)P.stride * sizeof(double2) + (size_t)P.n * sizeof(int) +
-         (size_t)P.NB * (P.n + P.L + P.NB) * sizeof(double2);
+         2 * (size_t)P.NB * (P.n + P.L + P.NB) * sizeof(double2);
 }
 
 static int choose_batch(sssvd_gpu_ctx* ctx, const LuPlan& P, int64_t shifts) {
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
   // keep what is already allocated for mats reusable; leave 4 GiB headroom for the tail
-  size_t avail = free_b + ctx->mats.cap + ctx->ipiv.cap + ctx->lw_T.cap + ctx->lw_linv.cap;
+  size_t avail = free_b + ctx->mats.cap + ctx->ipiv.cap + ctx->lw_T.cap + ctx->lw_linv.cap + ctx->lw2_T.cap +
+                 ctx->lw2_linv.cap;
   const size_t headroom = (size_t)4 << 30;
   avail = avail > headroom ? avail - headroom : avail / 2;
   int64_t b = std::max<int64_t>(1, (int64_t)(avail / bytes_per_shift(P)));
@@ -524,6 +583,8 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
   int* dstatus = ctx->status.as<int>(B);
   double* dmin = ctx->minpiv.as<double>(B);
   const LuWork work = make_work(ctx, P, B);
+  const bool lookahead = lookahead_on() && !reuse;
+  const LuWork work2 = lookahead ? make_work2(ctx, P, B) : LuWork{};
   std::vector<double2> hshift(B), hcoef((size_t)(M + 1) * B);
   std::vector<int> hstatus(B);
   for (int64_t j0 = jb; j0 < je; j0 += B) {
@@ -565,11 +626,15 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
           const int cnt = nb / ng + (g < nb % ng ? 1 : 0);
           CK(cudaStreamWaitEvent(ctx->gstream[g], ctx->ev_fork, 0));
           groups.push_back({mats + (size_t)b0 * P.stride, ipiv + (size_t)b0 * n, work_slice(work, P, b0), cnt,
-                            ctx->gstream[g], ctx->gstream_lo[g], ctx->ev_pre[g], ctx->ev_gemm[g]});
+                            ctx->gstream[g], ctx->gstream_lo[g], ctx->ev_pre[g], ctx->ev_gemm[g],
+                            lookahead ? work_slice(work2, P, b0) : LuWork{}});
           b0 += cnt;
         }
         const double th0 = now_s();
-        lu_solve_groups(P, groups);
+        if (lookahead)
+          lu_solve_groups_lookahead(P, groups);
+        else
+          lu_solve_groups(P, groups);
         const double th1 = now_s();
         for (int g = 0; g < ng; ++g) {
           CK(cudaEventRecord(ctx->ev_join[g], ctx->gstream[g]));
@@ -596,7 +661,8 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
           (uintptr_t)P.cluster, (uintptr_t)(P.leaf_variant + 1), (uintptr_t)P.ld, (uintptr_t)ctx->G.p,
           (uintptr_t)V_dev, (uintptr_t)mats, (uintptr_t)ipiv, (uintptr_t)work.linv, (uintptr_t)work.T,
           (uintptr_t)work.src, (uintptr_t)work.disp, (uintptr_t)dshift, (uintptr_t)dcoef, (uintptr_t)S_dev,
-          (uintptr_t)ctx->gmax.p, (uintptr_t)dstatus, (uintptr_t)dmin};
+          (uintptr_t)ctx->gmax.p, (uintptr_t)dstatus, (uintptr_t)dmin, (uintptr_t)lookahead,
+          (uintptr_t)work2.linv, (uintptr_t)work2.T, (uintptr_t)work2.src, (uintptr_t)work2.disp};
       for (auto& g : ctx->lu_graphs)
         if (g.key == key) replayed = &g;
       if (replayed) {
@@ -1369,7 +1435,7 @@ void sssvd_gpu_destroy(sssvd_gpu_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   DBuf* bufs[] = {&ctx->A, &ctx->G, &ctx->gmax, &ctx->mats, &ctx->ipiv, &ctx->shifts, &ctx->coef, &ctx->S, &ctx->V,
                   &ctx->status, &ctx->minpiv, &ctx->scratch, &ctx->t0, &ctx->t1, &ctx->t2, &ctx->t7, &ctx->work,
-                  &ctx->info, &ctx->lw_linv, &ctx->lw_T, &ctx->lw_src, &ctx->lw_disp, &ctx->jscr, &ctx->jperm, &ctx->jq, &ctx->jr, &ctx->jj,
+                  &ctx->info, &ctx->lw_linv, &ctx->lw_T, &ctx->lw_src, &ctx->lw_disp, &ctx->lw2_linv, &ctx->lw2_T, &ctx->lw2_src, &ctx->lw2_disp, &ctx->jscr, &ctx->jperm, &ctx->jq, &ctx->jr, &ctx->jj,
                   &ctx->qy, &ctx->qt, &ctx->qw};
   for (DBuf* b : bufs) b->release();
   for (auto& b : ctx->tail) b.release();
@@ -1590,7 +1656,7 @@ __global__ void debug_diff_kernel(const unsigned long long* a, const unsigned lo
 sssvd_status sssvd_debug_zgemm(sssvd_gpu_ctx* ctx, int variant, int64_t m, int64_t n, int64_t k, int64_t batch,
                                int reps, double* ms_out, int64_t* mismatches_out) {
   return guarded(ctx, [&]() {
-    if (m < 1 || n < 1 || k < 1 || batch < 1 || reps < 1 || variant < 0 || variant > 3)
+    if (m < 1 || n < 1 || k < 1 || batch < 1 || reps < 1 || variant < 0 || variant > 8)
       throw Status(SSSVD_E_INVALID_ARGUMENT, "debug_zgemm: bad arguments");
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
@@ -1610,8 +1676,21 @@ sssvd_status sssvd_debug_zgemm(sssvd_gpu_ctx* ctx, int variant, int64_t m, int64
       CK(cudaMemcpyAsync(C1, C0, nc * sizeof(double2), cudaMemcpyDeviceToDevice, s));
       zgemm_set_variant(0);
       CK(zgemm_sub((int)m, (int)n, (int)k, A, (int)k, m * k, B, (int)n, k * n, C0, (int)n, m * n, (int)batch, s));
-      zgemm_set_variant(variant);
-      CK(zgemm_sub((int)m, (int)n, (int)k, A, (int)k, m * k, B, (int)n, k * n, C1, (int)n, m * n, (int)batch, s));
+      // variant 8: cuBLAS zgemmStridedBatched on the same row-major data (C^T -= B^T A^T in its
+      // column-major view) -- a library comparator for the measurement only, never the product path
+      const cuDoubleComplex mone = make_cuDoubleComplex(-1.0, 0.0), one = make_cuDoubleComplex(1.0, 0.0);
+      auto run = [&](double2* Cx) {
+        if (variant == 8) {
+          CKB(cublasSetStream(ctx->blas, s));
+          CKB(cublasZgemmStridedBatched(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)n, (int)m, (int)k, &mone,
+                                        (const cuDoubleComplex*)B, (int)n, k * n, (const cuDoubleComplex*)A, (int)k,
+                                        m * k, &one, (cuDoubleComplex*)Cx, (int)n, m * n, (int)batch));
+        } else {
+          CK(zgemm_sub((int)m, (int)n, (int)k, A, (int)k, m * k, B, (int)n, k * n, Cx, (int)n, m * n, (int)batch, s));
+        }
+      };
+      zgemm_set_variant(variant == 8 ? 0 : variant);
+      run(C1);
       CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
       debug_diff_kernel<<<1184, 256, 0, s>>>((const unsigned long long*)C0, (const unsigned long long*)C1,
                                              2 * (long long)nc, cnt);
@@ -1621,8 +1700,7 @@ sssvd_status sssvd_debug_zgemm(sssvd_gpu_ctx* ctx, int variant, int64_t m, int64
       CK(cudaEventCreate(&e0));
       CK(cudaEventCreate(&e1));
       CK(cudaEventRecord(e0, s));
-      for (int r = 0; r < reps; ++r)
-        CK(zgemm_sub((int)m, (int)n, (int)k, A, (int)k, m * k, B, (int)n, k * n, C1, (int)n, m * n, (int)batch, s));
+      for (int r = 0; r < reps; ++r) run(C1);
       CK(cudaEventRecord(e1, s));
       CK(cudaEventSynchronize(e1));
       float ms = 0;

@@ -190,3 +190,23 @@ def test_graph_replay_is_bitwise_eager(dev):
     ref = orc.MomentAccumulator(orc.form_gram(orc.ProblemMatrix(a)), ro).accumulate(s0, 4).blocks
     for k in range(5):
         assert np.linalg.norm(runs[-1][k] - ref[k]) / np.linalg.norm(ref[k]) <= 1e-10
+
+
+def test_lookahead_schedule_is_bitwise_plain_schedule(dev, monkeypatch):
+    """The depth-1 look-ahead LU schedule (next block's columns on the panel stream, far columns on
+    the GEMM stream) applies every update to every column in the same order with the same
+    kernels, so its moments must equal the plain grouped schedule's bit for bit (n = 700: five full
+    128-wide blocks and a ragged one)."""
+    a = constructed(900, 700, np.linspace(0.05, 1.5, 700), 31, 32)
+    rg, ro = rules(0.6, 0.9, 32, 0.1)
+    s0 = orc.random_start(700, 8, 42)
+    monkeypatch.setenv("SSSVD_LOOKAHEAD", "0")
+    plain = gpu_blocks(dev, a, rg, s0, 3)
+    monkeypatch.setenv("SSSVD_LOOKAHEAD", "1")
+    look = [gpu_blocks(dev, a, rg, s0, 3) for _ in range(3)]   # eager, captured, replayed
+    for r in look:
+        for k in range(4):
+            assert np.array_equal(plain[k], r[k])
+    ref = orc.MomentAccumulator(orc.form_gram(orc.ProblemMatrix(a)), ro).accumulate(s0, 3).blocks
+    for k in range(4):
+        assert np.linalg.norm(look[-1][k] - ref[k]) / np.linalg.norm(ref[k]) <= 1e-10

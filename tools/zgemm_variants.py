@@ -1,6 +1,7 @@
 """Time the trailing-update GEMM variants (warp tiles 32x32 / 32x16 / 16x32 / 16x16) on the
 shapes the LU issues, and check each is bitwise the 32x32 kernel. Usage:
-    python tools/zgemm_variants.py [--reps 20]"""
+    python tools/zgemm_variants.py [--reps 20] [--shape i] [--variant v]
+Variant 8 is cuBLAS zgemmStridedBatched on the same data (a comparator, not the product path)."""
 import ctypes, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2109_13655_b200 import sssvd
@@ -19,8 +20,14 @@ def main():
     reps = int(sys.argv[sys.argv.index("--reps") + 1]) if "--reps" in sys.argv else 20
     dev = sssvd.Device(0)
     L = sssvd.lib()
-    for label, m, n, k, b in SHAPES:
-        for v in range(4):
+    only_shape = int(sys.argv[sys.argv.index("--shape") + 1]) if "--shape" in sys.argv else None
+    only_var = int(sys.argv[sys.argv.index("--variant") + 1]) if "--variant" in sys.argv else None
+    for si, (label, m, n, k, b) in enumerate(SHAPES):
+        if only_shape is not None and si != only_shape:
+            continue
+        for v in range(9):
+            if only_var is not None and v != only_var:
+                continue
             ms = ctypes.c_double()
             mism = ctypes.c_int64()
             dev.check(L.sssvd_debug_zgemm(dev.h, v, m, n, k, b, reps, ctypes.byref(ms), ctypes.byref(mism)))
