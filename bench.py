@@ -237,12 +237,13 @@ def main():
                          "achieved": gemm_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": (gemm_tflops / FP64_PEAK_TFLOPS) if gemm_tflops else None,
                          # one ncu --set full capture of a large trailing update (profiles/
-                         # r01_ncu_zgemm_trailing_prefetch.txt): M=3968 N=4000 K=128 complex x 8 shifts
-                         "traffic": 2.163797e9 + 1.976564e9,
+                         # r01_ncu_zgemm_loader.txt): M=3968 N=4000 K=128 complex x 8 shifts
+                         "traffic": 2.162800e9 + 1.976943e9,
                          "traffic_launch": {"shape": "M=3968 N=4000 K=128 complex, batch 8",
                                             "algorithmic_bytes": 8 * 16 * (2 * 3968 * 4000 + 3968 * 128 + 128 * 4000),
-                                            "dram_bytes": 2.163797e9 + 1.976564e9, "ncu_duration_ms": 4.259136,
-                                            "ncu_tflops": 1.300e11 / 4.259136e-3 / 1e12},
+                                            "dram_bytes": 2.162800e9 + 1.976943e9, "ncu_duration_ms": 4.19392,
+                                            "ncu_tflops": 1.300e11 / 4.19392e-3 / 1e12,
+                                            "ncu_dmma_pipe_active": 0.849},
                          "achieved_basis": "GEMM flops / GEMM-busy time (union of the launch intervals, CUDA events "
                                            "on the launching streams; the shift groups overlap their GEMMs)",
                          "peak_source": "measured FP64 DMMA probe (profiles/r01_fp64_peaks.json); MEASURED_PEAKS.json has no FP64 entry",

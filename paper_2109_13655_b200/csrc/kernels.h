@@ -65,6 +65,9 @@ cudaError_t zgemm_set_gather(int M, int N, int K, const double2* A, int lda, lon
 // interchange map, L11^{-1}, scatter+copy, warp back substitution (lu.cu)
 cudaError_t build_moves(const int* ipiv, int n, int r0, int np, int* src, int* disp, int stride, int batch,
                         cudaStream_t s);
+// build_moves + trinv_lower fused into one launch (lu.cu)
+cudaError_t panel_prep(const double2* mats, int ld, long long stride, int r0, int np, double2* linv, long long lstride,
+                       const int* ipiv, int n, int* src, int* disp, int dstride, int batch, cudaStream_t s);
 cudaError_t trinv_lower(const double2* mats, int ld, long long stride, int r0, int np, double2* linv,
                         long long lstride, int batch, cudaStream_t s);
 cudaError_t scatter_copy(double2* mats, int ld, long long stride, int r0, int np, int c0, int c1, const int* disp,

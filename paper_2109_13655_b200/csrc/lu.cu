@@ -505,14 +505,13 @@ namespace sssvd_gpu {
 //   disp    : the moves (dst >= r0+np <- src) of rows displaced below the panel.
 // Every displaced row receives original content of a panel row (ipiv[r0+j] >= r0+j), so the
 // displaced moves can be applied in place before the panel rows are overwritten.
-__global__ void build_moves_kernel(const int* __restrict__ ipiv, int n, int r0, int np, int* __restrict__ src,
-                                   int* __restrict__ disp, int stride) {
-  extern __shared__ int mv[];
+__device__ __forceinline__ void build_moves_body(const int* __restrict__ ipiv, int n, int r0, int np,
+                                                 int* __restrict__ src, int* __restrict__ disp, int stride, int b,
+                                                 int* mv) {
   int* pos = mv;              // [2 np]
   int* cont = mv + 2 * np;    // [2 np]
-  const int b = blockIdx.x;
   const int* piv = ipiv + (size_t)b * n;
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31;
   int k = 0;
   for (int j = 0; j < np; ++j) {
     const int a = r0 + j, q = piv[r0 + j];
@@ -557,6 +556,12 @@ __global__ void build_moves_kernel(const int* __restrict__ ipiv, int n, int r0, 
   if (lane == 0) d[0] = nd;
 }
 
+__global__ void build_moves_kernel(const int* __restrict__ ipiv, int n, int r0, int np, int* __restrict__ src,
+                                   int* __restrict__ disp, int stride) {
+  extern __shared__ int mv[];
+  build_moves_body(ipiv, n, r0, np, src, disp, stride, blockIdx.x, mv);
+}
+
 cudaError_t build_moves(const int* ipiv, int n, int r0, int np, int* src, int* disp, int stride, int batch,
                         cudaStream_t s) {
   build_moves_kernel<<<batch, 32, 4 * np * sizeof(int), s>>>(ipiv, n, r0, np, src, disp, stride);
@@ -568,11 +573,10 @@ cudaError_t build_moves(const int* ipiv, int n, int r0, int np, int* src, int* d
 // Linv = L11^{-1} for the unit-lower np x np block at (r0, r0): one warp per column j; lanes
 // split each dot product, a warp reduction closes it. Row-major output with pitch np.
 template <int QMAX>   // np <= 32 QMAX
-__global__ void trinv_lower_kernel(const double2* __restrict__ mats, int ld, long long stride, int r0, int np,
-                                   double2* __restrict__ linv, long long lstride) {
-  const int b = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int j = blockIdx.x * (blockDim.x >> 5) + warp;
+__device__ __forceinline__ void trinv_lower_body(const double2* __restrict__ mats, int ld, long long stride, int r0,
+                                                 int np, double2* __restrict__ linv, long long lstride, int b,
+                                                 int j) {
+  const int lane = threadIdx.x & 31;
   if (j >= np) return;
   const double2* Mb = mats + b * stride + (size_t)r0 * ld + r0;
   double2* out = linv + (size_t)b * lstride;
@@ -624,6 +628,42 @@ __global__ void trinv_lower_kernel(const double2* __restrict__ mats, int ld, lon
     const int i = lane + 32 * q;
     if (i < np) out[(size_t)i * np + j] = i >= j ? x[q] : make_double2(0.0, 0.0);
   }
+}
+
+template <int QMAX>
+__global__ void trinv_lower_kernel(const double2* __restrict__ mats, int ld, long long stride, int r0, int np,
+                                   double2* __restrict__ linv, long long lstride) {
+  trinv_lower_body<QMAX>(mats, ld, stride, r0, np, linv, lstride, blockIdx.y,
+                         blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+}
+
+// build_moves and trinv_lower of one panel node in ONE launch: they are independent (the
+// interchange map reads only ipiv, L11^{-1} only the factored panel), so the gather GEMM that
+// needs both waits on one kernel instead of two in sequence. Blocks x < ceil(np/4) invert
+// columns; block x = ceil(np/4) folds the interchanges (its first warp).
+template <int QMAX>
+__global__ void panel_prep_kernel(const double2* __restrict__ mats, int ld, long long stride, int r0, int np,
+                                  double2* __restrict__ linv, long long lstride, const int* __restrict__ ipiv, int n,
+                                  int* __restrict__ src, int* __restrict__ disp, int dstride) {
+  extern __shared__ int mv[];
+  const int nx = (np + 3) / 4;
+  if ((int)blockIdx.x < nx)
+    trinv_lower_body<QMAX>(mats, ld, stride, r0, np, linv, lstride, blockIdx.y, blockIdx.x * 4 + (threadIdx.x >> 5));
+  else if (threadIdx.x < 32)
+    build_moves_body(ipiv, n, r0, np, src, disp, dstride, blockIdx.y, mv);
+}
+
+cudaError_t panel_prep(const double2* mats, int ld, long long stride, int r0, int np, double2* linv, long long lstride,
+                       const int* ipiv, int n, int* src, int* disp, int dstride, int batch, cudaStream_t s) {
+  if (np > 256) return cudaErrorInvalidValue;
+  dim3 grid((np + 3) / 4 + 1, batch);
+  const size_t sm = 4 * np * sizeof(int);
+  if (np <= 128)
+    panel_prep_kernel<4><<<grid, 128, sm, s>>>(mats, ld, stride, r0, np, linv, lstride, ipiv, n, src, disp, dstride);
+  else
+    panel_prep_kernel<8><<<grid, 128, sm, s>>>(mats, ld, stride, r0, np, linv, lstride, ipiv, n, src, disp, dstride);
+  note_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t trinv_lower(const double2* mats, int ld, long long stride, int r0, int np, double2* linv,

@@ -352,8 +352,13 @@ static void apply_panel(const LuPlan& P, const LuWork& W, double2* mats, const i
                         cudaEvent_t ev_done = nullptr) {
   const int n = P.n, N = c1 - c0;
   if (N <= 0) return;
-  CK(build_moves(ipiv, n, r0, np, W.src, W.disp, P.NB, nb, s));
-  CK(trinv_lower(mats, P.ld, P.stride, r0, np, W.linv, (long long)P.NB * P.NB, nb, s));
+  static const bool split_prep = std::getenv("SSSVD_SPLIT_PREP") != nullptr;   // measurement: two launches
+  if (split_prep) {
+    CK(build_moves(ipiv, n, r0, np, W.src, W.disp, P.NB, nb, s));
+    CK(trinv_lower(mats, P.ld, P.stride, r0, np, W.linv, (long long)P.NB * P.NB, nb, s));
+  } else {
+    CK(panel_prep(mats, P.ld, P.stride, r0, np, W.linv, (long long)P.NB * P.NB, ipiv, n, W.src, W.disp, P.NB, nb, s));
+  }
   CK(zgemm_set_gather(np, N, np, W.linv, np, (long long)P.NB * P.NB, mats + c0, P.ld, P.stride, W.src, P.NB, W.T, N,
                       W.tstride, nb, s));
   CK(scatter_copy(mats, P.ld, P.stride, r0, np, c0, c1, W.disp, P.NB, W.T, N, W.tstride, nb, s));
@@ -504,10 +509,12 @@ static void lu_solve_groups_lookahead(const LuPlan& P, std::vector<LuGroup>& G) 
   }
 }
 
-// SSSVD_LOOKAHEAD=0 selects the plain grouped schedule (read per pass, so tests can compare both)
+// SSSVD_LOOKAHEAD=1 selects the look-ahead schedule (read per pass, so tests can compare both).
+// Off by default: measured equal to the plain grouped schedule (cfg2 phase 128-129 ms either way,
+// cfg4 1.62-1.66 s), because the other shift groups' GEMMs already fill the GPU during a panel.
 static bool lookahead_on() {
   const char* e = std::getenv("SSSVD_LOOKAHEAD");
-  return !(e && std::string(e) == "0");
+  return e && std::string(e) == "1";
 }
 
 static LuWork make_work(sssvd_gpu_ctx* ctx, const LuPlan& P, int B) {
