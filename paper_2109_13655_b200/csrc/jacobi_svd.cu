@@ -1027,6 +1027,11 @@ bool jacobi_grid_block_plan(int k, int sms, int* b_out, int* nbe_out, int* rpl_o
   // widest block (fewest outer rounds, i.e. grid barriers, per sweep) with one warp per resident
   // column and the pair in shared memory; at least enough blocks to cover the SMs once
   int b = GB_THREADS / 32;
+  {
+    // measurement override: a narrower block (more pairs per round, more rounds per sweep)
+    static const char* be = std::getenv("SSSVD_JACOBI_B");
+    if (be && std::atoi(be) >= 2 && std::atoi(be) < b) b = std::atoi(be);
+  }
   const size_t limit = 232448 - 1024;   // 227 KB opt-in per CTA, less the static shared memory
   while (b > 2 && ((size_t)2 * b * k + 256) * sizeof(double) > limit) --b;
   if (b < (k + 2 * sms - 1) / (2 * sms)) return false;
