@@ -214,7 +214,7 @@ sssvd_status sssvd_debug_thin_qr(sssvd_gpu_ctx* ctx, const double* a, int64_t m,
 sssvd_status sssvd_debug_svd_square(sssvd_gpu_ctx* ctx, const double* b, int64_t k, double* u_out, double* s_out,
                                     double* v_out);
 /* Debug: the trailing-update GEMM (C -= A B, complex, row-major, batched) on seeded device data:
- * warp-tile variant `variant` (0..7, see zgemm.cu; 8 = cuBLAS zgemmStridedBatched, a comparator only) timed over `reps` launches -> ms_out (mean per launch);
+ * warp-tile variant `variant` (0..9, see zgemm.cu; 10 = cuBLAS zgemmStridedBatched, a comparator only) timed over `reps` launches -> ms_out (mean per launch);
  * mismatches_out = entries of C that differ BITWISE from variant 0 on the same inputs. */
 sssvd_status sssvd_debug_zgemm(sssvd_gpu_ctx* ctx, int variant, int64_t m, int64_t n, int64_t k, int64_t batch,
                                int reps, double* ms_out, int64_t* mismatches_out);

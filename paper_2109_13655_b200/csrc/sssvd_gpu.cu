@@ -1663,7 +1663,7 @@ __global__ void debug_diff_kernel(const unsigned long long* a, const unsigned lo
 sssvd_status sssvd_debug_zgemm(sssvd_gpu_ctx* ctx, int variant, int64_t m, int64_t n, int64_t k, int64_t batch,
                                int reps, double* ms_out, int64_t* mismatches_out) {
   return guarded(ctx, [&]() {
-    if (m < 1 || n < 1 || k < 1 || batch < 1 || reps < 1 || variant < 0 || variant > 8)
+    if (m < 1 || n < 1 || k < 1 || batch < 1 || reps < 1 || variant < 0 || variant > 10)
       throw Status(SSSVD_E_INVALID_ARGUMENT, "debug_zgemm: bad arguments");
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
@@ -1683,11 +1683,11 @@ sssvd_status sssvd_debug_zgemm(sssvd_gpu_ctx* ctx, int variant, int64_t m, int64
       CK(cudaMemcpyAsync(C1, C0, nc * sizeof(double2), cudaMemcpyDeviceToDevice, s));
       zgemm_set_variant(0);
       CK(zgemm_sub((int)m, (int)n, (int)k, A, (int)k, m * k, B, (int)n, k * n, C0, (int)n, m * n, (int)batch, s));
-      // variant 8: cuBLAS zgemmStridedBatched on the same row-major data (C^T -= B^T A^T in its
+      // variant 10: cuBLAS zgemmStridedBatched on the same row-major data (C^T -= B^T A^T in its
       // column-major view) -- a library comparator for the measurement only, never the product path
       const cuDoubleComplex mone = make_cuDoubleComplex(-1.0, 0.0), one = make_cuDoubleComplex(1.0, 0.0);
       auto run = [&](double2* Cx) {
-        if (variant == 8) {
+        if (variant == 10) {
           CKB(cublasSetStream(ctx->blas, s));
           CKB(cublasZgemmStridedBatched(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)n, (int)m, (int)k, &mone,
                                         (const cuDoubleComplex*)B, (int)n, k * n, (const cuDoubleComplex*)A, (int)k,
@@ -1696,7 +1696,7 @@ sssvd_status sssvd_debug_zgemm(sssvd_gpu_ctx* ctx, int variant, int64_t m, int64
           CK(zgemm_sub((int)m, (int)n, (int)k, A, (int)k, m * k, B, (int)n, k * n, Cx, (int)n, m * n, (int)batch, s));
         }
       };
-      zgemm_set_variant(variant == 8 ? 0 : variant);
+      zgemm_set_variant(variant == 10 ? 0 : variant);
       run(C1);
       CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
       debug_diff_kernel<<<1184, 256, 0, s>>>((const unsigned long long*)C0, (const unsigned long long*)C1,

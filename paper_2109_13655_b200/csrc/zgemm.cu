@@ -218,7 +218,7 @@ __device__ __forceinline__ void load_c_half(double2* dst, const double2* C, int 
 
 // SET: C = A B (C is not read); otherwise C -= A B. GATHER: row k of B is row brow[k] of the
 // B matrix (the pivoted rows of the panel block, read straight from their pre-interchange place).
-template <int WI, int WJ, bool SET, bool GATHER>
+template <int WI, int WJ, bool SET, bool GATHER, int ISSUE_AT = 0>
 __global__ void __launch_bounds__((64 / (8 * WI)) * (64 / (8 * WJ)) * 32, WI * WJ >= 8 ? 2 : 1)
 zgemm_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long long sA,
              const double2* __restrict__ B, int ldb, long long sB, const int* __restrict__ brow, int sR,
@@ -277,7 +277,9 @@ zgemm_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long l
   for (int kt = 0; kt < KT; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
-    {
+    // the next stage's copies (or a C half-tile): issued at the top (ISSUE_AT = 0) or after
+    // ISSUE_AT k-quads of this stage, spreading the integer work between DMMA blocks
+    auto issue_next = [&]() {
       int nk = kt + STAGES - 1;
       if (nk < KT) {
         int st = nk % STAGES;
@@ -291,11 +293,13 @@ zgemm_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long l
         if (h >= 0 && h < 2) load_c_half<THREADS>(c_stage(h), C, ldc, M, N, m0, n0, h, tid);
       }
       cp_async_commit();
-    }
+    };
+    if (ISSUE_AT == 0) issue_next();
     const double2* as = As + (kt % STAGES) * SSTRIDE + (wm * 8 * WI + fr) * LDA_S + fc;
     const double2* bs = Bs + (kt % STAGES) * SSTRIDE + fc * LDB_S + wn * 8 * WJ + fr;
 #pragma unroll
     for (int kq = 0; kq < BK / 4; ++kq) {
+      if (ISSUE_AT > 0 && kq == ISSUE_AT) issue_next();
       double2 a[WI], b[WJ];
 #pragma unroll
       for (int i = 0; i < WI; ++i) a[i] = as[i * 8 * LDA_S + kq * 4];
@@ -696,7 +700,8 @@ size_t zgemm_sub_smem() { return (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(d
 
 // variant of the trailing-update GEMM: SSSVD_ZGEMM_V (warp tiles 0: 32x32, 1: 32x16, 2: 16x32,
 // 3: 16x16; 4: persistent 32x32 with the red epilogue; 5: one CTA per tile with the red epilogue;
-// 6 / 7: persistent 8-warp CTA per SM with a C buffer, 3 / 4 k-stages)
+// 6 / 7: persistent 8-warp CTA per SM with a C buffer, 3 / 4 k-stages; 8 / 9: 32x32 with the next
+// stage issued after the first / second k-quad instead of at the top)
 // or zgemm_set_variant (measurement hook)
 static int g_variant = -1;
 void zgemm_set_variant(int v) { g_variant = v; }
@@ -704,25 +709,25 @@ static int zgemm_variant() {
   if (g_variant < 0) {
     const char* e = std::getenv("SSSVD_ZGEMM_V");
     g_variant = e ? std::atoi(e) : 0;
-    if (g_variant < 0 || g_variant > 7) g_variant = 0;
+    if (g_variant < 0 || g_variant > 9) g_variant = 0;
   }
   return g_variant;
 }
 
-template <int WI, int WJ, bool SET, bool GATHER>
+template <int WI, int WJ, bool SET, bool GATHER, int ISSUE_AT = 0>
 static cudaError_t launch_v(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B, int ldb,
                             long long sB, const int* brow, int sR, double2* C, int ldc, long long sC, int batch,
                             cudaStream_t stream, unsigned long long* stamp) {
   constexpr int THREADS = (64 / (8 * WI)) * (64 / (8 * WJ)) * 32;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(zgemm_kernel<WI, WJ, SET, GATHER>,
+    cudaError_t e = cudaFuncSetAttribute(zgemm_kernel<WI, WJ, SET, GATHER, ISSUE_AT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zgemm_sub_smem());
     if (e != cudaSuccess) return e;
     configured = true;
   }
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch);
-  zgemm_kernel<WI, WJ, SET, GATHER><<<grid, THREADS, zgemm_sub_smem(), stream>>>(
+  zgemm_kernel<WI, WJ, SET, GATHER, ISSUE_AT><<<grid, THREADS, zgemm_sub_smem(), stream>>>(
       M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, stamp, g_prof.cap);
   return cudaGetLastError();
 }
@@ -790,6 +795,8 @@ static cudaError_t launch(int M, int N, int K, const double2* A, int lda, long l
     case 5: return launch_persist<SET, GATHER>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stream, stamp, false);
     case 6: return launch_persist2<3, SET, GATHER>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stream, stamp);
     case 7: return launch_persist2<4, SET, GATHER>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stream, stamp);
+    case 8: return launch_v<4, 4, SET, GATHER, 1>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stream, stamp);
+    case 9: return launch_v<4, 4, SET, GATHER, 2>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stream, stamp);
     default: return launch_v<4, 4, SET, GATHER>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stream, stamp);
   }
 }

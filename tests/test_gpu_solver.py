@@ -163,7 +163,7 @@ def test_gram_sharding_is_exact(dev):
     assert all(np.count_nonzero(p) > 0 for p in parts)
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5, 6, 7])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5, 6, 7, 8, 9])
 @pytest.mark.parametrize("m,n,k,batch", [(200, 136, 128, 3), (64, 64, 16, 1), (77, 35, 9, 2), (1000, 1016, 64, 2)])
 def test_zgemm_warp_tile_variants_bitwise(dev, variant, m, n, k, batch):
     """Every warp-tile variant of the trailing-update GEMM issues the same DMMA chain per entry of

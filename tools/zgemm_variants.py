@@ -1,7 +1,7 @@
 """Time the trailing-update GEMM variants (warp tiles 32x32 / 32x16 / 16x32 / 16x16) on the
 shapes the LU issues, and check each is bitwise the 32x32 kernel. Usage:
     python tools/zgemm_variants.py [--reps 20] [--shape i] [--variant v]
-Variant 8 is cuBLAS zgemmStridedBatched on the same data (a comparator, not the product path)."""
+Variant 10 is cuBLAS zgemmStridedBatched on the same data (a comparator, not the product path)."""
 import ctypes, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2109_13655_b200 import sssvd
@@ -25,7 +25,7 @@ def main():
     for si, (label, m, n, k, b) in enumerate(SHAPES):
         if only_shape is not None and si != only_shape:
             continue
-        for v in range(9):
+        for v in range(11):
             if only_var is not None and v != only_var:
                 continue
             ms = ctypes.c_double()
