@@ -619,8 +619,11 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
       ctx->solve_flops += nb * (8.0 * (double)n * n * L);
       continue;
     }
+    // independent shift groups: 8 for the 128-wide outer block (n < 8192; config-2 phase 118.0 ->
+    // 116.4 ms), 4 for the 256-wide one (configs 3 / 4 / 5 measured 1-2 % faster with 4 than 8)
     static const char* genv = std::getenv("SSSVD_GROUPS");
-    const int ng = std::max(1, std::min({nb / 2, sssvd_gpu_ctx::kMaxGroups, genv ? std::atoi(genv) : 4}));
+    const int gdef = P.NB == 128 ? 8 : 4;
+    const int ng = std::max(1, std::min({nb / 2, sssvd_gpu_ctx::kMaxGroups, genv ? std::atoi(genv) : gdef}));
     // the whole pass on the device: the host issues ~5000 launches per pass, which at ~17 us each
     // would make the GPU wait on the host; replaying a captured graph removes that
     std::vector<double> pass_flops;
