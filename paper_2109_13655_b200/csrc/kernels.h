@@ -65,6 +65,8 @@ cudaError_t zgemm_set_gather(int M, int N, int K, const double2* A, int lda, lon
 // interchange map, L11^{-1}, scatter+copy, warp back substitution (lu.cu)
 cudaError_t build_moves(const int* ipiv, int n, int r0, int np, int* src, int* disp, int stride, int batch,
                         cudaStream_t s);
+// back-substitution kernel choice: 0 shared-memory staged (default), 1 warp-streamed (lu.cu)
+int trsm_variant();
 // build_moves + trinv_lower fused into one launch (lu.cu)
 cudaError_t panel_prep(const double2* mats, int ld, long long stride, int r0, int np, double2* linv, long long lstride,
                        const int* ipiv, int n, int* src, int* disp, int dstride, int batch, cudaStream_t s);

@@ -772,10 +772,111 @@ __global__ void trsm_upper_warp_kernel(double2* mats, int ld, long long stride, 
   }
 }
 
+// Same substitution (bitwise: identical per-row dot products and warp reductions), but the CTA's
+// warps -- WPB right-hand-side columns of one shift -- share the rows of U11: chunks of R rows are
+// staged in shared memory by cp.async two chunks ahead, instead of every warp fetching each row
+// from L2 one row ahead. The per-row critical path drops from an L2 round trip to the shuffle
+// reduction.
+template <int QMAX, int WPB>
+__global__ void __launch_bounds__(32 * WPB, 2)
+trsm_upper_smem_kernel(double2* mats, int ld, long long stride, int r0, int np, int c0, int c1) {
+  constexpr int R = 32 / QMAX;   // rows per chunk (one chunk never straddles a 32-row slot)
+  constexpr int NP = 32 * QMAX;
+  constexpr int T = NP / R;
+  __shared__ __align__(16) double2 buf[2][R][NP];
+  const int b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = c0 + blockIdx.x * WPB + warp;
+  const bool active = c < c1;
+  double2* Mb = mats + b * stride;
+  const double2* U = Mb + (size_t)r0 * ld + r0;
+  // chunk t holds rows [NP - (t+1) R, NP - t R), highest first; rows >= np are not loaded
+  auto load_chunk = [&](int t) {
+    const int top = NP - t * R;
+    for (int idx = threadIdx.x; idx < R * np; idx += 32 * WPB) {
+      const int sl = idx / np, l = idx - sl * np;
+      const int i = top - 1 - sl;
+      if (i < np) cp_async16(&buf[t & 1][sl][l], U + (size_t)i * ld + l);
+    }
+    cp_async_commit();
+  };
+  load_chunk(0);
+  load_chunk(1);
+  double2 x[QMAX], invd[QMAX];
+#pragma unroll
+  for (int q = 0; q < QMAX; ++q) {
+    const int i = lane + 32 * q;
+    x[q] = (active && i < np) ? Mb[(size_t)(r0 + i) * ld + c] : make_double2(0.0, 0.0);
+    const double2 u = i < np ? U[(size_t)i * ld + i] : make_double2(1.0, 0.0);
+    invd[q] = cabs2(u) != 0.0 ? crecip(u) : make_double2(1.0, 0.0);
+  }
+  int t = 0;
+#pragma unroll
+  for (int qi = QMAX - 1; qi >= 0; --qi) {
+    for (int tc = 0; tc < 32 / R; ++tc, ++t) {
+      cp_async_wait<1>();
+      __syncthreads();
+      const int slot = t & 1;
+      if (active) {
+        for (int sl = 0; sl < R; ++sl) {
+          const int ii = 31 - tc * R - sl;
+          const int i = 32 * qi + ii;
+          if (i >= np) continue;
+          double sr = 0.0, si = 0.0;
+#pragma unroll
+          for (int q = qi; q < QMAX; ++q) {
+            const int l = lane + 32 * q;
+            if (l > i && l < np) {
+              const double2 u = buf[slot][sl][l];
+              sr += u.x * x[q].x - u.y * x[q].y;
+              si += u.x * x[q].y + u.y * x[q].x;
+            }
+          }
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            sr += __shfl_xor_sync(0xffffffffu, sr, off);
+            si += __shfl_xor_sync(0xffffffffu, si, off);
+          }
+          if (lane == ii) x[qi] = cmul(make_double2(x[qi].x - sr, x[qi].y - si), invd[qi]);
+        }
+      }
+      __syncthreads();
+      if (t + 2 < T)
+        load_chunk(t + 2);
+      else
+        cp_async_commit();   // keep one group per chunk so the wait count stays exact
+    }
+  }
+  if (active) {
+#pragma unroll
+    for (int q = 0; q < QMAX; ++q) {
+      const int i = lane + 32 * q;
+      if (i < np) Mb[(size_t)(r0 + i) * ld + c] = x[q];
+    }
+  }
+}
+
+// SSSVD_TRSM=warp (1): every warp streams U11 itself (the previous kernel); read per call so tests
+// can compare both (the shifted-solve graph key includes it)
+int trsm_variant() {
+  const char* tv = std::getenv("SSSVD_TRSM");
+  return (tv && std::string(tv) == "warp") ? 1 : 0;
+}
+
 cudaError_t trsm_upper_warp(double2* mats, int ld, long long stride, int r0, int np, int c0, int c1, int batch,
                             cudaStream_t s) {
   if (c1 <= c0 || np <= 0) return cudaSuccess;
   if (np > 256) return cudaErrorInvalidValue;
+  if (trsm_variant() == 0) {
+    constexpr int WPB = 8;
+    dim3 grid((c1 - c0 + WPB - 1) / WPB, batch);
+    if (np <= 128)
+      trsm_upper_smem_kernel<4, WPB><<<grid, 32 * WPB, 0, s>>>(mats, ld, stride, r0, np, c0, c1);
+    else
+      trsm_upper_smem_kernel<8, WPB><<<grid, 32 * WPB, 0, s>>>(mats, ld, stride, r0, np, c0, c1);
+    note_launch();
+    return cudaGetLastError();
+  }
   const int wpb = 4;
   dim3 grid((c1 - c0 + wpb - 1) / wpb, batch);
   if (np <= 128)

@@ -189,6 +189,11 @@ struct sssvd_gpu_ctx {
   cudaStream_t cstream = nullptr;   // result device->host copies, overlapped with the tail
   cudaEvent_t ev_copy = nullptr;
   double t_gram = 0, t_solves = 0, t_allreduce = 0, solve_flops = 0;
+  // the last starting block (random_start is a pure function of n, L, seed: ~1 ms of mt19937_64
+  // draws at n = 4096, L = 32, repeated by every run_solve of the same shape)
+  int64_t v0_n = -1, v0_L = -1;
+  uint64_t v0_seed = 0;
+  std::vector<double> v0;
 };
 
 // Page-locked host arrays for the large result fields (moment blocks, triplet vectors): their
@@ -579,6 +584,7 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
                         const std::vector<std::complex<double>>& coef, int64_t h, int64_t jb, int64_t je,
                         const double* V_dev, int L, int M, double* S_dev) {
   cudaStream_t s = ctx->stream;
+  const double t_entry = now_s();
   const int n = (int)ctx->n;
   LuPlan P = make_plan(n, L);
   CK(cudaMemsetAsync(S_dev, 0, sizeof(double) * (size_t)(M + 1) * n * L, s));
@@ -675,12 +681,31 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
           (uintptr_t)P.cluster, (uintptr_t)(P.leaf_variant + 1), (uintptr_t)P.ld, (uintptr_t)ctx->G.p,
           (uintptr_t)V_dev, (uintptr_t)mats, (uintptr_t)ipiv, (uintptr_t)work.linv, (uintptr_t)work.T,
           (uintptr_t)work.src, (uintptr_t)work.disp, (uintptr_t)dshift, (uintptr_t)dcoef, (uintptr_t)S_dev,
-          (uintptr_t)ctx->gmax.p, (uintptr_t)dstatus, (uintptr_t)dmin, (uintptr_t)lookahead,
+          (uintptr_t)ctx->gmax.p, (uintptr_t)dstatus, (uintptr_t)dmin, (uintptr_t)lookahead, (uintptr_t)trsm_variant(),
           (uintptr_t)work2.linv, (uintptr_t)work2.T, (uintptr_t)work2.src, (uintptr_t)work2.disp};
       for (auto& g : ctx->lu_graphs)
         if (g.key == key) replayed = &g;
       if (replayed) {
+        // SSSVD_DEBUG_PHASE=1: split the pass into host preparation (since moment_pass entry) and
+        // the graph's own device time (measurement only)
+        static const bool dbg_phase = std::getenv("SSSVD_DEBUG_PHASE") != nullptr;
+        cudaEvent_t g0 = nullptr, g1 = nullptr;
+        if (dbg_phase) {
+          cudaEventCreate(&g0);
+          cudaEventCreate(&g1);
+          cudaEventRecord(g0, s);
+        }
         CK(cudaGraphLaunch(replayed->exec, s));
+        if (dbg_phase) {
+          cudaEventRecord(g1, s);
+          cudaEventSynchronize(g1);
+          float gm = 0;
+          cudaEventElapsedTime(&gm, g0, g1);
+          std::fprintf(stderr, "[sssvd] phase host prep %.3f ms, graph device %.3f ms\n", (now_s() - t_entry) * 1e3 - gm,
+                       gm);
+          cudaEventDestroy(g0);
+          cudaEventDestroy(g1);
+        }
         note_launch(replayed->launches);
       } else if (ctx->lu_warm_key == key) {
         // second sighting: capture (the eager first run has set every kernel attribute)
@@ -1033,7 +1058,13 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
   ctx->fact_valid = false;
   ensure_gram(ctx, cfg.gram_cap > 0 ? cfg.gram_cap : 8192);
   tp12.mark("form_gram");
-  std::vector<double> v0 = random_start(n, L, cfg.params.seed);
+  if (ctx->v0_n != n || ctx->v0_L != L || ctx->v0_seed != cfg.params.seed) {
+    ctx->v0 = random_start(n, L, cfg.params.seed);
+    ctx->v0_n = n;
+    ctx->v0_L = L;
+    ctx->v0_seed = cfg.params.seed;
+  }
+  const std::vector<double>& v0 = ctx->v0;
   double start_norm2 = 0;
   for (double x : v0) start_norm2 += x * x;
   const double starting_norm = std::sqrt(start_norm2);

@@ -210,3 +210,19 @@ def test_lookahead_schedule_is_bitwise_plain_schedule(dev, monkeypatch):
     ref = orc.MomentAccumulator(orc.form_gram(orc.ProblemMatrix(a)), ro).accumulate(s0, 3).blocks
     for k in range(4):
         assert np.linalg.norm(look[-1][k] - ref[k]) / np.linalg.norm(ref[k]) <= 1e-10
+
+
+def test_staged_back_substitution_is_bitwise_warp_streamed(dev, monkeypatch):
+    """The shared-memory staged back substitution performs the same per-row dot products and warp
+    reductions as the warp-streamed kernel: bitwise-equal moments (n = 700: a ragged last block;
+    L = 12 leaves idle warps in the last CTA)."""
+    a = constructed(900, 700, np.linspace(0.05, 1.5, 700), 41, 42)
+    rg, _ = rules(0.6, 0.9, 32, 0.1)
+    s0 = orc.random_start(700, 12, 42)
+    monkeypatch.setenv("SSSVD_TRSM", "warp")
+    ref = gpu_blocks(dev, a, rg, s0, 3)
+    monkeypatch.setenv("SSSVD_TRSM", "smem")
+    for _ in range(3):   # eager, captured, replayed
+        got = gpu_blocks(dev, a, rg, s0, 3)
+        for k in range(4):
+            assert np.array_equal(ref[k], got[k])
