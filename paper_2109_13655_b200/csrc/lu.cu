@@ -692,9 +692,29 @@ __global__ void scatter_copy_kernel(double2* mats, int ld, long long stride, int
   double2* Mb = mats + b * stride;
   const int* d = disp + (size_t)b * (2 * dstride + 1);
   const int nd = d[0];
-  for (int t = 0; t < nd; ++t) Mb[(size_t)d[1 + 2 * t] * ld + c] = Mb[(size_t)d[2 + 2 * t] * ld + c];
+  // sources of the displaced moves are panel rows and their destinations lie below the panel, so
+  // the moves never alias: 8 loads are issued before their 8 stores (the compiler cannot prove
+  // this and would otherwise serialise one load-store round trip per move)
+  constexpr int U = 8;
+  int t = 0;
+  for (; t + U <= nd; t += U) {
+    double2 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = Mb[(size_t)d[2 + 2 * (t + u)] * ld + c];
+#pragma unroll
+    for (int u = 0; u < U; ++u) Mb[(size_t)d[1 + 2 * (t + u)] * ld + c] = v[u];
+  }
+  for (; t < nd; ++t) Mb[(size_t)d[1 + 2 * t] * ld + c] = Mb[(size_t)d[2 + 2 * t] * ld + c];
   const double2* Tb = T + b * tstride;
-  for (int q = 0; q < np; ++q) Mb[(size_t)(r0 + q) * ld + c] = Tb[(size_t)q * ldt + (c - c0)];
+  int q = 0;
+  for (; q + U <= np; q += U) {
+    double2 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = Tb[(size_t)(q + u) * ldt + (c - c0)];
+#pragma unroll
+    for (int u = 0; u < U; ++u) Mb[(size_t)(r0 + q + u) * ld + c] = v[u];
+  }
+  for (; q < np; ++q) Mb[(size_t)(r0 + q) * ld + c] = Tb[(size_t)q * ldt + (c - c0)];
 }
 
 cudaError_t scatter_copy(double2* mats, int ld, long long stride, int r0, int np, int c0, int c1, const int* disp,
