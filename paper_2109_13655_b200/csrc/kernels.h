@@ -43,7 +43,7 @@ cudaError_t leaf_lu_v2(double2* mats, int ld, long long stride, int n, int r0, i
 void leaf_profile_read(unsigned long long* out5, bool reset);
 // K2 v3 (lu.cu): shared-memory slab with thread-owned rows (same smem sizing as v1)
 cudaError_t leaf_lu_v3(double2* mats, int ld, long long stride, int n, int r0, int w, int W, int cluster, int* ipiv,
-                       int batch, cudaStream_t s);
+                       int batch, cudaStream_t s, int cb);
 // K3/K4 (lu.cu): interchanges ipiv[r0..r0+np) on columns [c0,c1), then optional unit-lower TRSM
 cudaError_t swap_trsm(double2* mats, int ld, long long stride, int n, int r0, int np, int c0, int c1,
                       const int* ipiv, bool do_trsm, int batch, cudaStream_t s);
@@ -67,6 +67,9 @@ cudaError_t build_moves(const int* ipiv, int n, int r0, int np, int* src, int* d
                         cudaStream_t s);
 // back-substitution kernel choice: 0 shared-memory staged (default), 1 warp-streamed (lu.cu)
 int trsm_variant();
+// leaf_lu_v3 applies its interchanges to the block columns [cb, r0) itself (lu.cu); false: the
+// caller launches swap_trsm
+bool leaf_swap_fused();
 // build_moves + trinv_lower fused into one launch (lu.cu)
 cudaError_t panel_prep(const double2* mats, int ld, long long stride, int r0, int np, double2* linv, long long lstride,
                        const int* ipiv, int n, int* src, int* disp, int dstride, int batch, cudaStream_t s);

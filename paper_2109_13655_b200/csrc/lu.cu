@@ -16,6 +16,7 @@
 //   * pivot_floor_kernel : min |U_ii| against 1e-30 (max|G| + |z|) (shifted_solver.hpp:27-30)
 // The trailing updates are zgemm_sub (zgemm.cu, DMMA).
 #include <cooperative_groups.h>
+#include <algorithm>
 #include <cstdlib>
 #include <string>
 
@@ -1181,7 +1182,7 @@ namespace sssvd_gpu {
 // and performs the interchange in the slab.
 template <int W, int NT>
 __global__ void __launch_bounds__(NT, 1)
-leaf_lu_v3_kernel(double2* mats, int ld, long long stride, int n, int r0, int w, int R, int* ipiv) {
+leaf_lu_v3_kernel(double2* mats, int ld, long long stride, int n, int r0, int w, int R, int* ipiv, int cb) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   constexpr int P = W + 1;
   double2* slab = reinterpret_cast<double2*>(sm_raw);   // R x P
@@ -1300,14 +1301,70 @@ leaf_lu_v3_kernel(double2* mats, int ld, long long stride, int n, int r0, int w,
     Mb[(size_t)(my0 + i) * ld + r0 + c] = slab[i * P + c];
   }
   cluster_sync_all();
+  // ---- epilogue (rank 0): this leaf's w interchanges applied to the block columns on its left,
+  // [cb, r0) (the separate swap_trsm launch of the recursive panel otherwise). Warp 0 folds the
+  // sequential swaps into <= 2w (destination <- source) moves; each thread then gathers every
+  // source of its column before scattering, so no load waits on a store. Only global rows of
+  // columns the leaf never touches are involved, and the slab is free again after the barrier.
+  if (cb < r0 && rank == 0) {
+    int* pos = reinterpret_cast<int*>(sm_raw);        // [2W] touched rows
+    int* cont = pos + 2 * W;                          // [2W] their final source rows
+    double2* buf = reinterpret_cast<double2*>(sm_raw + 1024);
+    __shared__ int kmv;
+    const int* piv = ipiv + (size_t)b * n;
+    if (warp == 0) {
+      int k = 0;
+      for (int j = 0; j < w; ++j) {
+        const int a = r0 + j, q = piv[r0 + j];
+        int ia = -1, iq = -1;
+        for (int base = 0; base < k; base += 32) {
+          const int t = base + lane;
+          const int pv = t < k ? pos[t] : -1;
+          const unsigned ba = __ballot_sync(0xffffffffu, pv == a);
+          const unsigned bq = __ballot_sync(0xffffffffu, pv == q);
+          if (ba && ia < 0) ia = base + __ffs(ba) - 1;
+          if (bq && iq < 0) iq = base + __ffs(bq) - 1;
+        }
+        if (ia < 0) {
+          if (lane == 0) { pos[k] = a; cont[k] = a; }
+          ia = k++;
+        }
+        if (q == a) iq = ia;
+        if (iq < 0) {
+          if (lane == 0) { pos[k] = q; cont[k] = q; }
+          iq = k++;
+        }
+        __syncwarp();
+        if (lane == 0 && ia != iq) { const int t = cont[ia]; cont[ia] = cont[iq]; cont[iq] = t; }
+        __syncwarp();
+      }
+      if (lane == 0) kmv = k;
+    }
+    __syncthreads();
+    const int k = kmv, ncl = r0 - cb;
+    for (int c = tid; c < ncl; c += NT) {
+      for (int e = 0; e < k; ++e) buf[(size_t)e * ncl + c] = Mb[(size_t)cont[e] * ld + cb + c];
+      for (int e = 0; e < k; ++e)
+        if (pos[e] != cont[e]) Mb[(size_t)pos[e] * ld + cb + c] = buf[(size_t)e * ncl + c];
+    }
+  }
+}
+
+// SSSVD_LEAF_SWAP=kernel: interchanges on the left block columns as a separate swap_trsm launch
+// (the previous schedule; read per call for A/B tests, part of the shifted-solve graph key)
+bool leaf_swap_fused() {
+  const char* e = std::getenv("SSSVD_LEAF_SWAP");
+  return !(e && std::string(e) == "kernel");
 }
 
 template <int W, int NT>
 static cudaError_t launch_leaf_v3(double2* mats, int ld, long long stride, int n, int r0, int w, int cluster,
-                                  int* ipiv, int batch, cudaStream_t s) {
+                                  int* ipiv, int batch, cudaStream_t s, int cb) {
   const int m = n - r0;
   const int R = (m + cluster - 1) / cluster;
-  const size_t smem = (size_t)R * (W + 1) * sizeof(double2);
+  // the slab, or the fused left-swap epilogue's move list + gather buffer if that is larger
+  const size_t smem = std::max((size_t)R * (W + 1) * sizeof(double2),
+                               cb < r0 ? 1024 + (size_t)2 * W * (r0 - cb) * sizeof(double2) : (size_t)0);
   static size_t configured = 0;
   if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(leaf_lu_v3_kernel<W, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1329,15 +1386,16 @@ static cudaError_t launch_leaf_v3(double2* mats, int ld, long long stride, int n
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   note_launch();
-  return cudaLaunchKernelEx(&cfg, leaf_lu_v3_kernel<W, NT>, mats, ld, stride, n, r0, w, R, ipiv);
+  return cudaLaunchKernelEx(&cfg, leaf_lu_v3_kernel<W, NT>, mats, ld, stride, n, r0, w, R, ipiv, cb);
 }
 
 cudaError_t leaf_lu_v3(double2* mats, int ld, long long stride, int n, int r0, int w, int W, int cluster, int* ipiv,
-                       int batch, cudaStream_t s) {
+                       int batch, cudaStream_t s, int cb) {
+  if (cb > r0) return cudaErrorInvalidValue;
   switch (W) {
-    case 8: return launch_leaf_v3<8, 512>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s);
-    case 16: return launch_leaf_v3<16, 512>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s);
-    case 32: return launch_leaf_v3<32, 256>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s);
+    case 8: return launch_leaf_v3<8, 512>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s, cb);
+    case 16: return launch_leaf_v3<16, 512>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s, cb);
+    case 32: return launch_leaf_v3<32, 256>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s, cb);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -226,3 +226,19 @@ def test_staged_back_substitution_is_bitwise_warp_streamed(dev, monkeypatch):
         got = gpu_blocks(dev, a, rg, s0, 3)
         for k in range(4):
             assert np.array_equal(ref[k], got[k])
+
+
+def test_leaf_fused_left_swaps_are_bitwise_separate_launch(dev, monkeypatch):
+    """The leaf kernel's epilogue applies its interchanges to the block columns on its left (the
+    separate swap_trsm launch otherwise): pure data movement, so bitwise-equal moments. n = 700
+    with a pivot-hungry shift set (interval inside the spectrum)."""
+    a = constructed(900, 700, np.linspace(0.05, 1.5, 700), 51, 52)
+    rg, _ = rules(0.6, 0.9, 32, 0.1)
+    s0 = orc.random_start(700, 8, 42)
+    monkeypatch.setenv("SSSVD_LEAF_SWAP", "kernel")
+    ref = gpu_blocks(dev, a, rg, s0, 3)
+    monkeypatch.setenv("SSSVD_LEAF_SWAP", "fused")
+    for _ in range(3):   # eager, captured, replayed
+        got = gpu_blocks(dev, a, rg, s0, 3)
+        for k in range(4):
+            assert np.array_equal(ref[k], got[k])
