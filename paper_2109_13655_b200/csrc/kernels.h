@@ -70,6 +70,8 @@ int trsm_variant();
 // leaf_lu_v3 applies its interchanges to the block columns [cb, r0) itself (lu.cu); false: the
 // caller launches swap_trsm
 bool leaf_swap_fused();
+// panel_prep form: 0 staged 8-warp (default), 1 the 4-warp ballot form (lu.cu)
+int panel_prep_variant();
 // build_moves + trinv_lower fused into one launch (lu.cu)
 cudaError_t panel_prep(const double2* mats, int ld, long long stride, int r0, int np, double2* linv, long long lstride,
                        const int* ipiv, int n, int* src, int* disp, int dstride, int batch, cudaStream_t s);

@@ -654,9 +654,168 @@ __global__ void panel_prep_kernel(const double2* __restrict__ mats, int ld, long
     build_moves_body(ipiv, n, r0, np, src, disp, dstride, blockIdx.y, mv);
 }
 
+// panel_prep, second form (default): 8 warps per CTA. The L11^{-1} columns of a CTA share the
+// rows of L11, staged in shared memory R rows at a time by cp.async two chunks ahead (the
+// single-warp prefetch of the first form waited on an L2 round trip per row); the interchange
+// fold looks positions up in a row-indexed table instead of a warp-ballot search. Bitwise the
+// first form: every dot product, reduction and fold step is unchanged.
+template <int QMAX>
+__global__ void __launch_bounds__(256)
+panel_prep2_kernel(const double2* __restrict__ mats, int ld, long long stride, int r0, int np,
+                   double2* __restrict__ linv, long long lstride, const int* __restrict__ ipiv, int n,
+                   int* __restrict__ src, int* __restrict__ disp, int dstride) {
+  constexpr int WPB = 8, R = 32 / QMAX, NP = 32 * QMAX;
+  __shared__ __align__(16) double2 buf[2][R][NP];
+  extern __shared__ int tbl[];   // build-moves CTA: [n - r0] slot of each row, then pos / cont
+  const int b = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const int nx = (np + WPB - 1) / WPB;
+  if ((int)blockIdx.x == nx) {
+    // ---- interchange map (semantics of build_moves_body)
+    int* pos = tbl + (n - r0);
+    int* cont = pos + 2 * np;
+    __shared__ int kmv;
+    const int* piv = ipiv + (size_t)b * n;
+    for (int j = tid; j < np; j += blockDim.x) {
+      tbl[j] = -1;
+      tbl[piv[r0 + j] - r0] = -1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int k = 0;
+      for (int j = 0; j < np; ++j) {
+        const int a = r0 + j, q = piv[r0 + j];
+        int ia = tbl[a - r0];
+        if (ia < 0) {
+          pos[k] = a;
+          cont[k] = a;
+          tbl[a - r0] = k;
+          ia = k++;
+        }
+        int iq = q == a ? ia : tbl[q - r0];
+        if (iq < 0) {
+          pos[k] = q;
+          cont[k] = q;
+          tbl[q - r0] = k;
+          iq = k++;
+        }
+        if (ia != iq) {
+          const int t = cont[ia];
+          cont[ia] = cont[iq];
+          cont[iq] = t;
+        }
+      }
+      kmv = k;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const int k = kmv;
+      int* so = src + (size_t)b * dstride;
+      int* d = disp + (size_t)b * (2 * dstride + 1);
+      int nd = 0;
+      for (int base = 0; base < k; base += 32) {
+        const int t = base + lane;
+        const bool below = t < k && pos[t] >= r0 + np && cont[t] != pos[t];
+        if (t < k && pos[t] < r0 + np) so[pos[t] - r0] = cont[t];
+        const unsigned bal = __ballot_sync(0xffffffffu, below);
+        if (below) {
+          const int sl = nd + __popc(bal & ((1u << lane) - 1));
+          d[1 + 2 * sl] = pos[t];
+          d[2 + 2 * sl] = cont[t];
+        }
+        nd += __popc(bal);
+      }
+      if (lane == 0) d[0] = nd;
+    }
+    return;
+  }
+  // ---- L11^{-1} columns j0 .. j0 + WPB - 1 (semantics of trinv_lower_body)
+  const int j0 = blockIdx.x * WPB, j = j0 + warp;
+  const bool active = j < np;
+  const double2* Mb = mats + b * stride + (size_t)r0 * ld + r0;
+  double2* out = linv + (size_t)b * lstride;
+  const int t0 = (j0 + 1) / R, T = (np + R - 1) / R;   // chunks of rows [t R, t R + R)
+  auto load_chunk = [&](int t) {
+    if (t < T) {
+      for (int idx = tid; idx < R * np; idx += 32 * WPB) {
+        const int sl = idx / np, l = idx - sl * np;
+        const int i = t * R + sl;
+        if (i < np) cp_async16(&buf[t & 1][sl][l], Mb + (size_t)i * ld + l);
+      }
+    }
+    cp_async_commit();
+  };
+  load_chunk(t0);
+  load_chunk(t0 + 1);
+  double2 x[QMAX];
+#pragma unroll
+  for (int q = 0; q < QMAX; ++q) x[q] = make_double2((lane + 32 * q) == j ? 1.0 : 0.0, 0.0);
+  for (int t = t0; t < T; ++t) {
+    cp_async_wait<1>();
+    __syncthreads();
+    if (active) {
+      for (int sl = 0; sl < R; ++sl) {
+        const int i = t * R + sl;
+        if (i <= j || i >= np) continue;
+        const int qi = i >> 5, ii = i & 31;
+        double sr = 0.0, si = 0.0;
+#pragma unroll
+        for (int q = 0; q < QMAX; ++q) {
+          const int l = lane + 32 * q;
+          if (q <= qi && l >= j && l < i) {
+            const double2 lr = buf[t & 1][sl][l];
+            sr += lr.x * x[q].x - lr.y * x[q].y;
+            si += lr.x * x[q].y + lr.y * x[q].x;
+          }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          sr += __shfl_xor_sync(0xffffffffu, sr, off);
+          si += __shfl_xor_sync(0xffffffffu, si, off);
+        }
+#pragma unroll
+        for (int q = 0; q < QMAX; ++q)
+          if (q == qi && lane == ii) x[q] = make_double2(-sr, -si);
+      }
+    }
+    __syncthreads();
+    load_chunk(t + 2);
+  }
+  if (active) {
+#pragma unroll
+    for (int q = 0; q < QMAX; ++q) {
+      const int i = lane + 32 * q;
+      if (i < np) out[(size_t)i * np + j] = i >= j ? x[q] : make_double2(0.0, 0.0);
+    }
+  }
+}
+
+// SSSVD_PANEL_PREP=v1: the 4-warp form with the ballot fold (read per call; graph key)
+int panel_prep_variant() {
+  const char* e = std::getenv("SSSVD_PANEL_PREP");
+  return (e && std::string(e) == "v1") ? 1 : 0;
+}
+
 cudaError_t panel_prep(const double2* mats, int ld, long long stride, int r0, int np, double2* linv, long long lstride,
                        const int* ipiv, int n, int* src, int* disp, int dstride, int batch, cudaStream_t s) {
   if (np > 256) return cudaErrorInvalidValue;
+  if (panel_prep_variant() == 0) {
+    const size_t sm2 = (size_t)(n - r0 + 4 * np) * sizeof(int);
+    static size_t configured = 0;
+    if (sm2 > configured) {
+      cudaError_t e = cudaFuncSetAttribute(panel_prep2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(panel_prep2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+      if (e != cudaSuccess) return e;
+      configured = sm2;
+    }
+    dim3 grid2((np + 7) / 8 + 1, batch);
+    if (np <= 128)
+      panel_prep2_kernel<4><<<grid2, 256, sm2, s>>>(mats, ld, stride, r0, np, linv, lstride, ipiv, n, src, disp, dstride);
+    else
+      panel_prep2_kernel<8><<<grid2, 256, sm2, s>>>(mats, ld, stride, r0, np, linv, lstride, ipiv, n, src, disp, dstride);
+    note_launch();
+    return cudaGetLastError();
+  }
   dim3 grid((np + 3) / 4 + 1, batch);
   const size_t sm = 4 * np * sizeof(int);
   if (np <= 128)

@@ -686,7 +686,7 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
           (uintptr_t)P.cluster, (uintptr_t)(P.leaf_variant + 1), (uintptr_t)P.ld, (uintptr_t)ctx->G.p,
           (uintptr_t)V_dev, (uintptr_t)mats, (uintptr_t)ipiv, (uintptr_t)work.linv, (uintptr_t)work.T,
           (uintptr_t)work.src, (uintptr_t)work.disp, (uintptr_t)dshift, (uintptr_t)dcoef, (uintptr_t)S_dev,
-          (uintptr_t)ctx->gmax.p, (uintptr_t)dstatus, (uintptr_t)dmin, (uintptr_t)lookahead, (uintptr_t)trsm_variant(), (uintptr_t)leaf_swap_fused(),
+          (uintptr_t)ctx->gmax.p, (uintptr_t)dstatus, (uintptr_t)dmin, (uintptr_t)lookahead, (uintptr_t)trsm_variant(), (uintptr_t)leaf_swap_fused(), (uintptr_t)panel_prep_variant(),
           (uintptr_t)work2.linv, (uintptr_t)work2.T, (uintptr_t)work2.src, (uintptr_t)work2.disp};
       for (auto& g : ctx->lu_graphs)
         if (g.key == key) replayed = &g;

@@ -242,3 +242,18 @@ def test_leaf_fused_left_swaps_are_bitwise_separate_launch(dev, monkeypatch):
         got = gpu_blocks(dev, a, rg, s0, 3)
         for k in range(4):
             assert np.array_equal(ref[k], got[k])
+
+
+def test_staged_panel_prep_is_bitwise_ballot_form(dev, monkeypatch):
+    """panel_prep's staged 8-warp form (L11 rows shared through shared memory, table-driven
+    interchange fold) reproduces the 4-warp ballot form bit for bit."""
+    a = constructed(900, 700, np.linspace(0.05, 1.5, 700), 61, 62)
+    rg, _ = rules(0.6, 0.9, 32, 0.1)
+    s0 = orc.random_start(700, 8, 42)
+    monkeypatch.setenv("SSSVD_PANEL_PREP", "v1")
+    ref = gpu_blocks(dev, a, rg, s0, 3)
+    monkeypatch.setenv("SSSVD_PANEL_PREP", "v2")
+    for _ in range(3):   # eager, captured, replayed
+        got = gpu_blocks(dev, a, rg, s0, 3)
+        for k in range(4):
+            assert np.array_equal(ref[k], got[k])
