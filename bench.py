@@ -161,11 +161,21 @@ def main():
             out.append(dev.run_solve(c))
         return out
 
+    e2e_parts = []
+
     def step_e2e():
         # public API from host memory: H2D of A inside, D2H of all triplets inside
         lib = sssvd.lib()
+        t0 = time.perf_counter()
         dev.check(lib.sssvd_gpu_set_operator(dev.h, sssvd.ctypes.c_void_p(a_pin.data_ptr()), w.m, w.n, w.m, 0))
-        return [dev.run_solve(c) for c in cfgs]
+        parts = [time.perf_counter() - t0]
+        out = []
+        for c in cfgs:
+            t0 = time.perf_counter()
+            out.append(dev.run_solve(c))
+            parts.append(time.perf_counter() - t0)
+        e2e_parts.append([round(x * 1e3, 2) for x in parts])
+        return out
 
     # GEMM timing is on from the first warm-up step: the library captures the shifted-solve pass
     # into a CUDA graph on its second run, keyed (among others) by the profiling state
@@ -205,6 +215,7 @@ def main():
     for _ in range(max(1, args.warmup)):
         res_e = step_e2e()
     barrier()
+    e2e_parts.clear()
     t0 = time.perf_counter()
     e2e_marks = [t0]
     for _ in range(args.steps):
@@ -241,7 +252,8 @@ def main():
                        "parallelism": f"shift-sharded x{world} (+1 NCCL all-reduce)",
                        "l2": "inputs larger than L2: A 134 MB, 16 factors x 272 MB per mode"},
             "e2e": {"value": te, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                    "step_ms": [round((e2e_marks[i + 1] - e2e_marks[i]) * 1e3, 3) for i in range(args.steps)]},
+                    "step_ms": [round((e2e_marks[i + 1] - e2e_marks[i]) * 1e3, 3) for i in range(args.steps)],
+                    "parts_ms": e2e_parts},   # per step: set_operator, then run_solve per mode
             "roofline": {"bound": "tensor", "kernel": "zgemm_sub_kernel (DMMA trailing update)",
                          "achieved": gemm_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": (gemm_tflops / FP64_PEAK_TFLOPS) if gemm_tflops else None,
