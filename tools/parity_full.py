@@ -23,6 +23,7 @@ for mode in modes:
     def near(s): return any(abs(s - e) <= 1e-9 * max(abs(e), s) for e in (w.a, w.b))
     def firm(s, tau, thr): return not near(s) and not (0.5 <= tau / thr <= 2.0)
     matched, worst_sigma, worst_res_ratio, mism, worst_vec = 0, 0.0, 0.0, [], 0.0
+    res_cases = []
     for i in range(o.triplets.count()):
         if not o.triplets.in_interval[i] or o.verdict.spurious[i] or not firm(os_[i], o.verdict.tau[i], othr):
             continue
@@ -34,7 +35,11 @@ for mode in modes:
             worst_sigma = max(worst_sigma, rel)
             for gv, ov in ((g.triplets.left[:, j], o.triplets.left[:, i]), (g.triplets.right[:, j], o.triplets.right[:, i])):
                 worst_vec = max(worst_vec, min(np.linalg.norm(gv - ov), np.linalg.norm(gv + ov)))
-            worst_res_ratio = max(worst_res_ratio, g.exact[j] / max(1e-9 * sigma.max(), 10 * o.residuals.exact[i]))
+            ratio = g.exact[j] / max(1e-9 * sigma.max(), 10 * o.residuals.exact[i])
+            worst_res_ratio = max(worst_res_ratio, ratio)
+            res_cases.append({"sigma": float(os_[i]), "ratio": float(ratio), "gpu_exact": float(g.exact[j]),
+                              "oracle_exact": float(o.residuals.exact[i]), "gpu_tau_ratio": float(g.tau[j] / gthr),
+                              "oracle_tau_ratio": float(o.verdict.tau[i] / othr)})
         else:
             mism.append({"oracle_sigma": float(os_[i]), "gpu_sigma": float(gs[j]), "rel": float(rel),
                          "gpu_tau_ratio": float(g.tau[j] / gthr), "oracle_tau_ratio": float(o.verdict.tau[i] / othr)})
@@ -50,7 +55,11 @@ for mode in modes:
            "truth_in_interval": int(np.sum((sigma >= w.a) & (sigma <= w.b))),
            "moment_blocks_max_relerr": blk, "firm_matched": matched, "firm_mismatches": mism[:20],
            "n_firm_mismatches": len(mism), "worst_matched_sigma_relerr": worst_sigma,
-           "worst_residual_over_bound": worst_res_ratio}
+           "worst_residual_over_bound": worst_res_ratio,
+           "n_residual_over_bound": sum(1 for x in res_cases if x["ratio"] > 1),
+           "residual_cases_worst": sorted(res_cases, key=lambda x: -x["ratio"])[:12],
+           "matched_exact_residual_quantiles": {q: [float(np.quantile([x[k] for x in res_cases], q)) for k in ("gpu_exact", "oracle_exact")]
+                                                for q in (0.5, 0.9, 1.0)} if res_cases else None}
     os.makedirs("gpurun_out", exist_ok=True)
     json.dump(out, open(f"gpurun_out/parity_cfg{c}_mode{mode}.json", "w"), indent=1)
     print(json.dumps({k: v for k, v in out.items() if k != "firm_mismatches"}), flush=True)
