@@ -8,14 +8,15 @@ import numpy as np
 from paper_2109_13655_b200 import sssvd, workloads
 from oracle import sssvd_oracle as orc
 
+DELTA = float(os.environ.get('PARITY_DELTA', '1e-20'))   # diagnostic: delta (moments.hpp:27) on both sides
 c = int(sys.argv[1]); modes = [int(x) for x in sys.argv[2:]] or list(workloads.CONFIGS[c].modes)
 w = workloads.CONFIGS[c]
 a, sigma = workloads.make_operator(c)
 dev = sssvd.Device(0)
 for mode in modes:
-    cfg = sssvd.RunConfig(w.a, w.b, mode=mode, params=sssvd.SsParams(block_size=w.L, moment_degree=w.M, quadrature_count=w.N), gram_cap=1 << 30)
+    cfg = sssvd.RunConfig(w.a, w.b, mode=mode, params=sssvd.SsParams(block_size=w.L, moment_degree=w.M, quadrature_count=w.N, lowrank_threshold=DELTA), gram_cap=1 << 30)
     t0 = time.time(); g = sssvd.run_solve(a, cfg, dev); tg = time.time() - t0
-    ocfg = orc.RunConfig(w.a, w.b, mode=[orc.SS_SVD, orc.SS_SVD_NT][mode], params=orc.SsParams(block_size=w.L, moment_degree=w.M, quadrature_count=w.N))
+    ocfg = orc.RunConfig(w.a, w.b, mode=[orc.SS_SVD, orc.SS_SVD_NT][mode], params=orc.SsParams(block_size=w.L, moment_degree=w.M, quadrature_count=w.N, lowrank_threshold=DELTA))
     t0 = time.time(); o = orc.run_solve(orc.ProblemMatrix(a), ocfg, gram_cap=1 << 30); to = time.time() - t0
     blk = max(float(np.linalg.norm(g.blocks.blocks[k] - o.blocks.blocks[k]) / np.linalg.norm(o.blocks.blocks[k])) for k in range(w.M + 1))
     gs, os_ = g.triplets.sigma, o.triplets.sigma
@@ -45,7 +46,7 @@ for mode in modes:
                          "gpu_tau_ratio": float(g.tau[j] / gthr), "oracle_tau_ratio": float(o.verdict.tau[i] / othr)})
     # every oracle candidate inside [a, b] (converged or not): relative distance to the nearest GPU value
     cand = [abs(gs[int(np.argmin(np.abs(gs - x)))] - x) / x for x, f in zip(os_, o.triplets.in_interval) if f]
-    out = {"cfg": c, "mode": mode, "gpu_s": tg, "oracle_s": to, "cores": os.cpu_count(),
+    out = {"cfg": c, "mode": mode, "delta": DELTA, "gpu_s": tg, "oracle_s": to, "cores": os.cpu_count(),
            "in_interval_sigma_reldiff_median": float(np.median(cand)) if cand else None,
            "in_interval_sigma_reldiff_max": float(np.max(cand)) if cand else None,
            "firm_matched_vector_max_diff": worst_vec,
@@ -61,5 +62,5 @@ for mode in modes:
            "matched_exact_residual_quantiles": {q: [float(np.quantile([x[k] for x in res_cases], q)) for k in ("gpu_exact", "oracle_exact")]
                                                 for q in (0.5, 0.9, 1.0)} if res_cases else None}
     os.makedirs("gpurun_out", exist_ok=True)
-    json.dump(out, open(f"gpurun_out/parity_cfg{c}_mode{mode}.json", "w"), indent=1)
+    json.dump(out, open(f"gpurun_out/parity_cfg{c}_mode{mode}" + ("" if DELTA == 1e-20 else f"_delta{DELTA:g}") + ".json", "w"), indent=1)
     print(json.dumps({k: v for k, v in out.items() if k != "firm_mismatches"}), flush=True)
