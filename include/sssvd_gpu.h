@@ -213,14 +213,17 @@ sssvd_status sssvd_debug_thin_qr(sssvd_gpu_ctx* ctx, const double* a, int64_t m,
  * u_out, v_out (k x k column-major), s_out[k] descending. */
 sssvd_status sssvd_debug_svd_square(sssvd_gpu_ctx* ctx, const double* b, int64_t k, double* u_out, double* s_out,
                                     double* v_out);
-/* Debug: the trailing-update GEMM (C -= A B, complex, row-major, batched) on seeded device data:
- * warp-tile variant `variant` (0..9, see zgemm.cu; 10 = cuBLAS zgemmStridedBatched, a comparator only) timed over `reps` launches -> ms_out (mean per launch);
- * mismatches_out = entries of C that differ BITWISE from variant 0 on the same inputs. */
+/* Debug: the trailing-update GEMM (C -= A B, complex, row-major, batched; zgemm.cu) on seeded device
+ * data, timed over `reps` launches -> ms_out (mean per launch); mismatches_out = entries of C that
+ * differ BITWISE between two runs on the same inputs (determinism). variant must be 0. */
 sssvd_status sssvd_debug_zgemm(sssvd_gpu_ctx* ctx, int variant, int64_t m, int64_t n, int64_t k, int64_t batch,
                                int reps, double* ms_out, int64_t* mismatches_out);
-/* Debug: cycles per leaf-kernel phase summed over columns (SSSVD_LEAF_PROF=1): out[0..3] phases,
- * out[4] columns, out[5] summed CTA lifetimes, out[6] leaves (7 entries). */
-void sssvd_debug_leaf_profile(uint64_t* out7);
+/* Debug: the tail GEMM (dgemm.cu) on host column-major data. mode 0: c_io (m x n, ldc) <- alpha
+ * op(a) b + beta c_io, op(a) = a (m x k, lda) or a^T (ta != 0: a is k x m); mode 1: c_io[j] <-
+ * ||op(a) b[:, j] - d[j] v[:, j]|| (v m x n with leading dimension ldc), the fused residual form. */
+sssvd_status sssvd_debug_dgemm(sssvd_gpu_ctx* ctx, int mode, int ta, int64_t m, int64_t n, int64_t k, double alpha,
+                               const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
+                               const double* d, const double* v, double* c_io, int64_t ldc);
 /* ---- Matrix Market ingest (matrix_market.hpp:34-149; host only) ---------------------------- *
  * sssvd_mm_read mirrors read_matrix_market: real/integer/double `array` (dense) and `coordinate`
  * (sparse, duplicates summed in file order, (skew-)symmetric expanded) formats; `complex` and

@@ -23,7 +23,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
             "--expt-relaxed-constexpr", "-I", CSRC]
-CU_SOURCES = ["zgemm.cu", "lu.cu", "gram.cu", "moments.cu", "jacobi_svd.cu", "householder_qr.cu", "sparse.cu", "sssvd_gpu.cu"]
+CU_SOURCES = ["zgemm.cu", "dgemm.cu", "lu.cu", "gram.cu", "moments.cu", "jacobi_svd.cu", "householder_qr.cu", "sparse.cu", "sssvd_gpu.cu"]
 CXX_SOURCES = ["host_mirror.cpp", "matrix_market.cpp", "problems.cpp"]
 
 
@@ -65,7 +65,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         list(ex.map(lambda j: _run(*j), jobs))
     if force or jobs or _stale(LIB, objs):
         _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs +
-             ["-lcublas", "-lcusolver", "-ldl"], os.path.join(BUILD, "link.log"))
+             ["-ldl"], os.path.join(BUILD, "link.log"))
     # the command-line front end (proj/tools/sssvd.cpp) over the C ABI, rpath'ed to this directory
     cli_src = os.path.join(CSRC, "cli.cpp")
     hpp = os.path.join(HERE, "..", "include", "sssvd_gpu.hpp")

@@ -105,12 +105,7 @@ gram_kernel(const double* __restrict__ A, int lda, int K, int n, double* __restr
 
 cudaError_t gram(const double* A, int lda, int K, int n, double* G, int ldg, int part, int nparts, cudaStream_t s) {
   const size_t smem = (size_t)2 * STAGES * TILE * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  SSSVD_CUDA_TRY(set_kernel_smem((const void*)gram_kernel, smem, false));
   const long long T = (n + BM - 1) / BM;
   const long long tiles = T * (T + 1) / 2;
   const long long mine = (tiles - part + nparts - 1) / nparts;

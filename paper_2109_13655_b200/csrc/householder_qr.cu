@@ -217,16 +217,7 @@ cudaError_t qr_panel(double* A, int lda, int m, int j, int w, double* Y, int ldy
   const int rp = qr_panel_plan(m - j, w, &C);
   if (rp == 0) return cudaErrorInvalidValue;
   const size_t smem = qr_panel_smem(rp, w);
-  static size_t configured = 0;
-  if (smem > configured) {
-    for (auto fn : {qr_panel_kernel<true>, qr_panel_kernel<false>}) {
-      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      if (e != cudaSuccess) return e;
-    }
-    configured = smem;
-  }
+  for (auto fn : {qr_panel_kernel<true>, qr_panel_kernel<false>}) SSSVD_CUDA_TRY(set_kernel_smem((const void*)fn, smem, true));
   cudaError_t e;
   if (C == 1) {
     qr_panel_kernel<false><<<1, QP_THREADS, smem, s>>>(A, lda, m, j, w, rp, Y, ldy, T, tau);
@@ -432,14 +423,8 @@ cudaError_t qr_panel_reg(double* A, int lda, int m, int j, int w, int W, double*
   while (C < 16 && (mp + C - 1) / C > cap) C *= 2;
   const int rp = (mp + C - 1) / C;
   if (rp > cap) return cudaErrorInvalidValue;
-  static bool configured = false;
-  if (!configured) {
-    for (auto fn : {qr_panel_reg_kernel<8, true>, qr_panel_reg_kernel<16, true>, qr_panel_reg_kernel<32, true>}) {
-      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      if (e != cudaSuccess) return e;
-    }
-    configured = true;
-  }
+  for (auto fn : {qr_panel_reg_kernel<8, true>, qr_panel_reg_kernel<16, true>, qr_panel_reg_kernel<32, true>})
+    SSSVD_CUDA_TRY(set_kernel_smem((const void*)fn, 0, true));
   cudaError_t e;
   if (C == 1) {
     if (W == 8) qr_panel_reg_kernel<8, false><<<1, QR_THREADS, 0, s>>>(A, lda, m, j, w, rp, Y, ldy, T, tau);
@@ -492,12 +477,7 @@ larft_kernel(const double* __restrict__ G, int kb, const double* __restrict__ ta
 cudaError_t larft(const double* G, int kb, const double* tau, double* T, cudaStream_t s) {
   if (kb < 1 || kb > 128) return cudaErrorInvalidValue;
   const size_t smem = (size_t)kb * kb * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 128 * 8);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  SSSVD_CUDA_TRY(set_kernel_smem((const void*)larft_kernel, 128 * 128 * 8, false));
   larft_kernel<<<1, 128, smem, s>>>(G, kb, tau, T);
   note_launch();
   return cudaGetLastError();

@@ -238,12 +238,8 @@ cudaError_t jacobi_svd(double* W, double* V, int k, int ldw, double* S, double t
   set_identity_kernel<<<148 * 4, 256, 0, s>>>(V, k, ldw);
   note_launch();
   if (k > 1) {
-    static bool configured = false;
-    if (!configured) {
-      e = cudaFuncSetAttribute(jacobi_svd_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      if (e != cudaSuccess) return e;
-      configured = true;
-    }
+    e = set_kernel_smem((const void*)jacobi_svd_cluster_kernel, 0, true);
+    if (e != cudaSuccess) return e;
     unsigned int* rot = scratch + 2;      // [2], [3] rotation counts (ping-pong by sweep parity)
     const int npairs = (k + (k & 1)) / 2;
     if (npairs > 256) {
@@ -279,397 +275,11 @@ cudaError_t jacobi_svd(double* W, double* V, int k, int ldw, double* S, double t
   return cudaGetLastError();
 }
 
-}  // namespace sssvd_gpu
-
-namespace sssvd_gpu {
-
-// ----------------------------------------------------------------------------- block Jacobi
-// Block one-sided Jacobi for k <= 512 (the tail's k x k factors of configs 1, 2, 4). The k columns
-// are split into 32 blocks of b = ceil(k/32) columns (zero padding columns never rotate). One
-// cluster of 16 CTAs; outer round = a tournament pairing of the 32 blocks: CTA c loads its block
-// pair (2b columns x k rows) into shared memory, orthogonalises all 2b columns with one inner
-// sweep (2b-1 inner rounds of b disjoint pairs, one warp per pair, __syncthreads between inner
-// rounds) while accumulating the 2b x 2b rotation Q, writes the block pair back, and applies
-// V[:, pair] <- V[:, pair] Q. Outer rounds are separated by the cluster barrier (blocks travel
-// through L2). Same rotations and threshold as the scalar kernel; 31 cluster barriers per sweep
-// instead of k-1.
-constexpr int BJ_THREADS = 512;
-constexpr int BJ_RPL = 16;   // rows per lane in the inner sweep (k <= 512)
-
-__device__ __forceinline__ void load_col(double (&x)[BJ_RPL], const double* w, int k, int lane) {
-#pragma unroll
-  for (int i = 0; i < BJ_RPL; ++i) {
-    const int r = lane + 32 * i;
-    x[i] = r < k ? w[r] : 0.0;
-  }
-}
-__device__ __forceinline__ void store_col(const double (&x)[BJ_RPL], double* w, int k, int lane) {
-#pragma unroll
-  for (int i = 0; i < BJ_RPL; ++i) {
-    const int r = lane + 32 * i;
-    if (r < k) w[r] = x[i];
-  }
-}
-// alpha = |x|^2, beta = |y|^2, gamma = x.y over the warp; rotate iff |gamma| > tol sqrt(alpha beta).
-// t = sign(D) 2 gamma / (|D| + sqrt(D^2 + 4 gamma^2)), D = beta - alpha (= sign(zeta) / (|zeta| +
-// sqrt(1 + zeta^2)) with zeta = D / (2 gamma): one sqrt and one division on the critical path).
-__device__ __forceinline__ bool pair_rotation(const double (&x)[BJ_RPL], const double (&y)[BJ_RPL], double tol,
-                                              double& cs, double& sn) {
-  double a = 0.0, bb = 0.0, g = 0.0, a2 = 0.0, bb2 = 0.0, g2 = 0.0;
-#pragma unroll
-  for (int i = 0; i < BJ_RPL; i += 2) {
-    a = fma(x[i], x[i], a);
-    bb = fma(y[i], y[i], bb);
-    g = fma(x[i], y[i], g);
-    a2 = fma(x[i + 1], x[i + 1], a2);
-    bb2 = fma(y[i + 1], y[i + 1], bb2);
-    g2 = fma(x[i + 1], y[i + 1], g2);
-  }
-  a += a2;
-  bb += bb2;
-  g += g2;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    a += __shfl_xor_sync(0xffffffffu, a, off);
-    bb += __shfl_xor_sync(0xffffffffu, bb, off);
-    g += __shfl_xor_sync(0xffffffffu, g, off);
-  }
-  if (!(g * g > tol * tol * a * bb) || g == 0.0) return false;
-  const double d = bb - a, g2x = 2.0 * g;
-  const double t = copysign(1.0, d) * g2x / (fabs(d) + sqrt(fma(d, d, g2x * g2x)));
-  cs = rsqrt(fma(t, t, 1.0));
-  sn = cs * t;
-  return true;
-}
-__device__ __forceinline__ void rotate_cols(double (&x)[BJ_RPL], double (&y)[BJ_RPL], double cs, double sn) {
-#pragma unroll
-  for (int i = 0; i < BJ_RPL; ++i) {
-    const double u = x[i], v = y[i];
-    x[i] = cs * u - sn * v;
-    y[i] = sn * u + cs * v;
-  }
-}
-__device__ __forceinline__ void rotate_q(double* Qs, int w2, int p, int q, double cs, double sn, int lane) {
-  if (lane < w2) {
-    double* qp = Qs + (size_t)p * w2;
-    double* qq = Qs + (size_t)q * w2;
-    const double u = qp[lane], v = qq[lane];
-    qp[lane] = cs * u - sn * v;
-    qq[lane] = sn * u + cs * v;
-  }
-}
-
-template <bool PROF>
-__global__ void __launch_bounds__(BJ_THREADS, 1)
-jacobi_block_kernel(double* __restrict__ Wm, double* __restrict__ Vm, int k, int ldw, int b, double tol,
-                    int max_sweeps, unsigned int* __restrict__ rot_count, int* __restrict__ sweeps_out,
-                    unsigned long long* __restrict__ prof) {
-  extern __shared__ __align__(16) double bsm[];
-  const int w2 = 2 * b;                 // columns per block pair
-  double* Ws = bsm;                     // [w2][k] columns
-  double* Qs = Ws + (size_t)w2 * k;     // [w2][w2] column-major
-  __shared__ int colid[32];             // global column of local column c (or -1)
-  __shared__ unsigned int cta_rot;
-  __shared__ __align__(8) unsigned long long mbar;
-  unsigned phase = 0;
-  const bool bulk = (k % 2) == 0;       // 16-byte aligned columns: TMA bulk loads and stores
-  if (threadIdx.x == 0) mbar_init(&mbar, 1);
-  __syncthreads();
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int c = blockIdx.x;             // block pair slot 0..15
-  const bool rec = PROF && blockIdx.x == 0 && tid == 0;
-  unsigned long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
-  int sweep = 0;
-  for (; sweep < max_sweeps; ++sweep) {
-    unsigned int my_rot = 0;
-    if (tid == 0) cta_rot = 0;
-    for (int round = 0; round < 31; ++round) {
-      if (rec) t0 = clock64();
-      // blocks at tournament positions c and 31 - c
-      const int bx = player(c, round, 32), by = player(31 - c, round, 32);
-      if (tid < w2) {
-        const int blk = tid < b ? bx : by;
-        const int gc = blk * b + (tid < b ? tid : tid - b);
-        colid[tid] = gc < k ? gc : -1;
-      }
-      __syncthreads();
-      // block pair -> Ws through L2 (other CTAs wrote these columns last round: bypass L1)
-      if (bulk) {
-        // TMA bulk copies, one column per issuing thread, all completing on one mbarrier
-        // (no registers held in flight); padding columns are zero-filled by the other threads
-        if (tid == 0) {
-          unsigned bytes = 0;
-          for (int lc = 0; lc < w2; ++lc)
-            if (colid[lc] >= 0) bytes += (unsigned)k * 8u;
-          mbar_expect_tx(&mbar, bytes);
-        }
-        if (tid < w2 && colid[tid] >= 0) bulk_g2s(Ws + (size_t)tid * k, Wm + (size_t)colid[tid] * ldw, (unsigned)k * 8u, &mbar);
-        for (int e = tid; e < w2 * k; e += BJ_THREADS)
-          if (colid[e / k] < 0) Ws[e] = 0.0;
-        mbar_wait(&mbar, phase);
-        phase ^= 1u;
-      } else {
-        for (int e = tid; e < w2 * k; e += BJ_THREADS) {
-          const int lc = e / k, r = e - lc * k;
-          const int gc = colid[lc];
-          Ws[e] = gc >= 0 ? __ldcg(Wm + (size_t)gc * ldw + r) : 0.0;
-        }
-      }
-      for (int e = tid; e < w2 * w2; e += BJ_THREADS) Qs[e] = (e / w2) == (e % w2) ? 1.0 : 0.0;
-      __syncthreads();
-      if (rec) t1 = clock64();
-      if (round == 0) {
-        // outer round 0 visits every block once: one full inner sweep over all pairs of the 2b
-        // local columns (intra-block and cross pairs); each warp keeps its pair in registers
-        // between the dot products and the rotation and writes back only if it rotates
-        for (int ir = 0; ir < w2 - 1; ++ir) {
-          for (int pi = warp; pi < b; pi += BJ_THREADS / 32) {
-            int p = player(pi, ir, w2), q = player(w2 - 1 - pi, ir, w2);
-            if (p > q) { int t = p; p = q; q = t; }
-            double* wp = Ws + (size_t)p * k;
-            double* wq = Ws + (size_t)q * k;
-            double x[BJ_RPL], y[BJ_RPL];
-            load_col(x, wp, k, lane);
-            load_col(y, wq, k, lane);
-            double cs, sn;
-            if (pair_rotation(x, y, tol, cs, sn)) {
-              rotate_cols(x, y, cs, sn);
-              store_col(x, wp, k, lane);
-              store_col(y, wq, k, lane);
-              rotate_q(Qs, w2, p, q, cs, sn, lane);
-              ++my_rot;
-            }
-          }
-          __syncthreads();
-        }
-      } else {
-        // later outer rounds: only the b x b cross pairs (the intra-block pairs were rotated in
-        // round 0 of this sweep). Warp w keeps its resident column w in registers; the partner
-        // columns b + (w + ir) mod b travel from warp to warp through shared memory, so each
-        // inner round moves one column per warp instead of two, and there are b rounds, not 2b-1.
-        double x[BJ_RPL];
-        const bool active = warp < b;
-        if (active) load_col(x, Ws + (size_t)warp * k, k, lane);
-        bool moved = false;
-        for (int ir = 0; ir < b; ++ir) {
-          if (active) {
-            const int q = b + (warp + ir) % b;
-            double* wq = Ws + (size_t)q * k;
-            double y[BJ_RPL];
-            load_col(y, wq, k, lane);
-            double cs, sn;
-            if (pair_rotation(x, y, tol, cs, sn)) {
-              rotate_cols(x, y, cs, sn);
-              store_col(y, wq, k, lane);
-              rotate_q(Qs, w2, warp, q, cs, sn, lane);
-              moved = true;
-              ++my_rot;
-            }
-          }
-          __syncthreads();
-        }
-        if (active && moved) store_col(x, Ws + (size_t)warp * k, k, lane);
-        __syncthreads();
-      }
-      if (rec) t2 = clock64();
-      // write the block pair back (TMA bulk store, overlapped with the V update below)
-      if (bulk) {
-        fence_proxy_async();   // make the generic-proxy smem writes visible to the bulk engine
-        __syncthreads();
-        if (tid < w2 && colid[tid] >= 0) bulk_s2g(Wm + (size_t)colid[tid] * ldw, Ws + (size_t)tid * k, (unsigned)k * 8u);
-        if (tid < w2) bulk_commit();
-      } else {
-        for (int e = tid; e < w2 * k; e += BJ_THREADS) {
-          const int lc = e / k, r = e - lc * k;
-          if (colid[lc] >= 0) Wm[(size_t)colid[lc] * ldw + r] = Ws[e];
-        }
-      }
-      unsigned long long t2a = rec ? clock64() : 0;
-      // V[:, pair] <- V[:, pair] Q on the FP64 tensor cores (DMMA m8n8k4): warp w owns rows
-      // [32w, 32w + 32); Q (zero-padded to 32 x 32, column-major) supplies the B fragments from
-      // smem, the V fragments come straight from L2 (next k-step prefetched), D goes back to HBM.
-      {
-        double* Q32 = Qs + (size_t)w2 * w2;   // [32][32] column-major, zero padded
-        for (int e = tid; e < 1024; e += BJ_THREADS) {
-          const int j = e >> 5, i = e & 31;
-          Q32[e] = (i < w2 && j < w2) ? Qs[(size_t)j * w2 + i] : 0.0;
-        }
-        __syncthreads();
-        const int r0 = warp * 32, fr = lane >> 2, fc = lane & 3;
-        if (r0 < k) {
-          // two passes of 16 output columns keep the accumulators at 16 doubles per lane
-#pragma unroll 1
-          for (int half = 0; half < 2; ++half) {
-            double acc[4][2][2];
-#pragma unroll
-            for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-              for (int nj = 0; nj < 2; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
-            double a_cur[4], a_nxt[4];
-            auto vload = [&](int kk, double (&a)[4]) {
-              const int slot = 4 * kk + fc;
-              const int gc = slot < w2 ? colid[slot] : -1;
-#pragma unroll
-              for (int mi = 0; mi < 4; ++mi) {
-                const int r = r0 + 8 * mi + fr;
-                a[mi] = (gc >= 0 && r < k) ? __ldcg(Vm + (size_t)gc * ldw + r) : 0.0;
-              }
-            };
-            vload(0, a_cur);
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-              if (kk + 1 < 8) vload(kk + 1, a_nxt);
-              double bq[2];
-#pragma unroll
-              for (int nj = 0; nj < 2; ++nj) bq[nj] = Q32[(size_t)(16 * half + 8 * nj + fr) * 32 + 4 * kk + fc];
-#pragma unroll
-              for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-                for (int nj = 0; nj < 2; ++nj) dmma884(acc[mi][nj][0], acc[mi][nj][1], a_cur[mi], bq[nj]);
-              if (kk + 1 < 8) {
-#pragma unroll
-                for (int mi = 0; mi < 4; ++mi) a_cur[mi] = a_nxt[mi];
-              }
-            }
-            // half 0 is staged in shared memory (pass 1 still reads the original V columns);
-            // half 1 goes straight to HBM (each warp touches only its own rows)
-            double* stage = Q32 + 1024;   // [16][k] column-major
-#pragma unroll
-            for (int nj = 0; nj < 2; ++nj)
-#pragma unroll
-              for (int e2 = 0; e2 < 2; ++e2) {
-                const int cl = 8 * nj + 2 * fc + e2, slot = 16 * half + cl;
-                const int gc = slot < w2 ? colid[slot] : -1;
-#pragma unroll
-                for (int mi = 0; mi < 4; ++mi) {
-                  const int r = r0 + 8 * mi + fr;
-                  if (r < k) {
-                    if (half == 0)
-                      stage[(size_t)cl * k + r] = acc[mi][nj][e2];
-                    else if (gc >= 0)
-                      Vm[(size_t)gc * ldw + r] = acc[mi][nj][e2];
-                  }
-                }
-              }
-          }
-          __syncwarp();
-          const double* stage = Q32 + 1024;
-          const int r = r0 + lane;
-#pragma unroll 4
-          for (int cl = 0; cl < 16; ++cl) {
-            const int gc = cl < w2 ? colid[cl] : -1;
-            if (gc >= 0 && r < k) Vm[(size_t)gc * ldw + r] = stage[(size_t)cl * k + r];
-          }
-        }
-      }
-      unsigned long long t2b = rec ? clock64() : 0;
-      // the cluster barrier's release/acquire orders the V stores for the other CTAs; only the
-      // TMA-issuing threads fence their (async-proxy) W stores
-      if (bulk && tid < w2) {
-        bulk_wait_all();
-        __threadfence();
-      }
-      if (rec) t3 = clock64();
-      cluster_sync_all();
-      if (rec) {
-        const unsigned long long t4 = clock64();
-        prof[0] += t1 - t0;   // load block pair
-        prof[1] += t2 - t1;   // inner sweep
-        prof[2] += t3 - t2;   // write back + V update
-        prof[3] += t4 - t3;   // cluster barrier
-        prof[4] += 1;
-        prof[5] += t2a - t2;  // W store issue
-        prof[6] += t2b - t2a; // V update (this thread's rows)
-      }
-    }
-    if (lane == 0 && my_rot) atomicAdd(&cta_rot, my_rot);
-    __syncthreads();
-    if (tid == 0 && cta_rot) atomicAdd(rot_count + (sweep & 1), cta_rot);
-    cluster_sync_all();
-    const unsigned int rc = *((volatile unsigned int*)(rot_count + (sweep & 1)));
-    if (c == 0 && tid == 0) rot_count[(sweep + 1) & 1] = 0;
-    cluster_sync_all();
-    if (rc == 0) {
-      ++sweep;
-      break;
-    }
-  }
-  if (c == 0 && tid == 0) *sweeps_out = sweep;
-}
-
-size_t jacobi_block_smem(int k) {
-  const int b = (k + 31) / 32;
-  // W pair + Q + the zero-padded 32 x 32 Q + the V staging half (16 x k)
-  return ((size_t)2 * b * k + (size_t)4 * b * b + 1024 + (size_t)16 * k) * sizeof(double);
-}
-
-cudaError_t jacobi_svd_block(double* W, double* V, int k, int ldw, double* S, double tol, int max_sweeps,
-                             unsigned int* scratch, int* sweeps_out, cudaStream_t s) {
-  const int b = (k + 31) / 32;
-  const size_t smem = jacobi_block_smem(k);
-  if (2 * b > 32 || smem > 220 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaMemsetAsync(scratch, 0, 8 * sizeof(unsigned int), s);
-  if (e != cudaSuccess) return e;
-  set_identity_kernel<<<148 * 4, 256, 0, s>>>(V, k, ldw);
-  note_launch();
-  static size_t configured = 0;
-  if (smem > configured) {
-    for (auto fn : {jacobi_block_kernel<false>, jacobi_block_kernel<true>}) {
-      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      if (e != cudaSuccess) return e;
-    }
-    configured = smem;
-  }
-  unsigned int* rot = scratch + 2;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(16, 1, 1);
-  cfg.blockDim = dim3(BJ_THREADS, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 16;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  static const bool prof_on = std::getenv("SSSVD_JACOBI_PROF") != nullptr;
-  static unsigned long long* dprof = nullptr;
-  if (prof_on && !dprof) {
-    cudaMalloc(&dprof, 8 * sizeof(unsigned long long));
-  }
-  if (prof_on) cudaMemsetAsync(dprof, 0, 8 * sizeof(unsigned long long), s);
-  if (prof_on)
-    e = cudaLaunchKernelEx(&cfg, jacobi_block_kernel<true>, W, V, k, ldw, b, tol, max_sweeps, rot, sweeps_out, dprof);
-  else
-    e = cudaLaunchKernelEx(&cfg, jacobi_block_kernel<false>, W, V, k, ldw, b, tol, max_sweeps, rot, sweeps_out,
-                           (unsigned long long*)nullptr);
-  if (e != cudaSuccess) return e;
-  note_launch();
-  if (prof_on) {
-    unsigned long long v[8];
-    cudaMemcpyAsync(v, dprof, sizeof(v), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    if (v[4]) std::fprintf(stderr, "[sssvd] block jacobi k=%d cycles/outer round: load+V %llu inner %llu store+V %llu (issue %llu, V %llu) barrier %llu\n",
-                           k, v[0] / v[4], v[1] / v[4], v[2] / v[4], v[5] / v[4], v[6] / v[4], v[3] / v[4]);
-  }
-  jacobi_finish_kernel<<<k, 256, 0, s>>>(W, k, ldw, S);
-  note_launch();
-  return cudaGetLastError();
-}
-
-}  // namespace sssvd_gpu
-
-namespace sssvd_gpu {
-
 // ----------------------------------------------------------------------------- grid block Jacobi
-// Block one-sided Jacobi for k > 512 (the tail's k x k factors of configs 3 and 5: k = 1024,
-// 2048) on the whole GPU. Same cyclic block ordering as jacobi_block_kernel (outer tournament over
-// nb blocks of b columns; round 0 of a sweep runs the full inner sweep of each block pair, later
-// rounds only the b x b cross pairs), but the block pairs are spread over one persistent CTA per
-// SM and outer rounds are separated by the software grid barrier. b is the widest block whose
+// Block one-sided Jacobi (every k from 64 to 2048: the tail's k x k factors of configs 1-5) on the
+// whole GPU. Cyclic block ordering: an outer tournament over nb blocks of b columns; round 0 of a
+// sweep runs the full inner sweep of each block pair, later rounds only the b x b cross pairs. The
+// block pairs are spread over one persistent CTA per SM and outer rounds are separated by the software grid barrier. b is the widest block whose
 // pair fits shared memory, up to one warp per resident column (k = 2048: b = 7, 147 pairs on
 // 148 SMs, 229 KB; k = 1024: b = 8, 64 pairs): nb - 1 grid barriers per sweep instead of the
 // scalar kernel's k - 1, and the column traffic of the inner rounds stays on chip.
@@ -1067,7 +677,7 @@ cudaError_t jacobi_svd_grid_block(double* W, double* V, int k, int ldw, double* 
                                           : (const void*)jacobi_grid_block_kernel<32, false>)
                                : (prof_on ? (const void*)jacobi_grid_block_kernel<64, true>
                                           : (const void*)jacobi_grid_block_kernel<64, false>);
-  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  e = set_kernel_smem(fn, smem, false);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, GB_THREADS, smem);

@@ -8,6 +8,8 @@
 namespace sssvd_gpu {
 
 cudaError_t cuda_fail(cudaError_t e, const char* expr, const char* file, int line);
+// per-(kernel, device) dynamic shared-memory / non-portable cluster attributes (zgemm.cu)
+cudaError_t set_kernel_smem(const void* fn, size_t bytes, bool nonportable_cluster);
 
 // instrumentation: every launcher bumps the launch counter; when profiling is on, zgemm_sub
 // brackets each launch with CUDA events on its stream (the dominant kernel's live timing)
@@ -33,61 +35,47 @@ cudaError_t assemble(const double* G, int n, int ldg, const double* V, int L, co
 cudaError_t load_rhs(const double* V, int n, int L, double2* out, int ld, long long stride, int batch, cudaStream_t s);
 // K2 leaf panel LU (lu.cu): rows [r0, n) x cols [r0, r0+w), W in {8,16,32}
 size_t leaf_smem_bytes(int n, int W, int cluster);
-cudaError_t leaf_lu(double2* mats, int ld, long long stride, int n, int r0, int w, int W, int cluster,
-                    int* ipiv, int batch, cudaStream_t s);
-// K2 v2 (lu.cu): register-resident leaf; variant 0: W32 (<=256 rows/CTA), 1: W16 (<=512), 2: W8 (<=1024)
-int leaf_v2_rows_per_cta(int variant);
-int leaf_v2_width(int variant);
-cudaError_t leaf_lu_v2(double2* mats, int ld, long long stride, int n, int r0, int w, int variant, int cluster,
-                       int* ipiv, int batch, cudaStream_t s);
-void leaf_profile_read(unsigned long long* out5, bool reset);
-// K2 v3 (lu.cu): shared-memory slab with thread-owned rows (same smem sizing as v1)
-cudaError_t leaf_lu_v3(double2* mats, int ld, long long stride, int n, int r0, int w, int W, int cluster, int* ipiv,
+// K2 (lu.cu): cluster leaf LU; cb < r0: the leaf also applies its interchanges to columns [cb, r0)
+cudaError_t leaf_lu(double2* mats, int ld, long long stride, int n, int r0, int w, int W, int cluster, int* ipiv,
                        int batch, cudaStream_t s, int cb);
-// K3/K4 (lu.cu): interchanges ipiv[r0..r0+np) on columns [c0,c1), then optional unit-lower TRSM
-cudaError_t swap_trsm(double2* mats, int ld, long long stride, int n, int r0, int np, int c0, int c1,
-                      const int* ipiv, bool do_trsm, int batch, cudaStream_t s);
-// K6 (lu.cu): rows r0..r0+np of columns [c0,c1) <- U11^{-1} (.)
-cudaError_t trsm_upper(double2* mats, int ld, long long stride, int r0, int np, int c0, int c1,
-                       int batch, cudaStream_t s);
 cudaError_t pivot_floor(const double2* mats, int ld, long long stride, int n, const double2* shifts,
                         const double* gmax, int* status, double* minpiv, int batch, cudaStream_t s);
 // K5 (zgemm.cu): C -= A B, row-major complex, batched
 cudaError_t zgemm_sub(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B,
                       int ldb, long long sB, double2* C, int ldc, long long sC, int batch,
                       cudaStream_t stream);
-// warp-tile variant of the GEMMs (zgemm.cu); < 0 re-reads SSSVD_ZGEMM_V
-void zgemm_set_variant(int v);
 // C = A B[brow[k], :] (row-gathered B), row-major complex, batched (zgemm.cu)
 cudaError_t zgemm_set_gather(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B,
                              int ldb, long long sB, const int* brow, int sR, double2* C, int ldc, long long sC,
                              int batch, cudaStream_t stream);
-// interchange map, L11^{-1}, scatter+copy, warp back substitution (lu.cu)
-cudaError_t build_moves(const int* ipiv, int n, int r0, int np, int* src, int* disp, int stride, int batch,
-                        cudaStream_t s);
-// back-substitution kernel choice: 0 shared-memory staged (default), 1 warp-streamed (lu.cu)
-int trsm_variant();
-// leaf_lu_v3 applies its interchanges to the block columns [cb, r0) itself (lu.cu); false: the
-// caller launches swap_trsm
-bool leaf_swap_fused();
-// panel_prep form: 0 staged 8-warp (default), 1 the 4-warp ballot form (lu.cu)
-int panel_prep_variant();
-// build_moves + trinv_lower fused into one launch (lu.cu)
+// K3/K4 (lu.cu): the panel's interchange map + L11^{-1} in one launch
 cudaError_t panel_prep(const double2* mats, int ld, long long stride, int r0, int np, double2* linv, long long lstride,
                        const int* ipiv, int n, int* src, int* disp, int dstride, int batch, cudaStream_t s);
-cudaError_t trinv_lower(const double2* mats, int ld, long long stride, int r0, int np, double2* linv,
-                        long long lstride, int batch, cudaStream_t s);
 cudaError_t scatter_copy(double2* mats, int ld, long long stride, int r0, int np, int c0, int c1, const int* disp,
                          int dstride, const double2* T, int ldt, long long tstride, int batch, cudaStream_t s);
-cudaError_t trsm_upper_warp(double2* mats, int ld, long long stride, int r0, int np, int c0, int c1, int batch,
+// K6 (lu.cu): rows r0..r0+np of columns [c0, c1) <- U11^{-1} (.), shared-memory staged
+cudaError_t trsm_upper_blocks(double2* mats, int ld, long long stride, int r0, int np, int c0, int c1, int batch,
                             cudaStream_t s);
+// Tail GEMMs on DMMA (dgemm.cu), column-major: C (m x n) = alpha op(A) B + beta C with op(A) = A
+// (m x k) or A^T (A stored k x m). Deep-K skinny outputs split K into `work` (reduced in fixed order)
+// when work_elems allows; deterministic.
+int dgemm_split_count(int m, int n, int k, size_t work_elems);
+cudaError_t dgemm(bool ta, int m, int n, int k, double alpha, const double* A, int lda, const double* B, int ldb,
+                  double beta, double* C, int ldc, double* work, size_t work_elems, cudaStream_t s);
+// out[j] = || op(A) B[:, j] - d[j] V[:, j] ||_2, fused epilogue; part: dgemm_norm_scratch(m, n) doubles
+size_t dgemm_norm_scratch(int m, int n);
+cudaError_t dgemm_colnorm_diff(bool ta, int m, int n, int k, const double* A, int lda, const double* B, int ldb,
+                               const double* d, const double* V, int ldv, double* out, double* part, cudaStream_t s);
+// out (cols x rows) = in^T, column-major (dgemm.cu)
+cudaError_t transpose(const double* in, int rows, int cols, int ldi, double* out, int ldo, cudaStream_t s);
+// sgn[j] = sign(U[:, j] . V[:, j]) for rows x cols column-major U, V (dgemm.cu)
+cudaError_t col_dot_sign(const double* U, const double* V, int rows, int cols, double* sgn, cudaStream_t s);
+// h <- (h + h^T) / 2 in place (dgemm.cu)
+cudaError_t symmetrize(double* h, int k, int ldh, cudaStream_t s);
 // one-sided Jacobi SVD (jacobi_svd.cu): W (k x k, in) -> W = U (unsorted), V, S = sigma
 cudaError_t jacobi_svd(double* W, double* V, int k, int ldw, double* S, double tol, int max_sweeps,
                        unsigned int* scratch, int* sweeps_out, cudaStream_t s);
-cudaError_t jacobi_svd_block(double* W, double* V, int k, int ldw, double* S, double tol, int max_sweeps,
-                             unsigned int* scratch, int* sweeps_out, cudaStream_t s);
-size_t jacobi_block_smem(int k);
-// k > 512: block Jacobi over the whole GPU (one block pair per SM per outer round)
+// 64 <= k <= 2048: block Jacobi over the whole GPU (one block pair per SM per outer round)
 cudaError_t jacobi_svd_grid_block(double* W, double* V, int k, int ldw, double* S, double tol, int max_sweeps,
                                   unsigned int* scratch, int* sweeps_out, cudaStream_t s);
 bool jacobi_grid_block_plan(int k, int sms, int* b, int* nbe, int* rpl, size_t* smem);

@@ -9,8 +9,6 @@
 //   step 5    : svd_small + assemble_triplets        |  (plain library QR/SVD/GEMM), the
 //   postproc. : tau, residual estimate, exact, Galerkin residual norms on the residual kernel
 // There is no CPU fallback: every numerical step runs on the GPU.
-#include <cublas_v2.h>
-#include <cusolverDn.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -49,16 +47,6 @@ struct Status : std::runtime_error {
     if (_e != cudaSuccess)                                                                       \
       throw Status(_e == cudaErrorMemoryAllocation ? SSSVD_E_OOM : SSSVD_E_CUDA,                 \
                    std::string(#expr) + ": " + cudaGetErrorString(_e));                          \
-  } while (0)
-#define CKB(expr)                                                                                \
-  do {                                                                                           \
-    cublasStatus_t _s = (expr);                                                                  \
-    if (_s != CUBLAS_STATUS_SUCCESS) throw Status(SSSVD_E_CUDA, std::string(#expr) + " failed"); \
-  } while (0)
-#define CKS(expr)                                                                                \
-  do {                                                                                           \
-    cusolverStatus_t _s = (expr);                                                                \
-    if (_s != CUSOLVER_STATUS_SUCCESS) throw Status(SSSVD_E_CUDA, std::string(#expr) + " failed"); \
   } while (0)
 #define CKN(expr)                                                                                \
   do {                                                                                           \
@@ -145,13 +133,12 @@ struct TailProf {
 using namespace sssvd_gpu;
 
 enum TailBuf { T_SC, T_Q, T_R, T_UR, T_VR, T_SV, T_US1, T_QM, T_LEFT, T_RIGHT, T_PERM, T_UT, T_BM, T_PM, T_PHI,
-               T_QS, T_SIG, T_PS, T_QSC, T_COEFF, T_X, T_IMG, T_NRM, T_INV, T_TAU, T_Y, T_CNP, T_COUNT };
+               T_QS, T_SIG, T_PS, T_QSC, T_COEFF, T_X, T_IMG, T_NRM, T_INV, T_TAU, T_Y, T_CNP, T_EU, T_EV, T_ES,
+               T_COUNT };
 
 struct sssvd_gpu_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
-  cublasHandle_t blas = nullptr;
-  cusolverDnHandle_t solver = nullptr;
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
   int max_batch = 0;
@@ -161,7 +148,7 @@ struct sssvd_gpu_ctx {
   bool transposed = false;
   bool has_gram = false;
   DBuf A, G, gmax, mats, ipiv, shifts, coef, S, V, status, minpiv, scratch;
-  DBuf t0, t1, t2, t7, work, info;
+  DBuf t0, t1, t2, t7, gwork;
   DBuf lw_linv, lw_T, lw_src, lw_disp, lw2_linv, lw2_T, lw2_src, lw2_disp, jscr, jperm, jq, jr, jj, qy, qt, qw;
   // factor cache (moments.hpp:106-116): the last pass left shifts [fact_jb, fact_je) factored in
   // one resident batch of `mats`, so a later pass with the same operator/shifts/L only replays the
@@ -270,7 +257,6 @@ namespace sssvd_gpu {
 // ----------------------------------------------------------------------------- LU driver
 struct LuPlan {
   int n, L, ld, NB, W, cluster;
-  int leaf_variant;   // >= 0: register-resident leaf_lu_v2 variant; -1: shared-memory leaf (v1)
   long long stride;
 };
 
@@ -320,26 +306,6 @@ static LuPlan make_plan(int n, int L) {
       p.cluster = c;
     }
   }
-  // register-resident leaf (v2): rows per CTA <= threads x rows-per-thread of the variant
-  p.leaf_variant = -1;
-  // default: shared-memory leaf (v1); the register-resident v2 needs a whole SM register file
-  // per CTA and its 8-CTA clusters do not reliably co-schedule (measured erratic), so opt-in
-  static const char* leaf_env = std::getenv("SSSVD_LEAF");
-  if (leaf_env && std::string(leaf_env) == "v2") {
-    for (int v = 0; v < 3 && p.leaf_variant < 0; ++v)
-      for (int c = 1; c <= 8; c *= 2)
-        if ((n + c - 1) / c <= leaf_v2_rows_per_cta(v)) {
-          p.leaf_variant = v;
-          p.cluster = c;
-          p.W = leaf_v2_width(v);
-          break;
-        }
-    if (p.leaf_variant < 0 && (n + 15) / 16 <= leaf_v2_rows_per_cta(2)) {
-      p.leaf_variant = 2;
-      p.cluster = 16;
-      p.W = leaf_v2_width(2);
-    }
-  }
   return p;
 }
 
@@ -361,13 +327,7 @@ static void apply_panel(const LuPlan& P, const LuWork& W, double2* mats, const i
                         cudaEvent_t ev_done = nullptr) {
   const int n = P.n, N = c1 - c0;
   if (N <= 0) return;
-  static const bool split_prep = std::getenv("SSSVD_SPLIT_PREP") != nullptr;   // measurement: two launches
-  if (split_prep) {
-    CK(build_moves(ipiv, n, r0, np, W.src, W.disp, P.NB, nb, s));
-    CK(trinv_lower(mats, P.ld, P.stride, r0, np, W.linv, (long long)P.NB * P.NB, nb, s));
-  } else {
-    CK(panel_prep(mats, P.ld, P.stride, r0, np, W.linv, (long long)P.NB * P.NB, ipiv, n, W.src, W.disp, P.NB, nb, s));
-  }
+  CK(panel_prep(mats, P.ld, P.stride, r0, np, W.linv, (long long)P.NB * P.NB, ipiv, n, W.src, W.disp, P.NB, nb, s));
   CK(zgemm_set_gather(np, N, np, W.linv, np, (long long)P.NB * P.NB, mats + c0, P.ld, P.stride, W.src, P.NB, W.T, N,
                       W.tstride, nb, s));
   CK(scatter_copy(mats, P.ld, P.stride, r0, np, c0, c1, W.disp, P.NB, W.T, N, W.tstride, nb, s));
@@ -399,20 +359,8 @@ static void factor_rec(const LuPlan& P, const LuWork& W, double2* mats, int* ipi
                        int w, int cb) {
   const int n = P.n;
   if (w <= P.W) {
-    static const char* leaf_env = std::getenv("SSSVD_LEAF");
-    static const bool use_v1 = leaf_env && std::string(leaf_env) == "v1";
-    if (P.leaf_variant >= 0)
-      CK(leaf_lu_v2(mats, P.ld, P.stride, n, c0, w, P.leaf_variant, P.cluster, ipiv, nb, s));
-    else if (use_v1)
-      CK(leaf_lu(mats, P.ld, P.stride, n, c0, w, P.W, P.cluster, ipiv, nb, s));
-    else if (leaf_swap_fused()) {
-      // the leaf applies its interchanges to the block columns [cb, c0) in its own epilogue
-      CK(leaf_lu_v3(mats, P.ld, P.stride, n, c0, w, P.W, P.cluster, ipiv, nb, s, cb));
-      return;
-    } else {
-      CK(leaf_lu_v3(mats, P.ld, P.stride, n, c0, w, P.W, P.cluster, ipiv, nb, s, c0));
-    }
-    if (c0 > cb) CK(swap_trsm(mats, P.ld, P.stride, n, c0, w, cb, c0, ipiv, false, nb, s));
+    // the leaf applies its interchanges to the block columns [cb, c0) in its own epilogue
+    CK(leaf_lu(mats, P.ld, P.stride, n, c0, w, P.W, P.cluster, ipiv, nb, s, cb));
     return;
   }
   int wl = ((w / 2) + P.W - 1) / P.W * P.W;
@@ -429,7 +377,7 @@ static void back_substitute(const LuPlan& P, double2* mats, int nb, cudaStream_t
   const int nblocks = (n + P.NB - 1) / P.NB;
   for (int bi = nblocks - 1; bi >= 0; --bi) {
     const int kb = bi * P.NB, nbk = std::min(P.NB, n - kb);
-    CK(trsm_upper_warp(mats, P.ld, P.stride, kb, nbk, n, ncols, nb, s));
+    CK(trsm_upper_blocks(mats, P.ld, P.stride, kb, nbk, n, ncols, nb, s));
     if (kb > 0)
       CK(zgemm_sub(kb, P.L, nbk, mats + kb, P.ld, P.stride, mats + (size_t)kb * P.ld + n, P.ld, P.stride,
                    mats + n, P.ld, P.stride, nb, s));
@@ -476,7 +424,7 @@ static void lu_solve_groups(const LuPlan& P, std::vector<LuGroup>& G) {
   for (int bi = nblocks - 1; bi >= 0; --bi) {
     const int kb = bi * P.NB, nbk = std::min(P.NB, n - kb);
     for (auto& g : G) {
-      CK(trsm_upper_warp(g.mats, P.ld, P.stride, kb, nbk, n, ncols, g.nb, g.s));
+      CK(trsm_upper_blocks(g.mats, P.ld, P.stride, kb, nbk, n, ncols, g.nb, g.s));
       if (kb > 0)
         CK(zgemm_sub(kb, P.L, nbk, g.mats + kb, P.ld, P.stride, g.mats + (size_t)kb * P.ld + n, P.ld, P.stride,
                      g.mats + n, P.ld, P.stride, g.nb, g.s));
@@ -515,7 +463,7 @@ static void lu_solve_groups_lookahead(const LuPlan& P, std::vector<LuGroup>& G) 
   for (int bi = nblocks - 1; bi >= 0; --bi) {
     const int kb = bi * P.NB, nbk = std::min(P.NB, n - kb);
     for (auto& g : G) {
-      CK(trsm_upper_warp(g.mats, P.ld, P.stride, kb, nbk, n, ncols, g.nb, g.s));
+      CK(trsm_upper_blocks(g.mats, P.ld, P.stride, kb, nbk, n, ncols, g.nb, g.s));
       if (kb > 0)
         CK(zgemm_sub(kb, P.L, nbk, g.mats + kb, P.ld, P.stride, g.mats + (size_t)kb * P.ld + n, P.ld, P.stride,
                      g.mats + n, P.ld, P.stride, g.nb, g.s));
@@ -683,10 +631,10 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
     } else {
       const std::vector<uintptr_t> key = {
           (uintptr_t)n, (uintptr_t)L, (uintptr_t)M, (uintptr_t)nb, (uintptr_t)ng, (uintptr_t)P.NB, (uintptr_t)P.W,
-          (uintptr_t)P.cluster, (uintptr_t)(P.leaf_variant + 1), (uintptr_t)P.ld, (uintptr_t)ctx->G.p,
+          (uintptr_t)P.cluster, (uintptr_t)P.ld, (uintptr_t)ctx->G.p,
           (uintptr_t)V_dev, (uintptr_t)mats, (uintptr_t)ipiv, (uintptr_t)work.linv, (uintptr_t)work.T,
           (uintptr_t)work.src, (uintptr_t)work.disp, (uintptr_t)dshift, (uintptr_t)dcoef, (uintptr_t)S_dev,
-          (uintptr_t)ctx->gmax.p, (uintptr_t)dstatus, (uintptr_t)dmin, (uintptr_t)lookahead, (uintptr_t)trsm_variant(), (uintptr_t)leaf_swap_fused(), (uintptr_t)panel_prep_variant(),
+          (uintptr_t)ctx->gmax.p, (uintptr_t)dstatus, (uintptr_t)dmin, (uintptr_t)lookahead,
           (uintptr_t)work2.linv, (uintptr_t)work2.T, (uintptr_t)work2.src, (uintptr_t)work2.disp};
       for (auto& g : ctx->lu_graphs)
         if (g.key == key) replayed = &g;
@@ -820,12 +768,14 @@ static void ensure_gram(sssvd_gpu_ctx* ctx, int64_t cap) {
 }
 
 // ----------------------------------------------------------------------------- dense tail helpers
-// column-major helpers on ctx->stream via cuBLAS/cuSOLVER (round-1 interim for QR / SVD)
-static void dgemm(sssvd_gpu_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* A,
-                  int lda, const double* B, int ldb, double beta, double* C, int ldc) {
+// column-major C = alpha op(A) B + beta C on ctx->stream (dgemm.cu: DMMA, split-K through the
+// context's GEMM workspace for deep skinny products)
+static constexpr size_t kGemmWork = (size_t)4 << 20;   // doubles (32 MB)
+static void dgemm(sssvd_gpu_ctx* ctx, bool ta, int m, int n, int k, double alpha, const double* A, int lda,
+                  const double* B, int ldb, double beta, double* C, int ldc) {
   if (m <= 0 || n <= 0) return;
-  CKB(cublasDgemm(ctx->blas, ta ? CUBLAS_OP_T : CUBLAS_OP_N, tb ? CUBLAS_OP_T : CUBLAS_OP_N, m, n, k, &alpha, A,
-                  lda, B, ldb, &beta, C, ldc));
+  double* work = ctx->gwork.as<double>(kGemmWork);
+  CK(sssvd_gpu::dgemm(ta, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, work, kGemmWork, ctx->stream));
 }
 
 // thin QR: A (m x k, lda=m) is overwritten by Q; R (k x k upper, ldr = k) returned
@@ -877,16 +827,16 @@ static void thin_qr(sssvd_gpu_ctx* ctx, double* A, int m, int k, double* R) {
         CK(qr_panel(A, m, m, j, wp, Y + (size_t)j * m + j, m, T + (size_t)p * 1024, tau + j, s));
       if (ntb > 0) {
         // inside the outer block: A[j:m, j+wp:jb+kb] -= Y (T^T (Y^T A[j:m, j+wp:jb+kb]))
-        dgemm(ctx, true, false, wp, ntb, mp, 1.0, Y + (size_t)j * m + j, m, A + (size_t)(j + wp) * m + j, m, 0.0, Wt, wp);
-        dgemm(ctx, true, false, wp, ntb, wp, 1.0, T + (size_t)p * 1024, 32, Wt, wp, 0.0, W2, wp);
-        dgemm(ctx, false, false, mp, ntb, wp, -1.0, Y + (size_t)j * m + j, m, W2, wp, 1.0,
+        dgemm(ctx, true, wp, ntb, mp, 1.0, Y + (size_t)j * m + j, m, A + (size_t)(j + wp) * m + j, m, 0.0, Wt, wp);
+        dgemm(ctx, true, wp, ntb, wp, 1.0, T + (size_t)p * 1024, 32, Wt, wp, 0.0, W2, wp);
+        dgemm(ctx, false, mp, ntb, wp, -1.0, Y + (size_t)j * m + j, m, W2, wp, 1.0,
               A + (size_t)(j + wp) * m + j, m);
       }
     }
     double* Yb = Y + (size_t)jb * m + jb;
     double* Tbb = Tb + (size_t)(jb / NBO) * NBO * NBO;
     if (kb > w) {
-      dgemm(ctx, true, false, kb, kb, mb, 1.0, Yb, m, Yb, m, 0.0, Gb, kb);
+      dgemm(ctx, true, kb, kb, mb, 1.0, Yb, m, Yb, m, 0.0, Gb, kb);
       CK(larft(Gb, kb, tau + jb, Tbb, s));
     }
     const int nt = k - jb - kb;
@@ -894,9 +844,9 @@ static void thin_qr(sssvd_gpu_ctx* ctx, double* A, int m, int k, double* R) {
       // trailing columns: A[jb:m, jb+kb:k] -= Y_b (T_b^T (Y_b^T A[jb:m, jb+kb:k]))
       const double* Tuse = kb > w ? Tbb : T + (size_t)(jb / w) * 1024;
       const int ldt = kb > w ? kb : 32;
-      dgemm(ctx, true, false, kb, nt, mb, 1.0, Yb, m, A + (size_t)(jb + kb) * m + jb, m, 0.0, Wt, kb);
-      dgemm(ctx, true, false, kb, nt, kb, 1.0, Tuse, ldt, Wt, kb, 0.0, W2, kb);
-      dgemm(ctx, false, false, mb, nt, kb, -1.0, Yb, m, W2, kb, 1.0, A + (size_t)(jb + kb) * m + jb, m);
+      dgemm(ctx, true, kb, nt, mb, 1.0, Yb, m, A + (size_t)(jb + kb) * m + jb, m, 0.0, Wt, kb);
+      dgemm(ctx, true, kb, nt, kb, 1.0, Tuse, ldt, Wt, kb, 0.0, W2, kb);
+      dgemm(ctx, false, mb, nt, kb, -1.0, Yb, m, W2, kb, 1.0, A + (size_t)(jb + kb) * m + jb, m);
     }
   }
   CK(copy_r(A, m, k, R, s));
@@ -907,9 +857,9 @@ static void thin_qr(sssvd_gpu_ctx* ctx, double* A, int m, int k, double* R) {
     double* Yb = Y + (size_t)jb * m + jb;
     const double* Tuse = kb > w ? Tb + (size_t)(jb / NBO) * NBO * NBO : T + (size_t)(jb / w) * 1024;
     const int ldt = kb > w ? kb : 32;
-    dgemm(ctx, true, false, kb, nq, mb, 1.0, Yb, m, A + (size_t)jb * m + jb, m, 0.0, Wt, kb);
-    dgemm(ctx, false, false, kb, nq, kb, 1.0, Tuse, ldt, Wt, kb, 0.0, W2, kb);
-    dgemm(ctx, false, false, mb, nq, kb, -1.0, Yb, m, W2, kb, 1.0, A + (size_t)jb * m + jb, m);
+    dgemm(ctx, true, kb, nq, mb, 1.0, Yb, m, A + (size_t)jb * m + jb, m, 0.0, Wt, kb);
+    dgemm(ctx, false, kb, nq, kb, 1.0, Tuse, ldt, Wt, kb, 0.0, W2, kb);
+    dgemm(ctx, false, mb, nq, kb, -1.0, Yb, m, W2, kb, 1.0, A + (size_t)jb * m + jb, m);
   }
 }
 
@@ -942,89 +892,73 @@ struct CopyFence {
 };
 
 static void svd_square(sssvd_gpu_ctx* ctx, double* B, int k, double* U, double* S, double* V) {
-  static const char* env = std::getenv("SSSVD_TAIL_SVD");
-  const std::string method = env ? env : "jacobi";
-  if (method == "jacobi" || method == "jacobi_n") {
-    // hand-written one-sided Jacobi (jacobi_svd.cu); columns sorted by nonincreasing sigma.
-    // Default: Jacobi on B^T (B is triangular: the transposed factor converges in far fewer
-    // sweeps, the dgejsv preconditioning idea): B^T Q = W = V_B S, so U_B = Q, V_B = W S^-1.
-    const bool transposed = method == "jacobi";
-    unsigned int* scr = static_cast<unsigned int*>(ctx->jscr.get(64));
-    int* sweeps = reinterpret_cast<int*>(scr + 8);
-    const double tol = (double)k * 2.220446049250313e-16;   // cosine noise is ~sqrt(k) eps
-    if (transposed) {
-      // dgejsv-style preconditioning: B^T = Q2 R2 (QR), one-sided Jacobi on X = R2^T (lower
-      // triangular, nearly orthogonal columns): X J = W = U S  =>  B = R2^T Q2^T = U S (Q2 J)^T,
-      // so U_B = W S^{-1} and V_B = Q2 J.
-      const double one = 1.0, zero = 0.0;
-      double* Q2 = ctx->jq.as<double>((size_t)k * k);
-      double* R2 = ctx->jr.as<double>((size_t)k * k);
-      CKB(cublasDgeam(ctx->blas, CUBLAS_OP_T, CUBLAS_OP_N, k, k, &one, B, k, &zero, Q2, k, Q2, k));
-      thin_qr(ctx, Q2, k, k, R2);                     // Q2 <- Q, R2 <- R of B^T
-      CKB(cublasDgeam(ctx->blas, CUBLAS_OP_T, CUBLAS_OP_N, k, k, &one, R2, k, &zero, U, k, U, k));   // X = R2^T
-      double* J = ctx->jj.as<double>((size_t)k * k);
-      cudaEvent_t je0 = nullptr, je1 = nullptr;
-      const bool dbg = std::getenv("SSSVD_DEBUG") != nullptr;
-      if (dbg) {
-        cudaEventCreate(&je0);
-        cudaEventCreate(&je1);
-        cudaEventRecord(je0, ctx->stream);
-      }
-      // default: the grid-wide block Jacobi (one block pair per SM per outer round); the
-      // one-cluster block kernel (SSSVD_JACOBI=cluster, k <= 512) and the scalar grid kernel
-      // (SSSVD_JACOBI=scalar, also the fallback where no block plan fits) stay selectable
-      static const char* jb = std::getenv("SSSVD_JACOBI");
-      const std::string jmode = jb ? jb : "";
-      const bool use_block = jmode == "cluster" && k <= 512 && k >= 64 && jacobi_block_smem(k) <= 220 * 1024;
-      int gb_b, gb_nbe, gb_rpl;
-      size_t gb_smem;
-      int sms = 148;
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-      const bool use_grid_block = !use_block && jmode != "scalar" &&
-                                  jacobi_grid_block_plan(k, sms, &gb_b, &gb_nbe, &gb_rpl, &gb_smem);
-      if (use_block)
-        CK(jacobi_svd_block(U, J, k, k, S, tol, 60, scr, sweeps, ctx->stream));
-      else if (use_grid_block)
-        CK(jacobi_svd_grid_block(U, J, k, k, S, tol, 60, scr, sweeps, ctx->stream));
-      else
-        CK(jacobi_svd(U, J, k, k, S, tol, 60, scr, sweeps, ctx->stream));   // U <- W S^-1, S
-      if (dbg) {
-        cudaEventRecord(je1, ctx->stream);
-        cudaEventSynchronize(je1);
-        float ms = 0;
-        cudaEventElapsedTime(&ms, je0, je1);
-        std::fprintf(stderr, "[sssvd] jacobi kernel %.2f ms\n", ms);
-        cudaEventDestroy(je0);
-        cudaEventDestroy(je1);
-      }
-      CKB(cublasDgemm(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_N, k, k, k, &one, Q2, k, J, k, &zero, V, k));
-    } else {
-      CK(cudaMemcpyAsync(U, B, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, ctx->stream));
-      CK(jacobi_svd(U, V, k, k, S, tol, 60, scr, sweeps, ctx->stream));
-    }
-    std::vector<double> sv = d2h(S, k, ctx->stream);
-    if (std::getenv("SSSVD_DEBUG")) {
-      int hs = 0;
-      CK(cudaMemcpy(&hs, sweeps, sizeof(int), cudaMemcpyDeviceToHost));
-      std::fprintf(stderr, "[sssvd] jacobi_svd k=%d sweeps=%d\n", k, hs);
-    }
-    std::vector<int> order(k);
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return sv[a] > sv[b]; });
-    std::vector<double> sorted(k);
-    for (int i = 0; i < k; ++i) sorted[i] = sv[order[i]];
-    int* perm = static_cast<int*>(ctx->jperm.get(sizeof(int) * k));
-    double* tmp = ctx->t7.as<double>((size_t)k * k + 64);
-    CK(cudaMemcpyAsync(perm, order.data(), sizeof(int) * k, cudaMemcpyHostToDevice, ctx->stream));
-    CK(gather_cols(U, k, perm, nullptr, k, k, tmp, k, ctx->stream));
-    CK(cudaMemcpyAsync(U, tmp, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, ctx->stream));
-    CK(gather_cols(V, k, perm, nullptr, k, k, tmp, k, ctx->stream));
-    CK(cudaMemcpyAsync(V, tmp, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, ctx->stream));
-    CK(cudaMemcpyAsync(S, sorted.data(), sizeof(double) * k, cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    return;
-  }
-  throw Status(SSSVD_E_INVALID_ARGUMENT, "SSSVD_TAIL_SVD: unknown method (jacobi | jacobi_n)");
+  // hand-written one-sided Jacobi (jacobi_svd.cu) with dgejsv-style preconditioning: B^T = Q2 R2
+  // (QR), one-sided Jacobi on X = R2^T (lower triangular, nearly orthogonal columns: far fewer
+  // sweeps than on B itself): X J = W = U S  =>  B = R2^T Q2^T = U S (Q2 J)^T, so U_B = W S^{-1}
+  // and V_B = Q2 J. Columns sorted by nonincreasing sigma (stable).
+  cudaStream_t st = ctx->stream;
+  unsigned int* scr = static_cast<unsigned int*>(ctx->jscr.get(64));
+  int* sweeps = reinterpret_cast<int*>(scr + 8);
+  const double tol = (double)k * 2.220446049250313e-16;   // cosine noise is ~sqrt(k) eps
+  double* Q2 = ctx->jq.as<double>((size_t)k * k);
+  double* R2 = ctx->jr.as<double>((size_t)k * k);
+  CK(transpose(B, k, k, k, Q2, k, st));
+  thin_qr(ctx, Q2, k, k, R2);                     // Q2 <- Q, R2 <- R of B^T
+  CK(transpose(R2, k, k, k, U, k, st));           // X = R2^T
+  double* J = ctx->jj.as<double>((size_t)k * k);
+  // the grid-wide block Jacobi (one block pair per SM per outer round) where a block plan fits
+  // (64 <= k <= 2048), else the scalar round-robin kernel
+  int gb_b, gb_nbe, gb_rpl;
+  size_t gb_smem;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  if (jacobi_grid_block_plan(k, sms, &gb_b, &gb_nbe, &gb_rpl, &gb_smem))
+    CK(jacobi_svd_grid_block(U, J, k, k, S, tol, 60, scr, sweeps, st));
+  else
+    CK(jacobi_svd(U, J, k, k, S, tol, 60, scr, sweeps, st));   // U <- W S^-1, S
+  dgemm(ctx, false, k, k, k, 1.0, Q2, k, J, k, 0.0, V, k);
+  std::vector<double> sv = d2h(S, k, st);
+  std::vector<int> order(k);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return sv[a] > sv[b]; });
+  std::vector<double> sorted(k);
+  for (int i = 0; i < k; ++i) sorted[i] = sv[order[i]];
+  int* perm = static_cast<int*>(ctx->jperm.get(sizeof(int) * k));
+  double* tmp = ctx->t7.as<double>((size_t)k * k + 64);
+  CK(cudaMemcpyAsync(perm, order.data(), sizeof(int) * k, cudaMemcpyHostToDevice, st));
+  CK(gather_cols(U, k, perm, nullptr, k, k, tmp, k, st));
+  CK(cudaMemcpyAsync(U, tmp, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, st));
+  CK(gather_cols(V, k, perm, nullptr, k, k, tmp, k, st));
+  CK(cudaMemcpyAsync(V, tmp, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(S, sorted.data(), sizeof(double) * k, cudaMemcpyHostToDevice, st));
+  CK(cudaStreamSynchronize(st));
+}
+
+// Symmetric eigendecomposition H = Q diag(theta) Q^T (theta ascending), standing in for
+// Eigen::SelfAdjointEigenSolver in naive_eigen_route (extract.hpp:114). H (k x k, destroyed) is
+// symmetric, so its SVD is U = Q sign(Lambda), V = Q, S = |Lambda|: theta_i = s_i sign(u_i . v_i)
+// and the eigenvectors are the right singular vectors, reordered by ascending theta (stable).
+static std::vector<double> sym_eig(sssvd_gpu_ctx* ctx, double* H, int k, double* Qout) {
+  cudaStream_t st = ctx->stream;
+  double* U = ctx->tail[T_EU].as<double>((size_t)k * k);
+  double* V = ctx->tail[T_EV].as<double>((size_t)k * k);
+  double* S = ctx->tail[T_ES].as<double>(k);
+  svd_square(ctx, H, k, U, S, V);
+  double* sgn = ctx->t2.as<double>(k);
+  CK(col_dot_sign(U, V, k, k, sgn, st));
+  std::vector<double> sv = d2h(S, k, st), sg = d2h(sgn, k, st);
+  std::vector<double> theta(k);
+  for (int i = 0; i < k; ++i) theta[i] = sg[i] * sv[i];
+  std::vector<int> order(k);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return theta[a] < theta[b]; });
+  std::vector<double> out(k);
+  for (int i = 0; i < k; ++i) out[i] = theta[order[i]];
+  int* perm = static_cast<int*>(ctx->jperm.get(sizeof(int) * k));
+  CK(cudaMemcpyAsync(perm, order.data(), sizeof(int) * k, cudaMemcpyHostToDevice, st));
+  CK(gather_cols(V, k, perm, nullptr, k, k, Qout, k, st));
+  CK(cudaStreamSynchronize(st));
+  return out;
 }
 
 static bool near_endpoint(double sigma, double endpoint) {
@@ -1195,7 +1129,7 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
   info.retained_rank = rank;
   res->basis_sv.assign(sv.begin(), sv.begin() + rank);
   double* US1 = B[T_US1].as<double>((size_t)n * rank);
-  dgemm(ctx, false, false, (int)n, rank, r, 1.0, Q, (int)n, UR, r, 0.0, US1, (int)n);
+  dgemm(ctx, false, (int)n, rank, r, 1.0, Q, (int)n, UR, r, 0.0, US1, (int)n);
   CK(cudaStreamSynchronize(s));
   tp.mark("U_S1 gemm");
   info.step_3 = now_s() - t0;
@@ -1218,7 +1152,7 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
     // ---- step 4: project_qr (extract.hpp:43-57)
     t0 = now_s();
     Ut = B[T_UT].as<double>((size_t)m * rank);
-    dgemm(ctx, false, false, (int)m, rank, (int)n, 1.0, Ad, lda, US1, (int)n, 0.0, Ut, (int)m);
+    dgemm(ctx, false, (int)m, rank, (int)n, 1.0, Ad, lda, US1, (int)n, 0.0, Ut, (int)m);
     Yk = B[T_Y].as<double>((size_t)m * rank);   // Y = A U_S1, kept for the Galerkin residuals
     CK(cudaMemcpyAsync(Yk, Ut, sizeof(double) * m * rank, cudaMemcpyDeviceToDevice, s));
     double* Bm = B[T_BM].as<double>((size_t)rank * rank);
@@ -1247,25 +1181,11 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
     // ---- naive_eigen_route (extract.hpp:108-139): Rayleigh-Ritz on G in span(U_S1)
     t0 = now_s();
     double* GU = B[T_UT].as<double>((size_t)n * rank);
-    dgemm(ctx, false, false, (int)n, rank, (int)n, 1.0, ctx->G.as<double>(0), (int)n, US1, (int)n, 0.0, GU, (int)n);
+    dgemm(ctx, false, (int)n, rank, (int)n, 1.0, ctx->G.as<double>(0), (int)n, US1, (int)n, 0.0, GU, (int)n);
     double* H = B[T_BM].as<double>((size_t)rank * rank);
-    dgemm(ctx, true, false, rank, rank, (int)n, 1.0, US1, (int)n, GU, (int)n, 0.0, H, rank);
-    std::vector<double> hh = d2h(H, (size_t)rank * rank, s);
-    for (int i = 0; i < rank; ++i)
-      for (int j = 0; j < i; ++j) {
-        const double v = (hh[(size_t)j * rank + i] + hh[(size_t)i * rank + j]) / 2.0;
-        hh[(size_t)j * rank + i] = hh[(size_t)i * rank + j] = v;
-      }
-    CK(cudaMemcpyAsync(H, hh.data(), sizeof(double) * rank * rank, cudaMemcpyHostToDevice, s));
-    double* theta_d = B[T_PHI].as<double>(rank);
-    int lwork = 0;
-    CKS(cusolverDnDsyevd_bufferSize(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, rank, H, rank,
-                                    theta_d, &lwork));
-    double* work = ctx->work.as<double>(lwork);
-    CKS(cusolverDnDsyevd(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, rank, H, rank, theta_d, work,
-                         lwork, ctx->info.as<int>(1)));
-    std::vector<double> theta = d2h(theta_d, rank, s);   // ascending
-    CK(cudaMemcpyAsync(Qm, H, sizeof(double) * rank * rank, cudaMemcpyDeviceToDevice, s));
+    dgemm(ctx, true, rank, rank, (int)n, 1.0, US1, (int)n, GU, (int)n, 0.0, H, rank);
+    CK(symmetrize(H, rank, rank, s));                  // (h + h^T) / 2 (extract.hpp:113)
+    std::vector<double> theta = sym_eig(ctx, H, rank, Qm);   // ascending, eigenvectors -> Qm
     for (int i = 0; i < rank; ++i) {
       sigma[i] = std::sqrt(std::max(theta[i], 0.0));
       invalid[i] = theta[i] > 0 ? 0 : 1;
@@ -1277,15 +1197,15 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
   // q (part of the result) goes out first, ahead of the triplet vectors on the copy engine
   res->q.resize((size_t)rank * rank);
   CK(cudaMemcpyAsync(res->q.data(), qs, sizeof(double) * rank * rank, cudaMemcpyDeviceToHost, s));
-  dgemm(ctx, false, false, (int)n, rank, rank, 1.0, US1, (int)n, qs, rank, 0.0, right, (int)n);
+  dgemm(ctx, false, (int)n, rank, rank, 1.0, US1, (int)n, qs, rank, 0.0, right, (int)n);
   double* sig_d = B[T_SIG].as<double>(rank);
   if (!naive) {
     double* ps = B[T_PS].as<double>((size_t)rank * rank);         // P[:, order]
     CK(gather_cols(Pm, rank, perm_d, nullptr, rank, rank, ps, rank, s));
-    dgemm(ctx, false, false, (int)m, rank, rank, 1.0, Ut, (int)m, ps, rank, 0.0, leftv, (int)m);
+    dgemm(ctx, false, (int)m, rank, rank, 1.0, Ut, (int)m, ps, rank, 0.0, leftv, (int)m);
   } else {
     double* av = B[T_UT].as<double>((size_t)m * rank);
-    dgemm(ctx, false, false, (int)m, rank, (int)n, 1.0, Ad, lda, right, (int)n, 0.0, av, (int)m);
+    dgemm(ctx, false, (int)m, rank, (int)n, 1.0, Ad, lda, right, (int)n, 0.0, av, (int)m);
     std::vector<double> inv(rank);
     for (int i = 0; i < rank; ++i) inv[i] = invalid[i] ? 0.0 : 1.0 / sigma[i];
     CK(cudaMemcpyAsync(sig_d, inv.data(), sizeof(double) * rank, cudaMemcpyHostToDevice, s));
@@ -1325,9 +1245,7 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
   tp.mark("tau + Sigma^+ q");
   {
     double* coeff = B[T_COEFF].as<double>((size_t)r * tcount);
-    double* X = B[T_X].as<double>((size_t)std::max(n, m) * tcount);
-    dgemm(ctx, false, false, r, tcount, rank, 1.0, VR, r, qsc_d, rank, 0.0, coeff, r);
-    dgemm(ctx, false, false, (int)n, tcount, r, 1.0, Sc + (size_t)n * L, (int)n, coeff, r, 0.0, X, (int)n);
+    dgemm(ctx, false, r, tcount, rank, 1.0, VR, r, qsc_d, rank, 0.0, coeff, r);
     std::vector<double> images(tcount);
     for (int i = 0; i < tcount; ++i) {
       if (use_exp) images[i] = sigma[i] > 1e-30 ? std::log(sigma[i] * sigma[i]) : 0.0;   // g^{-1}(sigma^2)
@@ -1336,21 +1254,24 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
     double* img_d = B[T_IMG].as<double>(tcount);
     CK(cudaMemcpyAsync(img_d, images.data(), sizeof(double) * tcount, cudaMemcpyHostToDevice, s));
     double* out_d = B[T_NRM].as<double>(3 * (size_t)tcount);
-    B[T_CNP].as<double>(colnorm_scratch((int)std::max(n, m), tcount));   // sized once for the three norms
-    CK(colnorm_diff(X, (int)n, right, (int)n, img_d, (int)n, tcount, out_d, B[T_CNP].as<double>(colnorm_scratch((int)n, tcount)), s));
+    double* part = B[T_CNP].as<double>(dgemm_norm_scratch((int)std::max(n, m), tcount));
+    // the three residual norms as GEMMs with the fused "- d_i w_i, column norm" epilogue:
+    //   transformed ||S+ (W Sigma^+ q_i) - img_i v_i|| (postprocess.hpp:91-95)
+    CK(dgemm_colnorm_diff(false, (int)n, tcount, r, Sc + (size_t)n * L, (int)n, coeff, r, img_d, right, (int)n, out_d,
+                          part, s));
     tp.mark("transformed residual");
-    // exact residual ||A^T u - sigma v|| (postprocess.hpp:34-41), Galerkin ||A v - sigma u||
+    //   exact ||A^T u_i - sigma_i v_i|| (postprocess.hpp:34-41)
     CK(cudaMemcpyAsync(sig_d, sigma.data(), sizeof(double) * tcount, cudaMemcpyHostToDevice, s));
-    dgemm(ctx, true, false, (int)n, tcount, (int)m, 1.0, Ad, lda, leftv, (int)m, 0.0, X, (int)n);
-    CK(colnorm_diff(X, (int)n, right, (int)n, sig_d, (int)n, tcount, out_d + tcount, B[T_CNP].as<double>(colnorm_scratch((int)n, tcount)), s));
-    if (Yk) {
-      // A v_i = A U_S1 q_i = Y q_i with Y = A U_S1 kept from project_qr: an m x r x r product
-      // instead of m x n x r (equal up to rounding)
-      dgemm(ctx, false, false, (int)m, tcount, rank, 1.0, Yk, (int)m, qs, rank, 0.0, X, (int)m);
-    } else {
-      dgemm(ctx, false, false, (int)m, tcount, (int)n, 1.0, Ad, lda, right, (int)n, 0.0, X, (int)m);
-    }
-    CK(colnorm_diff(X, (int)m, leftv, (int)m, sig_d, (int)m, tcount, out_d + 2 * tcount, B[T_CNP].as<double>(colnorm_scratch((int)m, tcount)), s));
+    CK(dgemm_colnorm_diff(true, (int)n, tcount, (int)m, Ad, lda, leftv, (int)m, sig_d, right, (int)n, out_d + tcount,
+                          part, s));
+    //   Galerkin ||A v_i - sigma_i u_i|| (pipeline.hpp:203-208); A v_i = A U_S1 q_i = Y q_i with Y = A U_S1
+    //   kept from project_qr: an m x r x r product instead of m x n x r (equal up to rounding)
+    if (Yk)
+      CK(dgemm_colnorm_diff(false, (int)m, tcount, rank, Yk, (int)m, qs, rank, sig_d, leftv, (int)m,
+                            out_d + 2 * tcount, part, s));
+    else
+      CK(dgemm_colnorm_diff(false, (int)m, tcount, (int)n, Ad, lda, right, (int)n, sig_d, leftv, (int)m,
+                            out_d + 2 * tcount, part, s));
     // one small read-back at the end: the copy engine is busy with the triplet vectors meanwhile
     std::vector<double> norms = d2h(out_d, 3 * (size_t)tcount, s);
     res->tau = d2h(tau_d, tcount, s);
@@ -1430,12 +1351,6 @@ static sssvd_status guarded(sssvd_gpu_ctx* ctx, F&& body) {
 extern "C" {
 
 uint64_t sssvd_gpu_launch_count(void) { return launch_count(); }
-// debug: per-column cycle breakdown of the leaf kernel (SSSVD_LEAF_PROF=1 builds it in)
-void sssvd_debug_leaf_profile(uint64_t* out5) {  // 7 entries
-  unsigned long long v[7];
-  leaf_profile_read(v, true);
-  for (int i = 0; i < 7; ++i) out5[i] = v[i];
-}
 void sssvd_gpu_profile_gemm(int enable) { zgemm_profile_enable(enable != 0); }
 void sssvd_gpu_profile_gemm_collect(double* ms, double* flops, uint64_t* launches) {
   unsigned long long l = 0;
@@ -1456,8 +1371,7 @@ sssvd_status sssvd_gpu_create(int device, sssvd_gpu_ctx** out) {
   if (prop.major != 10) return SSSVD_E_CUDA;  // sm_100a binary only
   auto* ctx = new sssvd_gpu_ctx();
   ctx->device = device;
-  if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cublasCreate(&ctx->blas) != CUBLAS_STATUS_SUCCESS || cusolverDnCreate(&ctx->solver) != CUSOLVER_STATUS_SUCCESS) {
+  if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete ctx;
     return SSSVD_E_CUDA;
   }
@@ -1473,8 +1387,6 @@ sssvd_status sssvd_gpu_create(int device, sssvd_gpu_ctx** out) {
   cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming);
-  cublasSetStream(ctx->blas, ctx->stream);
-  cusolverDnSetStream(ctx->solver, ctx->stream);
   *out = ctx;
   return SSSVD_OK;
 }
@@ -1484,14 +1396,12 @@ void sssvd_gpu_destroy(sssvd_gpu_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   DBuf* bufs[] = {&ctx->A, &ctx->G, &ctx->gmax, &ctx->mats, &ctx->ipiv, &ctx->shifts, &ctx->coef, &ctx->S, &ctx->V,
-                  &ctx->status, &ctx->minpiv, &ctx->scratch, &ctx->t0, &ctx->t1, &ctx->t2, &ctx->t7, &ctx->work,
-                  &ctx->info, &ctx->lw_linv, &ctx->lw_T, &ctx->lw_src, &ctx->lw_disp, &ctx->lw2_linv, &ctx->lw2_T, &ctx->lw2_src, &ctx->lw2_disp, &ctx->jscr, &ctx->jperm, &ctx->jq, &ctx->jr, &ctx->jj,
+                  &ctx->status, &ctx->minpiv, &ctx->scratch, &ctx->t0, &ctx->t1, &ctx->t2, &ctx->t7, &ctx->gwork,
+                  &ctx->lw_linv, &ctx->lw_T, &ctx->lw_src, &ctx->lw_disp, &ctx->lw2_linv, &ctx->lw2_T, &ctx->lw2_src, &ctx->lw2_disp, &ctx->jscr, &ctx->jperm, &ctx->jq, &ctx->jr, &ctx->jj,
                   &ctx->qy, &ctx->qt, &ctx->qw};
   for (DBuf* b : bufs) b->release();
   for (auto& b : ctx->tail) b.release();
   if (ctx->comm) nccl().CommDestroy(ctx->comm);
-  if (ctx->solver) cusolverDnDestroy(ctx->solver);
-  if (ctx->blas) cublasDestroy(ctx->blas);
   for (int g = 0; g < sssvd_gpu_ctx::kMaxGroups; ++g) {
     if (ctx->gstream[g]) cudaStreamDestroy(ctx->gstream[g]);
     if (ctx->gstream_lo[g]) cudaStreamDestroy(ctx->gstream_lo[g]);
@@ -1564,11 +1474,9 @@ sssvd_status sssvd_gpu_set_operator(sssvd_gpu_ctx* ctx, const double* a, int64_t
     if (!tr) {
       CK(pad_copy(stage, (int)rows, (int)cols, (int)lda, Ad, (int)ldp, s));
     } else {
-      // A^T via cuBLAS geam into a dense m x n buffer, then pad
+      // A^T into a dense m x n buffer (transpose kernel), then pad
       double* tmp = ctx->t1.as<double>((size_t)m * n);
-      const double one = 1.0, zero = 0.0;
-      CKB(cublasDgeam(ctx->blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)m, (int)n, &one, stage, (int)lda, &zero, tmp, (int)m,
-                      tmp, (int)m));
+      CK(transpose(stage, (int)rows, (int)cols, (int)lda, tmp, (int)m, s));
       CK(pad_copy(tmp, (int)m, (int)n, (int)m, Ad, (int)ldp, s));
     }
     finish_operator(ctx, m, n, ldp, tr);
@@ -1703,46 +1611,36 @@ __global__ void debug_diff_kernel(const unsigned long long* a, const unsigned lo
 }
 }  // namespace
 
+// debug: times the trailing-update GEMM C -= A B (complex, row-major, batched) on seeded data;
+// *mismatches_out counts the entries of a second run that differ bitwise from the first
+// (run-to-run determinism). variant must be 0 (the product kernel).
 sssvd_status sssvd_debug_zgemm(sssvd_gpu_ctx* ctx, int variant, int64_t m, int64_t n, int64_t k, int64_t batch,
                                int reps, double* ms_out, int64_t* mismatches_out) {
   return guarded(ctx, [&]() {
-    if (m < 1 || n < 1 || k < 1 || batch < 1 || reps < 1 || variant < 0 || variant > 10)
+    if (m < 1 || n < 1 || k < 1 || batch < 1 || reps < 1 || variant != 0)
       throw Status(SSSVD_E_INVALID_ARGUMENT, "debug_zgemm: bad arguments");
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
     const size_t na = (size_t)batch * m * k, nb = (size_t)batch * k * n, nc = (size_t)batch * m * n;
-    double2 *A = nullptr, *B = nullptr, *C0 = nullptr, *C1 = nullptr;
+    double2 *A = nullptr, *B = nullptr, *C0 = nullptr, *C1 = nullptr, *C2 = nullptr;
     unsigned long long* cnt = nullptr;
-    auto release = [&]() { cudaFree(A); cudaFree(B); cudaFree(C0); cudaFree(C1); cudaFree(cnt); };
+    auto release = [&]() { cudaFree(A); cudaFree(B); cudaFree(C0); cudaFree(C1); cudaFree(C2); cudaFree(cnt); };
     try {
       CK(cudaMalloc(&A, na * sizeof(double2)));
       CK(cudaMalloc(&B, nb * sizeof(double2)));
       CK(cudaMalloc(&C0, nc * sizeof(double2)));
       CK(cudaMalloc(&C1, nc * sizeof(double2)));
+      CK(cudaMalloc(&C2, nc * sizeof(double2)));
       CK(cudaMalloc(&cnt, sizeof(unsigned long long)));
       debug_fill_kernel<<<1184, 256, 0, s>>>((double*)A, 2 * (long long)na, 1);
       debug_fill_kernel<<<1184, 256, 0, s>>>((double*)B, 2 * (long long)nb, 2);
       debug_fill_kernel<<<1184, 256, 0, s>>>((double*)C0, 2 * (long long)nc, 3);
       CK(cudaMemcpyAsync(C1, C0, nc * sizeof(double2), cudaMemcpyDeviceToDevice, s));
-      zgemm_set_variant(0);
-      CK(zgemm_sub((int)m, (int)n, (int)k, A, (int)k, m * k, B, (int)n, k * n, C0, (int)n, m * n, (int)batch, s));
-      // variant 10: cuBLAS zgemmStridedBatched on the same row-major data (C^T -= B^T A^T in its
-      // column-major view) -- a library comparator for the measurement only, never the product path
-      const cuDoubleComplex mone = make_cuDoubleComplex(-1.0, 0.0), one = make_cuDoubleComplex(1.0, 0.0);
-      auto run = [&](double2* Cx) {
-        if (variant == 10) {
-          CKB(cublasSetStream(ctx->blas, s));
-          CKB(cublasZgemmStridedBatched(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)n, (int)m, (int)k, &mone,
-                                        (const cuDoubleComplex*)B, (int)n, k * n, (const cuDoubleComplex*)A, (int)k,
-                                        m * k, &one, (cuDoubleComplex*)Cx, (int)n, m * n, (int)batch));
-        } else {
-          CK(zgemm_sub((int)m, (int)n, (int)k, A, (int)k, m * k, B, (int)n, k * n, Cx, (int)n, m * n, (int)batch, s));
-        }
-      };
-      zgemm_set_variant(variant == 10 ? 0 : variant);
-      run(C1);
+      CK(cudaMemcpyAsync(C2, C0, nc * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+      CK(zgemm_sub((int)m, (int)n, (int)k, A, (int)k, m * k, B, (int)n, k * n, C1, (int)n, m * n, (int)batch, s));
+      CK(zgemm_sub((int)m, (int)n, (int)k, A, (int)k, m * k, B, (int)n, k * n, C2, (int)n, m * n, (int)batch, s));
       CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
-      debug_diff_kernel<<<1184, 256, 0, s>>>((const unsigned long long*)C0, (const unsigned long long*)C1,
+      debug_diff_kernel<<<1184, 256, 0, s>>>((const unsigned long long*)C1, (const unsigned long long*)C2,
                                              2 * (long long)nc, cnt);
       unsigned long long h = 0;
       CK(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -1750,7 +1648,8 @@ sssvd_status sssvd_debug_zgemm(sssvd_gpu_ctx* ctx, int variant, int64_t m, int64
       CK(cudaEventCreate(&e0));
       CK(cudaEventCreate(&e1));
       CK(cudaEventRecord(e0, s));
-      for (int r = 0; r < reps; ++r) run(C1);
+      for (int r = 0; r < reps; ++r)
+        CK(zgemm_sub((int)m, (int)n, (int)k, A, (int)k, m * k, B, (int)n, k * n, C1, (int)n, m * n, (int)batch, s));
       CK(cudaEventRecord(e1, s));
       CK(cudaEventSynchronize(e1));
       float ms = 0;
@@ -1760,12 +1659,41 @@ sssvd_status sssvd_debug_zgemm(sssvd_gpu_ctx* ctx, int variant, int64_t m, int64
       *ms_out = ms / reps;
       *mismatches_out = (int64_t)h;
     } catch (...) {
-      zgemm_set_variant(-1);
       release();
       throw;
     }
-    zgemm_set_variant(-1);
     release();
+  });
+}
+
+// debug: C = alpha op(A) B + beta C through the tail GEMM (dgemm.cu), host column-major buffers
+// (C in/out); mode 1: out[j] = ||op(A) B[:, j] - d_j V[:, j]|| (the fused residual form) into c_out
+sssvd_status sssvd_debug_dgemm(sssvd_gpu_ctx* ctx, int mode, int ta, int64_t m, int64_t n, int64_t k, double alpha,
+                               const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
+                               const double* d, const double* v, double* c_io, int64_t ldc) {
+  return guarded(ctx, [&]() {
+    if (m < 1 || n < 1 || k < 0 || lda < (ta ? std::max<int64_t>(k, 1) : m) || ldb < std::max<int64_t>(k, 1) ||
+        ldc < m || (mode != 0 && mode != 1))
+      throw Status(SSSVD_E_INVALID_ARGUMENT, "debug_dgemm: bad arguments");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const size_t na = (size_t)lda * (ta ? m : std::max<int64_t>(k, 1)), nb = (size_t)ldb * n, nc = (size_t)ldc * n;
+    double* A = ctx->t0.as<double>(na + nb + 2 * nc + n);
+    double *B = A + na, *C = B + nb, *Vd = C + nc, *dd = Vd + nc;
+    CK(cudaMemcpyAsync(A, a, sizeof(double) * na, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(B, b, sizeof(double) * nb, cudaMemcpyHostToDevice, s));
+    if (mode == 0) {
+      CK(cudaMemcpyAsync(C, c_io, sizeof(double) * nc, cudaMemcpyHostToDevice, s));
+      dgemm(ctx, ta != 0, (int)m, (int)n, (int)k, alpha, A, (int)lda, B, (int)ldb, beta, C, (int)ldc);
+      CK(cudaMemcpyAsync(c_io, C, sizeof(double) * nc, cudaMemcpyDeviceToHost, s));
+    } else {
+      CK(cudaMemcpyAsync(Vd, v, sizeof(double) * nc, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(dd, d, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+      double* part = ctx->t2.as<double>(dgemm_norm_scratch((int)m, (int)n));
+      CK(dgemm_colnorm_diff(ta != 0, (int)m, (int)n, (int)k, A, (int)lda, B, (int)ldb, dd, Vd, (int)ldc, C, part, s));
+      CK(cudaMemcpyAsync(c_io, C, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
   });
 }
 

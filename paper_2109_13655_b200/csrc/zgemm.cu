@@ -13,6 +13,8 @@
 // conflict-free LDS.128 per quarter-warp.
 #include <algorithm>
 #include <atomic>
+#include <map>
+#include <mutex>
 #include <cstdlib>
 #include <vector>
 
@@ -374,410 +376,34 @@ zgemm_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long l
   }
 }
 
-// Persistent form of the 32x32-warp-tile kernel (variants 4, 5): the cp.async ring runs across
-// tiles, so the next tile's first k-stages load while this tile's last ones compute, and C -= AB
-// leaves through fire-and-forget red.global.add.f64 of -acc (fl(c + (-x)) == fl(c - x): bitwise
-// the read-modify-write epilogue, with no C read into the SM and no C staging). Tiles are walked
-// t = blockIdx.x + i * gridDim.x over (batch, m-tile, n-tile); grid = 2 CTAs per SM (variant 4)
-// or one CTA per tile (variant 5, the red epilogue alone).
-__device__ __forceinline__ void red_add_f64(double* p, double v) {
-  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
-}
-
-template <bool SET, bool GATHER>
-__global__ void __launch_bounds__(128, 2)
-zgemm_persist_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long long sA,
-                     const double2* __restrict__ B, int ldb, long long sB, const int* __restrict__ brow, int sR,
-                     double2* C, int ldc, long long sC, int batch, unsigned long long* __restrict__ stamp,
-                     int stamp_cap) {
-  constexpr int THREADS = 128, WI = 4, WJ = 4;
-  extern __shared__ __align__(16) double2 smem[];
-  if (stamp && threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    atomicMin(stamp, t);
-  }
-  constexpr int SSTRIDE = A_STAGE + B_STAGE;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1;
-  const int tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
-  const int per = tm * tn, total = per * batch;
-  const int KT = (K + BK - 1) / BK;
-  const int ntiles = blockIdx.x < total ? (total - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int steps = ntiles * KT;
-
-  // producer state: the (tile, k-stage) of the next load
-  int ld_tile = 0, ld_kt = 0;
-  auto issue = [&](int slot) {
-    const int t = blockIdx.x + ld_tile * gridDim.x;
-    const int z = t / per, rem = t - z * per;
-    const int m0 = (rem / tn) * BM, n0 = (rem % tn) * BN;
-    load_stage<THREADS, GATHER>(smem + slot * SSTRIDE, smem + slot * SSTRIDE + A_STAGE, A + z * sA, lda, B + z * sB,
-                                ldb, GATHER ? brow + z * sR : brow, M, N, K, m0, n0, ld_kt * BK, tid);
-    if (++ld_kt == KT) {
-      ld_kt = 0;
-      ++ld_tile;
-    }
-  };
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < steps) issue(s);
-    cp_async_commit();
-  }
-
-  double acc_re[WI][WJ][2], acc_im[WI][WJ][2];
-#pragma unroll
-  for (int i = 0; i < WI; ++i)
-#pragma unroll
-    for (int j = 0; j < WJ; ++j) {
-      acc_re[i][j][0] = acc_re[i][j][1] = 0.0;
-      acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
-    }
-  const int fr = lane >> 2, fc = lane & 3;
-  int cur_tile = 0, cur_kt = 0;
-  for (int g = 0; g < steps; ++g) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    if (g + STAGES - 1 < steps) issue((g + STAGES - 1) % STAGES);
-    cp_async_commit();
-    const double2* as = smem + (g % STAGES) * SSTRIDE + (wm * 32 + fr) * LDA_S + fc;
-    const double2* bs = smem + (g % STAGES) * SSTRIDE + A_STAGE + fc * LDB_S + wn * 32 + fr;
-#pragma unroll
-    for (int kq = 0; kq < BK / 4; ++kq) {
-      double2 a[WI], b[WJ];
-#pragma unroll
-      for (int i = 0; i < WI; ++i) a[i] = as[i * 8 * LDA_S + kq * 4];
-#pragma unroll
-      for (int j = 0; j < WJ; ++j) b[j] = bs[kq * 4 * LDB_S + j * 8];
-      double nai[WI];
-#pragma unroll
-      for (int i = 0; i < WI; ++i) nai[i] = -a[i].y;
-#pragma unroll
-      for (int i = 0; i < WI; ++i)
-#pragma unroll
-        for (int j = 0; j < WJ; ++j) dmma884(acc_re[i][j][0], acc_re[i][j][1], a[i].x, b[j].x);
-#pragma unroll
-      for (int i = 0; i < WI; ++i)
-#pragma unroll
-        for (int j = 0; j < WJ; ++j) dmma884(acc_im[i][j][0], acc_im[i][j][1], a[i].x, b[j].y);
-#pragma unroll
-      for (int i = 0; i < WI; ++i)
-#pragma unroll
-        for (int j = 0; j < WJ; ++j) dmma884(acc_re[i][j][0], acc_re[i][j][1], nai[i], b[j].y);
-#pragma unroll
-      for (int i = 0; i < WI; ++i)
-#pragma unroll
-        for (int j = 0; j < WJ; ++j) dmma884(acc_im[i][j][0], acc_im[i][j][1], a[i].y, b[j].x);
-    }
-    if (++cur_kt == KT) {
-      // tile epilogue: the accumulators leave as stores (SET) or reductions (C -= AB); the next
-      // tile's first stages are already in flight
-      const int t = blockIdx.x + cur_tile * gridDim.x;
-      const int z = t / per, rem = t - z * per;
-      const int m0 = (rem / tn) * BM, n0 = (rem % tn) * BN;
-      double2* Cz = C + z * sC;
-#pragma unroll
-      for (int i = 0; i < WI; ++i) {
-        const int r = m0 + wm * 32 + i * 8 + fr;
-        if (r < M) {
-          double2* crow = Cz + (size_t)r * ldc + n0 + wn * 32 + 2 * fc;
-          const int cbase = n0 + wn * 32 + 2 * fc;
-#pragma unroll
-          for (int j = 0; j < WJ; ++j) {
-            const int c = cbase + j * 8;
-            if (SET) {
-              if (c < N) crow[j * 8] = make_double2(acc_re[i][j][0], acc_im[i][j][0]);
-              if (c + 1 < N) crow[j * 8 + 1] = make_double2(acc_re[i][j][1], acc_im[i][j][1]);
-            } else {
-              if (c < N) {
-                red_add_f64(&crow[j * 8].x, -acc_re[i][j][0]);
-                red_add_f64(&crow[j * 8].y, -acc_im[i][j][0]);
-              }
-              if (c + 1 < N) {
-                red_add_f64(&crow[j * 8 + 1].x, -acc_re[i][j][1]);
-                red_add_f64(&crow[j * 8 + 1].y, -acc_im[i][j][1]);
-              }
-            }
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < WJ; ++j) {
-          acc_re[i][j][0] = acc_re[i][j][1] = 0.0;
-          acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
-        }
-      }
-      cur_kt = 0;
-      ++cur_tile;
-    }
-  }
-  cp_async_wait<0>();
-  if (stamp) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      atomicMax(stamp + stamp_cap, t);
-    }
-  }
-}
-
-// Persistent, C-buffered form (variants 6, 7): one CTA of 8 warps (32x16 warp tiles) per SM walks
-// its tiles t = blockIdx.x + i * gridDim.x. The cp.async ring of PS stages runs across tiles (the
-// next tile's first k-stages load under this tile's last ones), and the tile's C block is
-// prefetched into its own shared buffer with the tile's first k-stage, so the read-modify-write
-// epilogue never waits on HBM. Each CTA start, prologue and C fetch is paid once per SM instead of
-// once per tile.
-template <int PS>
-constexpr size_t persist2_smem() {
-  return ((size_t)PS * (A_STAGE + B_STAGE) + (size_t)BM * CP) * sizeof(double2);
-}
-
-template <int PS, bool SET, bool GATHER>
-__global__ void __launch_bounds__(256, 1)
-zgemm_persist2_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long long sA,
-                      const double2* __restrict__ B, int ldb, long long sB, const int* __restrict__ brow, int sR,
-                      double2* C, int ldc, long long sC, int batch, unsigned long long* __restrict__ stamp,
-                      int stamp_cap) {
-  constexpr int THREADS = 256, WI = 4, WJ = 2, WARPS_N = 4;
-  extern __shared__ __align__(16) double2 smem[];
-  if (stamp && threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    atomicMin(stamp, t);
-  }
-  constexpr int SSTRIDE = A_STAGE + B_STAGE;
-  double2* Cs = smem + PS * SSTRIDE;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp / WARPS_N, wn = warp % WARPS_N;
-  const int tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
-  const int per = tm * tn, total = per * batch;
-  const int KT = (K + BK - 1) / BK;
-  const int ntiles = blockIdx.x < total ? (total - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int steps = ntiles * KT;
-
-  // producer: (tile, k-stage) of the next load
-  int p_tile = 0, p_kt = 0;
-  StageLoader<THREADS> ld;
-  auto issue = [&](int slot) {
-    const int t = blockIdx.x + p_tile * gridDim.x;
-    const int z = t / per, rem = t - z * per;
-    const int m0 = (rem / tn) * BM, n0 = (rem % tn) * BN;
-    double2* As = smem + slot * SSTRIDE;
-    if (GATHER) {
-      load_stage<THREADS, GATHER>(As, As + A_STAGE, A + z * sA, lda, B + z * sB, ldb, brow + z * sR, M, N, K, m0, n0,
-                                  p_kt * BK, tid);
-    } else {
-      if (p_kt == 0) ld.init(A + z * sA, lda, B + z * sB, ldb, M, N, m0, n0, tid);
-      ld.load(As, As + A_STAGE, K - p_kt * BK, false);
-    }
-    if (++p_kt == KT) {
-      p_kt = 0;
-      ++p_tile;
-    }
-  };
-  auto fetch_c = [&](int tile) {   // C block of `tile` -> Cs (pitch CP)
-    const int t = blockIdx.x + tile * gridDim.x;
-    const int z = t / per, rem = t - z * per;
-    const int m0 = (rem / tn) * BM, n0 = (rem % tn) * BN;
-    const double2* Cz = C + z * sC;
-#pragma unroll
-    for (int i = 0; i < (BM * BN) / THREADS; ++i) {
-      const int idx = tid + i * THREADS;
-      const int r = idx / BN, c = idx % BN;
-      const bool p = (m0 + r < M) && (n0 + c < N);
-      cp_async16(Cs + r * CP + c, p ? Cz + (size_t)(m0 + r) * ldc + n0 + c : Cz, p);
-    }
-  };
-#pragma unroll
-  for (int s = 0; s < PS - 1; ++s) {
-    if (s < steps) issue(s);
-    if (!SET && s == 0 && steps > 0) fetch_c(0);
-    cp_async_commit();
-  }
-
-  double acc_re[WI][WJ][2], acc_im[WI][WJ][2];
-#pragma unroll
-  for (int i = 0; i < WI; ++i)
-#pragma unroll
-    for (int j = 0; j < WJ; ++j) {
-      acc_re[i][j][0] = acc_re[i][j][1] = 0.0;
-      acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
-    }
-  const int fr = lane >> 2, fc = lane & 3;
-  int c_tile = 0, c_kt = 0;
-  for (int g = 0; g < steps; ++g) {
-    cp_async_wait<PS - 2>();
-    __syncthreads();
-    if (g + PS - 1 < steps) issue((g + PS - 1) % PS);
-    // the C block of this tile rides with the tile's first k-step (the buffer was released by the
-    // previous tile's epilogue before the barrier above)
-    if (!SET && c_kt == 0 && g > 0) fetch_c(c_tile);
-    cp_async_commit();
-    const double2* as = smem + (g % PS) * SSTRIDE + (wm * 8 * WI + fr) * LDA_S + fc;
-    const double2* bs = smem + (g % PS) * SSTRIDE + A_STAGE + fc * LDB_S + wn * 8 * WJ + fr;
-#pragma unroll
-    for (int kq = 0; kq < BK / 4; ++kq) {
-      double2 a[WI], b[WJ];
-#pragma unroll
-      for (int i = 0; i < WI; ++i) a[i] = as[i * 8 * LDA_S + kq * 4];
-#pragma unroll
-      for (int j = 0; j < WJ; ++j) b[j] = bs[kq * 4 * LDB_S + j * 8];
-      double nai[WI];
-#pragma unroll
-      for (int i = 0; i < WI; ++i) nai[i] = -a[i].y;
-#pragma unroll
-      for (int i = 0; i < WI; ++i)
-#pragma unroll
-        for (int j = 0; j < WJ; ++j) dmma884(acc_re[i][j][0], acc_re[i][j][1], a[i].x, b[j].x);
-#pragma unroll
-      for (int i = 0; i < WI; ++i)
-#pragma unroll
-        for (int j = 0; j < WJ; ++j) dmma884(acc_im[i][j][0], acc_im[i][j][1], a[i].x, b[j].y);
-#pragma unroll
-      for (int i = 0; i < WI; ++i)
-#pragma unroll
-        for (int j = 0; j < WJ; ++j) dmma884(acc_re[i][j][0], acc_re[i][j][1], nai[i], b[j].y);
-#pragma unroll
-      for (int i = 0; i < WI; ++i)
-#pragma unroll
-        for (int j = 0; j < WJ; ++j) dmma884(acc_im[i][j][0], acc_im[i][j][1], a[i].y, b[j].x);
-    }
-    if (++c_kt == KT) {
-      // epilogue of tile c_tile. Its C group was committed with the tile's first step; the wait at
-      // the top of step x leaves only the newest PS - 2 groups pending, so with KT >= PS the wait +
-      // barrier of this step already covered it, else wait for it here
-      if (!SET && KT < PS) {
-        cp_async_wait<0>();
-        __syncthreads();
-      }
-      const int t = blockIdx.x + c_tile * gridDim.x;
-      const int z = t / per, rem = t - z * per;
-      const int m0 = (rem / tn) * BM, n0 = (rem % tn) * BN;
-      double2* Cz = C + z * sC;
-#pragma unroll
-      for (int i = 0; i < WI; ++i) {
-        const int rt = wm * 8 * WI + i * 8 + fr;
-        const int r = m0 + rt;
-        if (r < M) {
-          double2* crow = Cz + (size_t)r * ldc + n0 + wn * 8 * WJ + 2 * fc;
-          const int cbase = n0 + wn * 8 * WJ + 2 * fc;
-          const double2* cs = Cs + rt * CP + wn * 8 * WJ + 2 * fc;
-#pragma unroll
-          for (int j = 0; j < WJ; ++j) {
-            const int c = cbase + j * 8;
-            if (SET) {
-              if (c < N) crow[j * 8] = make_double2(acc_re[i][j][0], acc_im[i][j][0]);
-              if (c + 1 < N) crow[j * 8 + 1] = make_double2(acc_re[i][j][1], acc_im[i][j][1]);
-            } else {
-              const double2 v0 = cs[j * 8], v1 = cs[j * 8 + 1];
-              if (c < N) crow[j * 8] = make_double2(v0.x - acc_re[i][j][0], v0.y - acc_im[i][j][0]);
-              if (c + 1 < N) crow[j * 8 + 1] = make_double2(v1.x - acc_re[i][j][1], v1.y - acc_im[i][j][1]);
-            }
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < WJ; ++j) {
-          acc_re[i][j][0] = acc_re[i][j][1] = 0.0;
-          acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
-        }
-      }
-      c_kt = 0;
-      ++c_tile;
-    }
-  }
-  cp_async_wait<0>();
-  if (stamp) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      atomicMax(stamp + stamp_cap, t);
-    }
-  }
-}
-
 size_t zgemm_sub_smem() { return (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double2); }
 
-// variant of the trailing-update GEMM: SSSVD_ZGEMM_V (warp tiles 0: 32x32, 1: 32x16, 2: 16x32,
-// 3: 16x16; 4: persistent 32x32 with the red epilogue; 5: one CTA per tile with the red epilogue;
-// 6 / 7: persistent 8-warp CTA per SM with a C buffer, 3 / 4 k-stages; 8 / 9: 32x32 with the next
-// stage issued after the first / second k-quad instead of at the top)
-// or zgemm_set_variant (measurement hook)
-static int g_variant = -1;
-void zgemm_set_variant(int v) { g_variant = v; }
-static int zgemm_variant() {
-  if (g_variant < 0) {
-    // default 8: the next stage's copies go out after the first k-quad's DMMAs (+1 % over the
-    // top-of-stage issue, tools/zgemm_variants.py; bitwise identical)
-    const char* e = std::getenv("SSSVD_ZGEMM_V");
-    g_variant = e ? std::atoi(e) : 8;
-    if (g_variant < 0 || g_variant > 9) g_variant = 8;
-  }
-  return g_variant;
-}
-
-template <int WI, int WJ, bool SET, bool GATHER, int ISSUE_AT = 0>
-static cudaError_t launch_v(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B, int ldb,
-                            long long sB, const int* brow, int sR, double2* C, int ldc, long long sC, int batch,
-                            cudaStream_t stream, unsigned long long* stamp) {
-  constexpr int THREADS = (64 / (8 * WI)) * (64 / (8 * WJ)) * 32;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(zgemm_kernel<WI, WJ, SET, GATHER, ISSUE_AT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zgemm_sub_smem());
+// Per-device kernel attributes: cudaFuncSetAttribute applies to the current device only, so the
+// largest dynamic shared-memory size set so far is remembered per (kernel, device).
+cudaError_t set_kernel_smem(const void* fn, size_t bytes, bool nonportable_cluster) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;   // bytes + 1 once configured
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = done[{fn, dev}];
+  if (cur > bytes) return cudaSuccess;
+  if (bytes > 48 * 1024 || cur == 0) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(bytes, 48 * 1024));
     if (e != cudaSuccess) return e;
-    configured = true;
   }
-  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch);
-  zgemm_kernel<WI, WJ, SET, GATHER, ISSUE_AT><<<grid, THREADS, zgemm_sub_smem(), stream>>>(
-      M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, stamp, g_prof.cap);
-  return cudaGetLastError();
-}
-
-template <bool SET, bool GATHER>
-static cudaError_t launch_persist(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B,
-                                  int ldb, long long sB, const int* brow, int sR, double2* C, int ldc, long long sC,
-                                  int batch, cudaStream_t stream, unsigned long long* stamp, bool persistent) {
-  static bool configured = false;
-  static int sms = 148;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(zgemm_persist_kernel<SET, GATHER>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zgemm_sub_smem());
+  if (nonportable_cluster) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    configured = true;
   }
-  const long long total = (long long)((M + BM - 1) / BM) * ((N + BN - 1) / BN) * batch;
-  const int grid = (int)(persistent ? std::min<long long>(total, 2LL * sms) : total);
-  zgemm_persist_kernel<SET, GATHER><<<grid, 128, zgemm_sub_smem(), stream>>>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR,
-                                                                             C, ldc, sC, batch, stamp, g_prof.cap);
-  return cudaGetLastError();
+  cur = bytes + 1;
+  return cudaSuccess;
 }
 
-template <int PS, bool SET, bool GATHER>
-static cudaError_t launch_persist2(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B,
-                                   int ldb, long long sB, const int* brow, int sR, double2* C, int ldc, long long sC,
-                                   int batch, cudaStream_t stream, unsigned long long* stamp) {
-  static bool configured = false;
-  static int sms = 148;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(zgemm_persist2_kernel<PS, SET, GATHER>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)persist2_smem<PS>());
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    configured = true;
-  }
-  const long long total = (long long)((M + BM - 1) / BM) * ((N + BN - 1) / BN) * batch;
-  const int grid = (int)std::min<long long>(total, sms);
-  zgemm_persist2_kernel<PS, SET, GATHER><<<grid, 256, persist2_smem<PS>(), stream>>>(
-      M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stamp, g_prof.cap);
-  return cudaGetLastError();
-}
-
+// C -= A B (SET = false) or C = A B[brow] (SET = GATHER = true). The next k-stage's copies are
+// issued after the first k-quad's DMMAs (measured +1 % over issuing them at the top of the stage;
+// bitwise identical).
 template <bool SET, bool GATHER>
 static cudaError_t launch(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B, int ldb,
                           long long sB, const int* brow, int sR, double2* C, int ldc, long long sC, int batch,
@@ -789,18 +415,12 @@ static cudaError_t launch(int M, int N, int K, const double2* A, int lda, long l
     g_prof.flops.push_back(8.0 * M * (double)N * K * batch);
   }
   note_launch();
-  switch (zgemm_variant()) {
-    case 1: return launch_v<4, 2, SET, GATHER>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stream, stamp);
-    case 2: return launch_v<2, 4, SET, GATHER>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stream, stamp);
-    case 3: return launch_v<2, 2, SET, GATHER>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stream, stamp);
-    case 4: return launch_persist<SET, GATHER>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stream, stamp, true);
-    case 5: return launch_persist<SET, GATHER>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stream, stamp, false);
-    case 6: return launch_persist2<3, SET, GATHER>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stream, stamp);
-    case 7: return launch_persist2<4, SET, GATHER>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stream, stamp);
-    case 9: return launch_v<4, 4, SET, GATHER, 2>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stream, stamp);
-    case 0: return launch_v<4, 4, SET, GATHER>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stream, stamp);
-    default: return launch_v<4, 4, SET, GATHER, 1>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stream, stamp);
-  }
+  auto kern = zgemm_kernel<4, 4, SET, GATHER, 1>;
+  SSSVD_CUDA_TRY(set_kernel_smem((const void*)kern, zgemm_sub_smem(), false));
+  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch);
+  kern<<<grid, 128, zgemm_sub_smem(), stream>>>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, stamp,
+                                                  g_prof.cap);
+  return cudaGetLastError();
 }
 
 cudaError_t zgemm_sub(int M, int N, int K, const double2* A, int lda, long long sA,

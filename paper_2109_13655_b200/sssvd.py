@@ -117,10 +117,11 @@ EXPORTED_SYMBOLS = [
     "sssvd_gpu_run_solve", "sssvd_result_info_get", "sssvd_result_copy", "sssvd_result_note",
     "sssvd_result_free", "sssvd_contour", "sssvd_random_start", "sssvd_validate_params",
     "sssvd_moment_coefficients", "sssvd_build_info", "sssvd_gpu_launch_count", "sssvd_gpu_profile_gemm",
-    "sssvd_gpu_profile_gemm_collect", "sssvd_debug_leaf_profile", "sssvd_debug_gram_part",
+    "sssvd_gpu_profile_gemm_collect", "sssvd_debug_gram_part",
     "sssvd_gpu_set_operator_csc", "sssvd_mm_read", "sssvd_mm_info_get", "sssvd_mm_values", "sssvd_mm_colptr",
     "sssvd_mm_rowind", "sssvd_mm_free", "sssvd_mm_write", "sssvd_host_last_error", "sssvd_build_model",
     "sssvd_filter_profile", "sssvd_debug_thin_qr", "sssvd_debug_svd_square", "sssvd_debug_zgemm",
+    "sssvd_debug_dgemm",
 ]
 
 class _MmInfo(ctypes.Structure):
@@ -167,6 +168,8 @@ def lib():
     L.sssvd_debug_svd_square.argtypes = [vp, dp, i64, dp, dp, dp]
     L.sssvd_debug_zgemm.argtypes = [vp, ctypes.c_int, i64, i64, i64, i64, ctypes.c_int, dp,
                                     ctypes.POINTER(ctypes.c_int64)]
+    L.sssvd_debug_dgemm.argtypes = [vp, ctypes.c_int, ctypes.c_int, i64, i64, i64, ctypes.c_double, dp, i64, dp, i64,
+                                    ctypes.c_double, dp, dp, dp, i64]
     L.sssvd_build_model.argtypes = [ctypes.c_int, i64, i64, ctypes.c_uint64, dp, dp]
     L.sssvd_filter_profile.argtypes = [ctypes.c_double, ctypes.c_double, i64, ctypes.c_double, ctypes.c_int,
                                        ctypes.c_double, ctypes.c_double, i64, ctypes.c_int, dp, dp]
@@ -453,6 +456,41 @@ class Device:
         u, v, sv = np.empty((k, k), order="F"), np.empty((k, k), order="F"), np.empty(k)
         self.check(lib().sssvd_debug_svd_square(self.h, _ptr(b), k, _ptr(u), _ptr(sv), _ptr(v)))
         return u, sv, v
+
+    def dgemm(self, a: np.ndarray, b: np.ndarray, c: Optional[np.ndarray] = None, alpha: float = 1.0,
+              beta: float = 0.0, trans_a: bool = False, lda: Optional[int] = None, ldb: Optional[int] = None,
+              ldc: Optional[int] = None) -> np.ndarray:
+        """Debug: the tail GEMM C = alpha op(A) B + beta C (column-major; optional padded leading
+        dimensions exercise the unaligned staging path)."""
+        a = np.asfortranarray(a, dtype=np.float64)
+        b = np.asfortranarray(b, dtype=np.float64)
+        k, n = b.shape
+        m = a.shape[1] if trans_a else a.shape[0]
+        lda = lda or a.shape[0]
+        ldb = ldb or b.shape[0]
+        ldc = ldc or m
+        ap = np.zeros((lda, a.shape[1]), order="F"); ap[:a.shape[0]] = a
+        bp = np.zeros((ldb, n), order="F"); bp[:k] = b
+        cp = np.zeros((ldc, n), order="F")
+        if c is not None:
+            cp[:m] = c
+        self.check(lib().sssvd_debug_dgemm(self.h, 0, int(trans_a), m, n, k, alpha, _ptr(ap), lda, _ptr(bp), ldb,
+                                           beta, None, None, _ptr(cp), ldc))
+        return cp[:m].copy()
+
+    def dgemm_colnorm_diff(self, a: np.ndarray, b: np.ndarray, d: np.ndarray, v: np.ndarray,
+                           trans_a: bool = False) -> np.ndarray:
+        """Debug: ||op(A) B[:, j] - d_j V[:, j]|| per column through the fused GEMM epilogue."""
+        a = np.asfortranarray(a, dtype=np.float64)
+        b = np.asfortranarray(b, dtype=np.float64)
+        v = np.asfortranarray(v, dtype=np.float64)
+        d = np.ascontiguousarray(d, dtype=np.float64)
+        k, n = b.shape
+        m = a.shape[1] if trans_a else a.shape[0]
+        out = np.zeros(max(m, 1) * n)
+        self.check(lib().sssvd_debug_dgemm(self.h, 1, int(trans_a), m, n, k, 1.0, _ptr(a), a.shape[0], _ptr(b),
+                                           max(k, 1), 0.0, _ptr(d), _ptr(v), _ptr(out), m))
+        return out[:n].copy()
 
     def run_solve(self, config: RunConfig) -> "RunResult":
         c = config._c()

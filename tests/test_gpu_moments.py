@@ -212,48 +212,18 @@ def test_lookahead_schedule_is_bitwise_plain_schedule(dev, monkeypatch):
         assert np.linalg.norm(look[-1][k] - ref[k]) / np.linalg.norm(ref[k]) <= 1e-10
 
 
-def test_staged_back_substitution_is_bitwise_warp_streamed(dev, monkeypatch):
-    """The shared-memory staged back substitution performs the same per-row dot products and warp
-    reductions as the warp-streamed kernel: bitwise-equal moments (n = 700: a ragged last block;
-    L = 12 leaves idle warps in the last CTA)."""
+def test_graph_capture_and_replay_are_bitwise_eager(dev):
+    """The shifted-solve pass runs eagerly on its first sighting, is captured into a CUDA graph on
+    the second and replayed afterwards: all three must give the same moments bit for bit, and match
+    the oracle (n = 700: a ragged last block; a pivot-hungry interval inside the spectrum; L = 12
+    leaves idle warps in the back substitution)."""
     a = constructed(900, 700, np.linspace(0.05, 1.5, 700), 41, 42)
-    rg, _ = rules(0.6, 0.9, 32, 0.1)
+    rg, ro = rules(0.6, 0.9, 32, 0.1)
     s0 = orc.random_start(700, 12, 42)
-    monkeypatch.setenv("SSSVD_TRSM", "warp")
-    ref = gpu_blocks(dev, a, rg, s0, 3)
-    monkeypatch.setenv("SSSVD_TRSM", "smem")
-    for _ in range(3):   # eager, captured, replayed
-        got = gpu_blocks(dev, a, rg, s0, 3)
+    runs = [gpu_blocks(dev, a, rg, s0, 3) for _ in range(3)]   # eager, captured, replayed
+    for r in runs[1:]:
         for k in range(4):
-            assert np.array_equal(ref[k], got[k])
-
-
-def test_leaf_fused_left_swaps_are_bitwise_separate_launch(dev, monkeypatch):
-    """The leaf kernel's epilogue applies its interchanges to the block columns on its left (the
-    separate swap_trsm launch otherwise): pure data movement, so bitwise-equal moments. n = 700
-    with a pivot-hungry shift set (interval inside the spectrum)."""
-    a = constructed(900, 700, np.linspace(0.05, 1.5, 700), 51, 52)
-    rg, _ = rules(0.6, 0.9, 32, 0.1)
-    s0 = orc.random_start(700, 8, 42)
-    monkeypatch.setenv("SSSVD_LEAF_SWAP", "kernel")
-    ref = gpu_blocks(dev, a, rg, s0, 3)
-    monkeypatch.setenv("SSSVD_LEAF_SWAP", "fused")
-    for _ in range(3):   # eager, captured, replayed
-        got = gpu_blocks(dev, a, rg, s0, 3)
-        for k in range(4):
-            assert np.array_equal(ref[k], got[k])
-
-
-def test_staged_panel_prep_is_bitwise_ballot_form(dev, monkeypatch):
-    """panel_prep's staged 8-warp form (L11 rows shared through shared memory, table-driven
-    interchange fold) reproduces the 4-warp ballot form bit for bit."""
-    a = constructed(900, 700, np.linspace(0.05, 1.5, 700), 61, 62)
-    rg, _ = rules(0.6, 0.9, 32, 0.1)
-    s0 = orc.random_start(700, 8, 42)
-    monkeypatch.setenv("SSSVD_PANEL_PREP", "v1")
-    ref = gpu_blocks(dev, a, rg, s0, 3)
-    monkeypatch.setenv("SSSVD_PANEL_PREP", "v2")
-    for _ in range(3):   # eager, captured, replayed
-        got = gpu_blocks(dev, a, rg, s0, 3)
-        for k in range(4):
-            assert np.array_equal(ref[k], got[k])
+            assert np.array_equal(runs[0][k], r[k])
+    ref = orc.MomentAccumulator(orc.form_gram(orc.ProblemMatrix(a)), ro).accumulate(s0, 3).blocks
+    for k in range(4):
+        assert np.linalg.norm(runs[0][k] - ref[k]) / np.linalg.norm(ref[k]) <= 1e-10
