@@ -102,6 +102,14 @@ void sssvd_shard_range(int64_t h, int nranks, int rank, int64_t* begin, int64_t*
  * means `a` is a device pointer on the context's GPU. */
 sssvd_status sssvd_gpu_set_operator(sssvd_gpu_ctx* ctx, const double* a, int64_t rows, int64_t cols,
                                     int64_t lda, int on_device);
+/* Multi-GPU form of set_operator: collective over the context's communicator. Only rank `root`
+ * reads `a` (host or device as on_device says; others may pass NULL); the padded operator is then
+ * sent to every rank with ONE ncclBroadcast over NVLink ("A is broadcast once").
+ * rows/cols must be given on every rank. Without a communicator it is set_operator. */
+sssvd_status sssvd_gpu_set_operator_root(sssvd_gpu_ctx* ctx, const double* a, int64_t rows, int64_t cols,
+                                         int64_t lda, int on_device, int root);
+/* Number of ranks of the context's NCCL communicator (ncclCommCount); 1 without one. */
+sssvd_status sssvd_gpu_comm_size(sssvd_gpu_ctx* ctx, int* nranks);
 /* ProblemMatrix::from_sparse (problem.hpp:27-35) + upload: A given as compressed sparse column
  * (Eigen's SparseMatrix layout) in the user orientation, colptr[cols+1], rowind[nnz] strictly
  * increasing inside each column, values[nnz]; all three are device pointers if on_device != 0.

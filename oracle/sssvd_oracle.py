@@ -8,8 +8,8 @@ The reference (proj/include/sssvd/*.hpp) is header-only C++ on Eigen 3, which is
 here, so it cannot be compiled. This module restates its
 algorithm line by line; each function cites the reference lines it follows. Dense kernels
 come from LAPACK through scipy (OpenBLAS): zgetrf/zgetrs in place of Eigen::PartialPivLU,
-dgeqrf/dorgqr in place of Eigen::HouseholderQR, and dgesvd/dgejsv in place of
-Eigen::JacobiSVD. Seeded inputs are bit-identical to the reference's because they are drawn
+dgeqrf/dorgqr in place of Eigen::HouseholderQR, and the preconditioned one-sided Jacobi
+SVD dgejsv (JOBA='C': no rank truncation) in place of Eigen::JacobiSVD. Seeded inputs are bit-identical to the reference's because they are drawn
 by the same libstdc++ code (oracle/rng.cpp).
 
 Pinning: parity of this oracle is pinned against every known-answer constant and tolerance
@@ -535,9 +535,30 @@ class ReducedBasis:
 
 
 def _svd(mat: np.ndarray):
-    """Backward-stable SVD standing in for Eigen::JacobiSVD (LAPACK dgesvd)."""
-    u, s, vt = sla.svd(mat, full_matrices=False, lapack_driver="gesvd", check_finite=False)
-    return u, s, vt.T
+    """Jacobi SVD standing in for Eigen::JacobiSVD (moments.hpp:199, extract.hpp:68).
+
+    The reference picks a Jacobi method on purpose: it never deflates roundoff-level singular values
+    to zero, so delta = 1e-20 keeps the full direction set (moments.hpp:183-189). LAPACK dgejsv
+    (preconditioned one-sided Jacobi, Drmac-Veselic) with JOBA = 'C' keeps every value above
+    underflow as well (no rank truncation), like the library's QR-preconditioned one-sided Jacobi
+    (csrc/jacobi_svd.cu). Returns (U, sigma nonincreasing, V) with mat = U diag(sigma) V^T; a
+    matrix with fewer rows than columns is decomposed through its transpose (dgejsv needs m >= n).
+    """
+    a = np.asfortranarray(mat, dtype=np.float64)
+    m, n = a.shape
+    if m < n:
+        v, s, u = _svd(a.T)
+        return u, s, v
+    if n == 0:
+        return np.zeros((m, 0)), np.zeros(0), np.zeros((0, 0))
+    sva, u, v, work, _, info = sla.lapack.dgejsv(a, joba=0, jobu=0, jobv=0)
+    if info < 0:
+        raise ValueError(f"dgejsv: illegal argument {-info}")
+    if info > 0:   # no convergence in the Jacobi sweeps: fall back to the bidiagonal SVD
+        u2, s2, vt2 = sla.svd(a, full_matrices=False, lapack_driver="gesvd", check_finite=False)
+        return u2, s2, vt2.T
+    s = sva * (work[1] / work[0])
+    return u[:, :n], s, v[:, :n]
 
 
 def low_rank(stacked: np.ndarray, delta: float) -> ReducedBasis:

@@ -61,17 +61,23 @@ moments_kernel(const double2* __restrict__ mats, int ld, long long stride, int x
 
 cudaError_t moments(const double2* mats, int ld, long long stride, int xcol, int n, int L, int nb,
                     const double2* coef, int M, double* S, cudaStream_t s) {
-  if (M > 32) return cudaErrorInvalidValue;
   const long long nl = (long long)n * L;
   int blocks = (int)std::min<long long>((nl + 255) / 256, 148 * 8);
-  const size_t smem = (size_t)(M + 1) * nb * sizeof(double2);
-  if (M <= 8)
-    moments_kernel<8><<<blocks, 256, smem, s>>>(mats, ld, stride, xcol, n, L, nb, coef, M, S);
-  else if (M <= 16)
-    moments_kernel<16><<<blocks, 256, smem, s>>>(mats, ld, stride, xcol, n, L, nb, coef, M, S);
-  else
-    moments_kernel<32><<<blocks, 256, smem, s>>>(mats, ld, stride, xcol, n, L, nb, coef, M, S);
-  note_launch();
+  // degrees in chunks of at most 33 (the register-resident accumulators): any M the reference
+  // accepts (L M <= n) works; each chunk re-reads X_j once
+  for (int k0 = 0; k0 <= M; k0 += 33) {
+    const int mc = std::min(M - k0, 32);
+    const double2* cc = coef + (size_t)k0 * nb;
+    double* Sk = S + (size_t)k0 * nl;
+    const size_t smem = (size_t)(mc + 1) * nb * sizeof(double2);
+    if (mc <= 8)
+      moments_kernel<8><<<blocks, 256, smem, s>>>(mats, ld, stride, xcol, n, L, nb, cc, mc, Sk);
+    else if (mc <= 16)
+      moments_kernel<16><<<blocks, 256, smem, s>>>(mats, ld, stride, xcol, n, L, nb, cc, mc, Sk);
+    else
+      moments_kernel<32><<<blocks, 256, smem, s>>>(mats, ld, stride, xcol, n, L, nb, cc, mc, Sk);
+    note_launch();
+  }
   return cudaGetLastError();
 }
 

@@ -84,6 +84,8 @@ struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   bool ok = false;
@@ -100,9 +102,12 @@ static NcclApi& nccl() {
       api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
       api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
       api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+      api.Broadcast = (decltype(api.Broadcast))dlsym(h, "ncclBroadcast");
+      api.CommCount = (decltype(api.CommCount))dlsym(h, "ncclCommCount");
       api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
       api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
-      api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy && api.GetErrorString;
+      api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.Broadcast && api.CommDestroy &&
+               api.GetErrorString;
     }
   }
   if (!api.ok) throw Status(SSSVD_E_NCCL, "libnccl.so.2 not found");
@@ -712,6 +717,39 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
   }
 }
 
+// Every rank calls this after its shifted-solve pass and before the moment all-reduce. A failure on
+// any rank (a shift on the spectrum, a device error) is agreed on first (one int all-reduce, max),
+// so every rank throws together instead of the healthy ranks waiting forever in a collective the
+// failed rank never reaches. The reference simply propagates the exception (parallel.hpp:44-50).
+static void agree_status(sssvd_gpu_ctx* ctx, int code, const std::string& msg) {
+  if (ctx->comm && ctx->nranks > 1) {
+    int* d = ctx->scratch.as<int>(2048) + 2046;
+    int h = code;
+    CK(cudaMemcpyAsync(d, &h, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    CKN(nccl().AllReduce(d, d, 1, ncclInt32, ncclMax, ctx->comm, ctx->stream));
+    CK(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (h != SSSVD_OK && code == SSSVD_OK)
+      throw Status((sssvd_status)h, "shifted solves failed on another rank (status " + std::to_string(h) + ")");
+  }
+  if (code != SSSVD_OK) throw Status((sssvd_status)code, msg);
+}
+
+// moment_pass on every rank, then the failure agreement above
+static void moment_pass_agreed(sssvd_gpu_ctx* ctx, const std::vector<std::complex<double>>& shifts,
+                               const std::vector<std::complex<double>>& coef, int64_t h, int64_t jb, int64_t je,
+                               const double* V_dev, int L, int M, double* S_dev) {
+  int code = SSSVD_OK;
+  std::string msg;
+  try {
+    moment_pass(ctx, shifts, coef, h, jb, je, V_dev, L, M, S_dev);
+  } catch (const Status& e) {
+    code = e.code;
+    msg = e.what();
+  }
+  agree_status(ctx, code, msg);
+}
+
 static void allreduce_S(sssvd_gpu_ctx* ctx, double* S, size_t count) {
   if (!ctx->comm) return;   // a 1-rank communicator still runs the collective (exercised by the tests)
   CKN(nccl().AllReduce(S, S, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
@@ -734,6 +772,39 @@ static void finish_operator(sssvd_gpu_ctx* ctx, int64_t m, int64_t n, int64_t ld
   ctx->transposed = tr;
   ctx->has_gram = false;
   ctx->fact_valid = false;
+}
+
+// ProblemMatrix::from_dense (problem.hpp:47-58) into HBM: A (rows x cols, column-major, lda) is
+// staged on the device, transposed there when rows < cols (the reference's auto-transpose), and
+// padded to the internal operator (m x n, m >= n, leading dimension ldp = roundup(m, 8), zero rows)
+static void upload_operator(sssvd_gpu_ctx* ctx, const double* a, int64_t rows, int64_t cols, int64_t lda,
+                            int on_device, int64_t* m_out, int64_t* n_out, int64_t* ldp_out, bool* tr_out) {
+  if (rows <= 0 || cols <= 0 || lda < rows) throw Status(SSSVD_E_INVALID_ARGUMENT, "set_operator: bad shape");
+  if (!a) throw Status(SSSVD_E_INVALID_ARGUMENT, "set_operator: null matrix");
+  cudaStream_t s = ctx->stream;
+  const bool tr = rows < cols;
+  const int64_t m = tr ? cols : rows, n = tr ? rows : cols;
+  const int64_t ldp = (m + 7) / 8 * 8;
+  double* Ad = ctx->A.as<double>((size_t)ldp * n);
+  double* stage;
+  if (on_device) {
+    stage = const_cast<double*>(a);
+  } else {
+    stage = ctx->t0.as<double>((size_t)lda * cols);
+    CK(cudaMemcpyAsync(stage, a, sizeof(double) * lda * cols, cudaMemcpyHostToDevice, s));
+  }
+  if (!tr) {
+    CK(pad_copy(stage, (int)rows, (int)cols, (int)lda, Ad, (int)ldp, s));
+  } else {
+    // A^T into a dense m x n buffer (transpose kernel), then pad
+    double* tmp = ctx->t1.as<double>((size_t)m * n);
+    CK(transpose(stage, (int)rows, (int)cols, (int)lda, tmp, (int)m, s));
+    CK(pad_copy(tmp, (int)m, (int)n, (int)m, Ad, (int)ldp, s));
+  }
+  *m_out = m;
+  *n_out = n;
+  *ldp_out = ldp;
+  *tr_out = tr;
 }
 
 // Gram of the current operator into ctx->G (row-major == column-major, symmetric) + max|G|
@@ -779,6 +850,27 @@ static void dgemm(sssvd_gpu_ctx* ctx, bool ta, int m, int n, int k, double alpha
 }
 
 // thin QR: A (m x k, lda=m) is overwritten by Q; R (k x k upper, ldr = k) returned
+// QR panel plan for m rows: panel width w, 32 halved until the tallest panel's rows fit one
+// cluster (register panel: 16 CTAs x 256 threads x 64 / w rows); beyond that the shared-memory
+// panel (its slab budget; also SSSVD_QR_PANEL=smem). False: no panel holds m rows on chip
+// (about 368k rows at w = 1), checked by run_solve before the shifted-solve phase.
+static bool qr_plan(int m, int* w_out, bool* reg_out) {
+  static const char* pe = std::getenv("SSSVD_QR_PANEL");
+  const bool reg_panel = !(pe && std::string(pe) == "smem");
+  int w = 32, c = 0;
+  if (reg_panel)
+    while (w > 8 && m > 16 * qr_panel_reg_rows(w)) w /= 2;
+  const bool use_reg = reg_panel && m <= 16 * qr_panel_reg_rows(w);
+  if (!use_reg) {
+    w = 32;
+    while (w > 1 && qr_panel_plan(m, w, &c) == 0) w /= 2;
+    if (qr_panel_plan(m, w, &c) == 0) return false;
+  }
+  *w_out = w;
+  *reg_out = use_reg;
+  return true;
+}
+
 static void thin_qr(sssvd_gpu_ctx* ctx, double* A, int m, int k, double* R) {
   // hand-written blocked Householder QR (householder_qr.cu), two levels: cluster panels of w
   // columns, whose updates stay inside an outer block of NBO columns; the outer block's reflectors
@@ -786,21 +878,9 @@ static void thin_qr(sssvd_gpu_ctx* ctx, double* A, int m, int k, double* R) {
   // matrix and in the Q formation as K = NBO DGEMMs (the rank-w updates re-read the whole trailing
   // matrix once per panel)
   cudaStream_t s = ctx->stream;
-  // panel width: 32 columns, halved until the tallest panel's rows fit one cluster (register panel:
-  // 16 CTAs x 256 threads x 64 / w rows; shared-memory panel: its slab budget, the fallback and
-  // SSSVD_QR_PANEL=smem)
-  static const char* pe = std::getenv("SSSVD_QR_PANEL");
-  const bool reg_panel = !(pe && std::string(pe) == "smem");
-  int w = 32, c = 0;
-  if (reg_panel) {
-    while (w > 8 && m > 16 * qr_panel_reg_rows(w)) w /= 2;
-  }
-  const bool use_reg = reg_panel && m <= 16 * qr_panel_reg_rows(w);
-  if (!use_reg) {
-    w = 32;
-    while (w > 1 && qr_panel_plan(m, w, &c) == 0) w /= 2;
-    if (qr_panel_plan(m, w, &c) == 0) throw Status(SSSVD_E_LENGTH, "thin_qr: operator too tall for the on-chip QR panel");
-  }
+  int w = 32;
+  bool use_reg = true;
+  if (!qr_plan(m, &w, &use_reg)) throw Status(SSSVD_E_LENGTH, "thin_qr: operator too tall for the on-chip QR panel");
   static const char* nbo_env = std::getenv("SSSVD_QR_NB");
   // measured (tools/qr_time.py): the merged factor pays off from k ~ 1024 (16384 x 2048: 52 -> 35
   // ms); below, the larft + Y^T Y overhead outweighs the saved re-reads (4096 x 512: 4.4 vs 4.8 ms)
@@ -973,6 +1053,14 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
   const int64_t n = ctx->n, m = ctx->m;
   if (n <= 0) throw Status(SSSVD_E_INVALID_ARGUMENT, "no operator set");
   validate_params(cfg.params, n);
+  {
+    // the tail's Householder panels keep a panel's rows on chip: project_qr factors m rows and
+    // low_rank n rows; refuse up front instead of after the shifted-solve phase
+    int w;
+    bool reg;
+    if (!qr_plan((int)m, &w, &reg) || !qr_plan((int)n, &w, &reg))
+      throw Status(SSSVD_E_LENGTH, "run_solve: operator too tall for the on-chip QR panel of the extraction step");
+  }
   CopyFence copy_fence{ctx->cstream};   // every return path waits for the result copies
   const bool use_exp = cfg.mode == SSSVD_MODE_SS_SVD_NT || cfg.mode == SSSVD_MODE_NAIVE_NT;
   const bool naive = cfg.mode == SSSVD_MODE_NAIVE || cfg.mode == SSSVD_MODE_NAIVE_NT;
@@ -1031,7 +1119,7 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
   for (int64_t nu = 1; nu < cfg.params.refinement_steps; ++nu) {
     // refine (moments.hpp:121-128): S0 <- 2 sum_j Re(w_j X_j) == moment pass with M = 0
     CK(cudaEventRecord(e0, s));
-    moment_pass(ctx, shifts, w, h, jb, je, Vd, L, 0, S);
+    moment_pass_agreed(ctx, shifts, w, h, jb, je, Vd, L, 0, S);
     CK(cudaEventRecord(e1, s));
     allreduce_S(ctx, S, (size_t)n * L);
     CK(cudaEventRecord(e2, s));
@@ -1049,7 +1137,8 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
   // while the shifted-solve pass runs, a helper thread takes the pinned result buffers from the
   // pool at their largest sizes (page-locking hundreds of MB costs ~0.3 s per GB when the pool
   // has to grow)
-  auto reserve = std::async(std::launch::async, [res, m, n, L, M] {
+  auto reserve = std::async(std::launch::async, [res, m, n, L, M, dev = ctx->device] {
+    cudaSetDevice(dev);   // page-locked allocations from this thread must not create a context on GPU 0
     const size_t rmax = (size_t)L * M;
     res->left.resize((size_t)m * rmax);
     res->right.resize((size_t)n * rmax);
@@ -1057,7 +1146,7 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
     res->q.resize(rmax * rmax);
   });
   CK(cudaEventRecord(e0, s));
-  moment_pass(ctx, shifts, coef, h, jb, je, Vd, L, M, S);
+  moment_pass_agreed(ctx, shifts, coef, h, jb, je, Vd, L, M, S);
   CK(cudaEventRecord(e1, s));
   allreduce_S(ctx, S, (size_t)(M + 1) * n * L);
   CK(cudaEventRecord(e2, s));
@@ -1456,30 +1545,59 @@ sssvd_status sssvd_gpu_init_comm(sssvd_gpu_ctx* ctx, const void* uid, int nranks
 sssvd_status sssvd_gpu_set_operator(sssvd_gpu_ctx* ctx, const double* a, int64_t rows, int64_t cols, int64_t lda,
                                     int on_device) {
   return guarded(ctx, [&]() {
-    if (rows <= 0 || cols <= 0 || lda < rows) throw Status(SSSVD_E_INVALID_ARGUMENT, "set_operator: bad shape");
     CK(cudaSetDevice(ctx->device));
-    cudaStream_t s = ctx->stream;
+    int64_t m, n, ldp;
+    bool tr;
+    upload_operator(ctx, a, rows, cols, lda, on_device, &m, &n, &ldp, &tr);
+    finish_operator(ctx, m, n, ldp, tr);
+  });
+}
+
+sssvd_status sssvd_gpu_set_operator_root(sssvd_gpu_ctx* ctx, const double* a, int64_t rows, int64_t cols,
+                                         int64_t lda, int on_device, int root) {
+  return guarded(ctx, [&]() {
+    CK(cudaSetDevice(ctx->device));
+    if (!ctx->comm || ctx->nranks <= 1) {   // a single rank: plain upload
+      int64_t m, n, ldp;
+      bool tr;
+      upload_operator(ctx, a, rows, cols, lda, on_device, &m, &n, &ldp, &tr);
+      finish_operator(ctx, m, n, ldp, tr);
+      return;
+    }
+    if (root < 0 || root >= ctx->nranks) throw Status(SSSVD_E_INVALID_ARGUMENT, "set_operator_root: bad root");
+    if (rows <= 0 || cols <= 0) throw Status(SSSVD_E_INVALID_ARGUMENT, "set_operator: bad shape");
     const bool tr = rows < cols;
     const int64_t m = tr ? cols : rows, n = tr ? rows : cols;
     const int64_t ldp = (m + 7) / 8 * 8;
+    int code = SSSVD_OK;
+    std::string msg;
+    if (ctx->rank == root) {
+      try {
+        int64_t m2, n2, ldp2;
+        bool tr2;
+        upload_operator(ctx, a, rows, cols, lda, on_device, &m2, &n2, &ldp2, &tr2);
+      } catch (const Status& e) {
+        code = e.code;
+        msg = e.what();
+      }
+    }
+    agree_status(ctx, code, msg);   // the root's upload failed: every rank returns its status
+    // one broadcast of the padded internal operator (ldp x n, m >= n) from the root over NVLink
     double* Ad = ctx->A.as<double>((size_t)ldp * n);
-    // stage the user matrix on the device, then pad (and transpose if needed) on the device
-    double* stage;
-    if (on_device) {
-      stage = const_cast<double*>(a);
-    } else {
-      stage = ctx->t0.as<double>((size_t)lda * cols);
-      CK(cudaMemcpyAsync(stage, a, sizeof(double) * lda * cols, cudaMemcpyHostToDevice, s));
-    }
-    if (!tr) {
-      CK(pad_copy(stage, (int)rows, (int)cols, (int)lda, Ad, (int)ldp, s));
-    } else {
-      // A^T into a dense m x n buffer (transpose kernel), then pad
-      double* tmp = ctx->t1.as<double>((size_t)m * n);
-      CK(transpose(stage, (int)rows, (int)cols, (int)lda, tmp, (int)m, s));
-      CK(pad_copy(tmp, (int)m, (int)n, (int)m, Ad, (int)ldp, s));
-    }
+    CKN(nccl().Broadcast(Ad, Ad, (size_t)ldp * n, ncclDouble, root, ctx->comm, ctx->stream));
     finish_operator(ctx, m, n, ldp, tr);
+  });
+}
+
+sssvd_status sssvd_gpu_comm_size(sssvd_gpu_ctx* ctx, int* nranks) {
+  return guarded(ctx, [&]() {
+    if (!ctx->comm) {
+      *nranks = 1;
+      return;
+    }
+    int c = ctx->nranks;
+    if (nccl().CommCount) CKN(nccl().CommCount(ctx->comm, &c));
+    *nranks = c;
   });
 }
 
@@ -1765,12 +1883,12 @@ sssvd_status sssvd_gpu_moments(sssvd_gpu_ctx* ctx, int64_t h, const double* shif
     CK(cudaMemcpyAsync(Vd, s0, sizeof(double) * n * L, cudaMemcpyHostToDevice, s));
     double* S = ctx->S.as<double>((size_t)(M + 1) * n * L);
     for (int64_t nu = 1; nu < ell; ++nu) {
-      moment_pass(ctx, z, w, h, jb, je, Vd, (int)L, 0, S);
+      moment_pass_agreed(ctx, z, w, h, jb, je, Vd, (int)L, 0, S);
       allreduce_S(ctx, S, (size_t)n * L);
       CK(blocks_to_colmajor(S, (int)n, (int)L, 1, Vd, s));
     }
     auto coef = moment_coefficients(w, t, h, M);
-    moment_pass(ctx, z, coef, h, jb, je, Vd, (int)L, (int)M, S);
+    moment_pass_agreed(ctx, z, coef, h, jb, je, Vd, (int)L, (int)M, S);
     allreduce_S(ctx, S, (size_t)(M + 1) * n * L);
     double* Sc = ctx->t0.as<double>((size_t)(M + 1) * n * L);
     CK(blocks_to_colmajor(S, (int)n, (int)L, (int)M + 1, Sc, s));

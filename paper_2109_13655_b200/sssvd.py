@@ -113,7 +113,7 @@ class _Info(ctypes.Structure):
 EXPORTED_SYMBOLS = [
     "sssvd_default_config", "sssvd_gpu_create", "sssvd_gpu_destroy", "sssvd_gpu_last_error",
     "sssvd_gpu_set_batch", "sssvd_gpu_nccl_unique_id", "sssvd_gpu_init_comm", "sssvd_shard_range",
-    "sssvd_gpu_set_operator", "sssvd_gpu_form_gram", "sssvd_gpu_shifted_solve", "sssvd_gpu_moments",
+    "sssvd_gpu_set_operator", "sssvd_gpu_set_operator_root", "sssvd_gpu_comm_size", "sssvd_gpu_form_gram", "sssvd_gpu_shifted_solve", "sssvd_gpu_moments",
     "sssvd_gpu_run_solve", "sssvd_result_info_get", "sssvd_result_copy", "sssvd_result_note",
     "sssvd_result_free", "sssvd_contour", "sssvd_random_start", "sssvd_validate_params",
     "sssvd_moment_coefficients", "sssvd_build_info", "sssvd_gpu_launch_count", "sssvd_gpu_profile_gemm",
@@ -152,6 +152,8 @@ def lib():
     L.sssvd_shard_range.argtypes = [i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.sssvd_shard_range.restype = None
     L.sssvd_gpu_set_operator.argtypes = [vp, dp, i64, i64, i64, ip]
+    L.sssvd_gpu_set_operator_root.argtypes = [vp, dp, i64, i64, i64, ip, ip]
+    L.sssvd_gpu_comm_size.argtypes = [vp, ctypes.POINTER(ctypes.c_int)]
     L.sssvd_gpu_set_operator_csc.argtypes = [vp, i64, i64, i64, dp, dp, dp, ip]
     L.sssvd_gpu_form_gram.argtypes = [vp, i64, dp]
     L.sssvd_mm_read.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
@@ -428,6 +430,19 @@ class Device:
             self.set_operator_csc(s.shape[0], s.shape[1], s.indptr, s.indices, s.data)
         else:
             self.set_operator(a.dense().T if a.transposed() else a.dense())
+
+    def set_operator_root(self, a_ptr: Optional[int], rows: int, cols: int, lda: int, on_device: bool = False,
+                          root: int = 0):
+        """Collective upload: rank `root` passes the operator (host or device pointer), the other
+        ranks None; one ncclBroadcast of the padded operator reaches every rank."""
+        self.check(lib().sssvd_gpu_set_operator_root(self.h, ctypes.c_void_p(a_ptr) if a_ptr else None, rows, cols,
+                                                     lda, int(on_device), root))
+        self._n = min(rows, cols)
+
+    def comm_size(self) -> int:
+        c = ctypes.c_int(0)
+        self.check(lib().sssvd_gpu_comm_size(self.h, ctypes.byref(c)))
+        return c.value
 
     def set_operator_device(self, ptr: int, rows: int, cols: int, lda: int):
         self.check(lib().sssvd_gpu_set_operator(self.h, ctypes.c_void_p(ptr), rows, cols, lda, 1))
