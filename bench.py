@@ -1,24 +1,33 @@
 """Benchmark: time-to-triplets of the block SS-SVD shifted-solve path on B200 (BASELINE.json).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
 
-One step = one run_solve per solve mode of the workload (config 2: NT off and NT on, as
-BASELINE.json configs[1] states "both run"), i.e. time-to-triplets for the config.
-  value : device time (CUDA events on the library stream, max over ranks) of a step with the
-          operator already resident in HBM (set_operator from a device pointer)
-  e2e   : the same step through the public C ABI from pinned HOST memory: H2D of A, the solve,
-          and D2H of every triplet (sigma, u, v, tau, residuals) inside the timed region
-Multi-GPU (torchrun, one rank per GPU, NCCL): the h quadrature points are sharded contiguously
-over the ranks (sssvd_shard_range) and the partial moment blocks are summed with one NCCL
-all-reduce inside the library; total work is fixed ("strong" scaling).
---impl reference times the reference algorithm's CPU restatement (oracle/, numpy + LAPACK over
-all host threads) on a bounded sample of the same workload (see cpu_baseline.sample).
+The workload is BASELINE config 5 by default (16384 x 16384, L=128, M=16, N=128: the largest
+configuration and the one the north-star targets name); --config 1..4 selects the others.
+
+One step = one end-to-end solve through the public C ABI, per solve mode of the config:
+  sssvd_gpu_set_operator(_root) from pinned HOST memory (H2D + pad + NaN check), then
+  sssvd_gpu_run_solve (Gram, shifted solves + moments, tail, postprocess), whose results (sigma,
+  tau, residuals, triplet vectors, moment blocks) are copied to host memory before it returns.
+CUDA events on the current stream bracket each step (the library calls return synchronised):
+  e2e   : from before the operator upload to the end of run_solve (H2D and D2H included);
+  value : from the end of the upload (the operator is resident in HBM) to the end of run_solve.
+Multi-GPU (one rank per GPU, NCCL): the h = N/2 quadrature points are sharded contiguously over
+the ranks, rank 0 uploads A and ONE ncclBroadcast sends it to the others, the partial moment
+blocks are summed with one ncclAllReduce inside the library; total work is fixed ("strong"). The
+step time is the max over ranks. `--gpus N` without torchrun re-launches itself under
+torch.distributed.run with N ranks.
+
+--impl reference times the reference algorithm on the host cores: the CPU restatement of
+run_solve (oracle/, numpy + LAPACK over all host threads; the reference itself needs Eigen, absent
+here), as a bounded sample per step (see cpu_sample()).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -30,12 +39,8 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "time-to-triplets (s)"
-PEAKS = {}
-try:
-    PEAKS = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-except Exception:
-    pass
-FP64_PEAK_TFLOPS = 37.1   # measured: DMMA probe, profiles/r01_fp64_peaks.json (cuBLAS ZGEMM 36.8)
+FP64_PEAK_TFLOPS = 37.1   # measured DMMA probe, profiles/r01_fp64_peaks.json (MEASURED_PEAKS.json has no FP64 entry)
+ZGEMM_PROFILE = os.path.join(ROOT, "profiles", "r02_ncu_zgemm_cfg5.json")
 
 
 def parse():
@@ -43,10 +48,25 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--config", type=int, default=2)
+    p.add_argument("--config", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
+
+
+def relaunch_distributed(args):
+    """`bench.py --gpus N` outside torchrun: run N ranks under torch.distributed.run (127.0.0.1)."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")   # keep stdout to the one JSON line
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd, env=env))
 
 
 class Clocks:
@@ -61,8 +81,8 @@ class Clocks:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, text=True)
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except Exception:
             self.proc = None
@@ -78,53 +98,116 @@ class Clocks:
             self.proc.wait()
 
     def summary(self):
-        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(s[0]) for s in self.samples if s and num(s[0]) is not None]
+        mx = [num(s[1]) for s in self.samples if len(s) > 1 and num(s[1]) is not None]
+        pw = [num(s[7]) for s in self.samples if len(s) > 7 and num(s[7]) is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and s[3 + i] == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(sm)}
+                "reasons": reasons, "samples": len(sm), "power_w_max": max(pw) if pw else None}
+
+
+# ----------------------------------------------------------------------------- CPU sample
+def cpu_sample(w, a, steps, warmup, log=None):
+    """The reference algorithm on the host cores (oracle/: the CPU restatement of run_solve with
+    numpy + LAPACK over all host threads), as a bounded sample of the config's run_solve:
+      * once (first warm-up step): form_gram (problem.hpp:81-95) and the tail (steps 3-5 +
+        postprocess, pipeline.hpp:141-231) on stacked blocks [V, G V, .., G^M V] of the moment
+        blocks' shapes (the tail's cost is set by the shapes, not the values);
+      * every step: ONE full-size shifted factorisation + block solve + its moment update
+        (shifted_solver.hpp:20-40, moments.hpp:132-147) at shift j = step mod h.
+    Per-step estimate of run_solve = h * t_shift + t_gram + t_tail (summed over the modes)."""
+    from oracle import sssvd_oracle as orc
+    A = orc.ProblemMatrix(a)
+    h = w.N // 2
+    t0 = time.perf_counter()
+    gram = orc.form_gram(A, 1 << 30)
+    t_gram = time.perf_counter() - t0
+    absmax = float(np.abs(gram).max())
+    v0 = orc.random_start(w.n, w.L, 42)
+    t_tail = {}
+    rules = {}
+    for mode in w.modes:
+        rules[mode] = orc.ContourRule(w.a, w.b, w.N, 0.1, orc.SpectralTransform(orc.EXP if mode == 1 else orc.IDENTITY))
+    for mode in w.modes:
+        blocks, x = [], v0.copy()
+        for _ in range(w.M + 1):
+            blocks.append(x / np.linalg.norm(x))
+            x = gram @ blocks[-1]
+        res = orc.RunResult(input_transposed=A.transposed)
+        res.blocks, res.starting_norm = orc.MomentBlocks(blocks), float(np.linalg.norm(v0))
+        cfg = orc.RunConfig(w.a, w.b, mode=[orc.SS_SVD, orc.SS_SVD_NT][mode],
+                            params=orc.SsParams(block_size=w.L, moment_degree=w.M, quadrature_count=w.N))
+        t0 = time.perf_counter()
+        orc.finish_solve(A, cfg, res, gram)
+        t_tail[mode] = time.perf_counter() - t0
+    per_step = []
+    for i in range(warmup + steps):
+        dt = 0.0
+        for mode in w.modes:
+            rule = rules[mode]
+            j = i % h
+            t0 = time.perf_counter()
+            x = orc.ShiftedFactorization(gram, rule.shift(j), absmax).solve(v0)
+            s = np.zeros_like(v0)
+            p = complex(1.0)
+            for _ in range(w.M + 1):
+                s += 2.0 * (complex(rule.weights[j]) * p * x).real
+                p *= complex(rule.nodes[j])
+            dt_shift = time.perf_counter() - t0
+            dt += h * dt_shift + t_gram + t_tail[mode]
+        if i >= warmup:
+            per_step.append(dt)
+        if log:
+            log(f"[cpu] step {i}: estimate {dt:.1f} s (shift sample {dt_shift:.2f} s)")
+    cores = os.cpu_count()
+    sample = (f"{w.name}: per step one full-size shifted LU + block solve + moment update "
+              f"(n={w.n}, L={w.L}) at shift j = step mod {h}, per mode; form_gram ({t_gram:.2f} s) and the tail "
+              f"({', '.join(f'{v:.2f} s' for v in t_tail.values())}) timed once on blocks of the moment shapes; "
+              f"value = sum over modes of {h} * t_shift + t_gram + t_tail; numpy/OpenBLAS on {cores} host threads")
+    return float(np.mean(per_step)), cores, sample
 
 
 def run_reference(args, rank, world):
-    """CPU arm: the oracle restatement on this host's cores (rank 0 only)."""
+    """CPU arm (rank 0 only; other ranks exit without work)."""
     if rank != 0:
         return
     from paper_2109_13655_b200 import workloads
-    from oracle import sssvd_oracle as orc
     w = workloads.CONFIGS[args.config]
-    a, sigma = workloads.make_operator(args.config, use_torch=False)
-    A = orc.ProblemMatrix(a)
-    # bounded sample: one full run_solve of the first mode; the other mode repeats the same
-    # steps 1-2 work on the same shapes, so the step time is scaled by the mode count
-    mode = w.modes[0]
-    ocfg = orc.RunConfig(w.a, w.b, mode=[orc.SS_SVD, orc.SS_SVD_NT][mode],
-                         params=orc.SsParams(block_size=w.L, moment_degree=w.M, quadrature_count=w.N))
-    times = []
-    for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        orc.run_solve(A, ocfg, gram_cap=1 << 30)
-        dt = (time.perf_counter() - t0) * len(w.modes)
-        if i >= args.warmup:
-            times.append(dt)
-    v = float(np.mean(times))
-    cores = os.cpu_count()
-    sample = (f"{w.name}: oracle run_solve of mode {mode} (all {w.N // 2} shifts, full tail) per step, "
-              f"x{len(w.modes)} modes; numpy/OpenBLAS on {cores} host threads")
+    a, _ = workloads.make_operator(args.config)
+    sha = workloads.sha256(a)
+    v, cores, sample = cpu_sample(w, a, args.steps, args.warmup, log=lambda s: print(s, file=sys.stderr, flush=True))
     print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": world,
                       "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
                       "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                      "config": {"workload": w.description, "m": w.m, "n": w.n, "L": w.L, "M": w.M, "N": w.N},
+                      "config": config_block(w, world), "input_sha256": sha,
                       "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "port", "sample": sample},
                       "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
           flush=True)
 
 
+def config_block(w, world):
+    return {"workload": w.description, "m": w.m, "n": w.n, "L": w.L, "M": w.M, "N": w.N,
+            "modes": ["ss-svd" if m == 0 else "ss-svd-nt" for m in w.modes],
+            "parallelism": f"quadrature points sharded over {world} GPU(s), A broadcast once, 1 NCCL all-reduce",
+            "l2": "inputs larger than L2 (A and every shifted factor exceed the 126 MB L2)"}
+
+
+# ----------------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_distributed(args)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.warmup < 3:
+        args.warmup = 3
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -141,173 +224,128 @@ def main():
         uid = [sssvd.Device.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         dev.init_comm(uid[0], world, rank)
+    comm_nranks = dev.comm_size()
 
-    a, sigma = workloads.make_operator(args.config)
-    a_dev = torch.from_numpy(a.T.copy()).cuda()   # column-major A == row-major A^T, resident in HBM
-    a_pin = torch.from_numpy(np.ascontiguousarray(a.T)).pin_memory()
+    # the operator in pinned host memory on rank 0 (column-major A == row-major A^T)
+    a_pin = a = sha = sigma = None
+    if rank == 0:
+        a_pin = torch.empty((w.n, w.m), dtype=torch.float64).pin_memory()
+        a, sigma = workloads.make_operator(args.config, out=a_pin.numpy())
+        sha = workloads.sha256(a)
     cfgs = [sssvd.RunConfig(w.a, w.b, mode=m, params=sssvd.SsParams(block_size=w.L, moment_degree=w.M,
                                                                      quadrature_count=w.N), gram_cap=1 << 30)
             for m in w.modes]
+    a_ptr = a_pin.data_ptr() if a_pin is not None else None
 
     def barrier():
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
 
-    def step_device():
-        dev.set_operator_device(a_dev.data_ptr(), w.m, w.n, w.m)
-        out = []
-        for c in cfgs:
-            out.append(dev.run_solve(c))
+    def step(evs):
+        evs[0].record()
+        if world > 1:
+            dev.set_operator_root(a_ptr, w.m, w.n, w.m, on_device=False, root=0)
+        else:
+            dev.check(sssvd.lib().sssvd_gpu_set_operator(dev.h, sssvd.ctypes.c_void_p(a_ptr), w.m, w.n, w.m, 0))
+        evs[1].record()
+        out = [dev.run_solve(c) for c in cfgs]
+        for r in out:   # results are in host memory when run_solve returns; read the small fields
+            _ = (r.triplets.sigma[:1], r.tau[:1], r.exact[:1])
+        evs[2].record()
         return out
 
-    e2e_parts = []
-
-    def step_e2e():
-        # public API from host memory: H2D of A inside, D2H of all triplets inside
-        lib = sssvd.lib()
-        t0 = time.perf_counter()
-        dev.check(lib.sssvd_gpu_set_operator(dev.h, sssvd.ctypes.c_void_p(a_pin.data_ptr()), w.m, w.n, w.m, 0))
-        parts = [time.perf_counter() - t0]
-        out = []
-        for c in cfgs:
-            t0 = time.perf_counter()
-            out.append(dev.run_solve(c))
-            parts.append(time.perf_counter() - t0)
-        e2e_parts.append([round(x * 1e3, 2) for x in parts])
-        return out
-
-    # GEMM timing is on from the first warm-up step: the library captures the shifted-solve pass
-    # into a CUDA graph on its second run, keyed (among others) by the profiling state
+    # GEMM stamps on from the first warm-up step: the library captures the shifted-solve pass into
+    # a CUDA graph on its second run, keyed (among others) by the profiling state
     sssvd.profile_gemm(True)
     for _ in range(args.warmup):
-        res = step_device()
+        res = step([torch.cuda.Event(enable_timing=True) for _ in range(3)])
     barrier()
     sssvd.profile_gemm_collect()   # discard the warm-up timings
-    # ---- timed region (device events on the current stream bracket library work that is
-    #      synchronised inside run_solve; CUDA events + synchronize on both sides)
     launches0 = sssvd.launch_count()
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    ev0, ev1 = evs[0], evs[-1]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    phases = []
     with Clocks(local) as clk:
-        # nvidia-smi's start-up touches the driver; let it reach its sampling loop before the
-        # timed region so the first timed step does not absorb it
         t_wait = time.perf_counter()
         while not clk.samples and time.perf_counter() - t_wait < 3.0:
             time.sleep(0.05)
         time.sleep(0.2)
         barrier()
-        ev0.record()
         for i in range(args.steps):
-            res = step_device()
-            evs[i + 1].record()
+            res = step(evs[i])
+            phases.append(res)
         barrier()
     launches = sssvd.launch_count() - launches0
     gemm_ms, gemm_flops, gemm_launches = sssvd.profile_gemm_collect()
     sssvd.profile_gemm(False)
-    t = ev0.elapsed_time(ev1) / 1e3 / args.steps
+    e2e_steps = [e[0].elapsed_time(e[2]) / 1e3 for e in evs]
+    val_steps = [e[1].elapsed_time(e[2]) / 1e3 for e in evs]
+    t, te = float(np.mean(val_steps)), float(np.mean(e2e_steps))
     if dist:
-        tt = torch.tensor([t], device="cuda")
+        tt = torch.tensor([t, te], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t = float(tt.item())
-    # ---- e2e through the public API with host buffers (same W warm-up steps as the device leg:
-    #      the library's pinned result pool reaches its steady state there)
-    for _ in range(max(1, args.warmup)):
-        res_e = step_e2e()
-    barrier()
-    e2e_parts.clear()
-    t0 = time.perf_counter()
-    e2e_marks = [t0]
-    for _ in range(args.steps):
-        res_e = step_e2e()   # returns after the results are in host memory
-        e2e_marks.append(time.perf_counter())
-    barrier()
-    te = (time.perf_counter() - t0) / args.steps
-    if dist:
-        tt = torch.tensor([te], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        te = float(tt.item())
-    h2d = a.nbytes + len(cfgs) * (w.n * w.L * 8)
-    d2h = sum(r.triplets.left.nbytes + r.triplets.right.nbytes + 5 * r.triplets.sigma.nbytes +
-              sum(b.nbytes for b in r.blocks.blocks) for r in res_e)
-
-    # phase-level FP64 roofline (north star): shifted-solve flops / device time of the phase
-    dt = res[0].device_times
-    h_local = None
-    solve_s = sum(r.device_times["shifted_solves_s"] for r in res)
-    solve_flops = sum(r.device_times["shifted_solve_flops"] for r in res)
+        t, te = float(tt[0]), float(tt[1])
+    last = phases[-1]
+    h2d = (a.nbytes if a is not None else 0)
+    d2h = sum(r.triplets.left.nbytes + r.triplets.right.nbytes + 6 * r.triplets.sigma.nbytes + r.triplets.q.nbytes +
+              sum(b.nbytes for b in r.blocks.blocks) for r in last)
+    solve_s = sum(r.device_times["shifted_solves_s"] for r in last)
+    solve_flops = sum(r.device_times["shifted_solve_flops"] for r in last)
     gemm_tflops = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
-    counts = [{"mode": c.mode, "nonspurious_in_interval": r.count_nonspurious_in_interval,
-               "in_interval": r.count_in_interval, "boundary": r.count_boundary} for c, r in zip(cfgs, res)]
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.config)
+        try:
+            v, cores, sample = cpu_sample(w, a, 1, 0)
+            cpu = {"value": v, "unit": "s", "cores": cores, "kind": "port", "sample": sample}
+        except Exception as e:  # reported, never required
+            cpu = {"value": None, "unit": "s", "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
+    traffic = None
+    prof = {}
+    if os.path.exists(ZGEMM_PROFILE):
+        prof = json.load(open(ZGEMM_PROFILE))
+        traffic = prof.get("dram_bytes_per_launch")
     if rank == 0:
         line = {
             "metric": METRIC, "value": t, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": False, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": w.description, "m": w.m, "n": w.n, "L": w.L, "M": w.M, "N": w.N,
-                       "modes": ["ss-svd" if m == 0 else "ss-svd-nt" for m in w.modes],
-                       "parallelism": f"shift-sharded x{world} (+1 NCCL all-reduce)",
-                       "l2": "inputs larger than L2: A 134 MB, 16 factors x 272 MB per mode"},
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded A = U diag(sigma) V^T, GPU-generated)",
+            "config": config_block(w, world),
             "e2e": {"value": te, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                    "step_ms": [round((e2e_marks[i + 1] - e2e_marks[i]) * 1e3, 3) for i in range(args.steps)],
-                    "parts_ms": e2e_parts},   # per step: set_operator, then run_solve per mode
-            "roofline": {"bound": "tensor", "kernel": "zgemm_sub_kernel (DMMA trailing update)",
+                    "step_s": [round(x, 4) for x in e2e_steps]},
+            "roofline": {"bound": "tensor", "kernel": "zgemm_kernel (DMMA trailing update of the blocked LU)",
                          "achieved": gemm_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": (gemm_tflops / FP64_PEAK_TFLOPS) if gemm_tflops else None,
-                         # one ncu --set full capture of a large trailing update (profiles/
-                         # r01_ncu_zgemm_loader.txt): M=3968 N=4000 K=128 complex x 8 shifts
-                         "traffic": 2.162800e9 + 1.976943e9,
-                         "traffic_launch": {"shape": "M=3968 N=4000 K=128 complex, batch 8",
-                                            "algorithmic_bytes": 8 * 16 * (2 * 3968 * 4000 + 3968 * 128 + 128 * 4000),
-                                            "dram_bytes": 2.162800e9 + 1.976943e9, "ncu_duration_ms": 4.19392,
-                                            "ncu_tflops": 1.300e11 / 4.19392e-3 / 1e12,
-                                            "ncu_dmma_pipe_active": 0.849},
-                         "achieved_basis": "GEMM flops / GEMM-busy time (union of the launch intervals, CUDA events "
-                                           "on the launching streams; the shift groups overlap their GEMMs)",
-                         "peak_source": "measured FP64 DMMA probe (profiles/r01_fp64_peaks.json); MEASURED_PEAKS.json has no FP64 entry",
-                         "gemm_launches": gemm_launches, "gemm_busy_ms_per_step": gemm_ms / args.steps,
+                         "traffic": traffic,
+                         "traffic_launch": prof or None,
+                         "achieved_basis": "algorithmic GEMM flops (8 M N K per complex launch) / GEMM-busy time (union "
+                                           "of the launch intervals from %globaltimer stamps; the shift groups overlap "
+                                           "their GEMMs), rank 0",
+                         "peak_source": "measured FP64 DMMA probe (tools/fp64_peak.cu, profiles/r01_fp64_peaks.json); "
+                                        "MEASURED_PEAKS.json has no FP64 entry",
+                         "gemm_launches": gemm_launches, "gemm_busy_s_per_step": gemm_ms / 1e3 / args.steps,
                          "phase_tflops": solve_flops / solve_s / 1e12 if solve_s > 0 else None,
                          "phase_frac": (solve_flops / solve_s / 1e12 / FP64_PEAK_TFLOPS) if solve_s > 0 else None,
                          "phase_flops_per_step": solve_flops, "phase_s_per_step": solve_s},
-            "phases_s": {"steps_1_2": sum(r.timings.steps_1_2 for r in res), "step_3": sum(r.timings.step_3 for r in res),
-                         "step_4": sum(r.timings.step_4 for r in res), "step_5": sum(r.timings.step_5 for r in res),
-                         "postprocess": sum(r.timings.postprocess for r in res), "gram": dt["gram_s"],
-                         "allreduce": sum(r.device_times["allreduce_s"] for r in res)},
-            "counts": counts,
+            "phases_s": {"steps_1_2": sum(r.timings.steps_1_2 for r in last),
+                         "step_3": sum(r.timings.step_3 for r in last), "step_4": sum(r.timings.step_4 for r in last),
+                         "step_5": sum(r.timings.step_5 for r in last),
+                         "postprocess": sum(r.timings.postprocess for r in last),
+                         "gram": last[0].device_times["gram_s"],
+                         "allreduce": sum(r.device_times["allreduce_s"] for r in last)},
+            "counts": [{"mode": c.mode, "nonspurious_in_interval": r.count_nonspurious_in_interval,
+                        "in_interval": r.count_in_interval, "boundary": r.count_boundary} for c, r in zip(cfgs, last)],
             "truth_in_interval": int(np.sum((sigma >= w.a) & (sigma <= w.b))),
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            "step_ms": [round(evs[i].elapsed_time(evs[i + 1]), 3) for i in range(args.steps)],
+            "step_s": [round(x, 4) for x in val_steps],
             "gpu_launches": int(launches // max(1, args.steps)),
             "gpu_launches_timed_region": int(launches),
-            "input_sha256": workloads.sha256(a),
+            "comm_nranks": comm_nranks, "comm_nranks_ok": comm_nranks == world,
+            "input_sha256": sha,
         }
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
-
-
-def cpu_baseline(cfg):
-    """Oracle (reference restatement) on the host cores, bounded sample of the same workload."""
-    try:
-        from paper_2109_13655_b200 import workloads
-        from oracle import sssvd_oracle as orc
-        w = workloads.CONFIGS[cfg]
-        a, _ = workloads.make_operator(cfg, use_torch=False)
-        mode = w.modes[0]
-        ocfg = orc.RunConfig(w.a, w.b, mode=[orc.SS_SVD, orc.SS_SVD_NT][mode],
-                             params=orc.SsParams(block_size=w.L, moment_degree=w.M, quadrature_count=w.N))
-        t0 = time.perf_counter()
-        orc.run_solve(orc.ProblemMatrix(a), ocfg, gram_cap=1 << 30)
-        dt = time.perf_counter() - t0
-        return {"value": dt * len(w.modes), "unit": "s", "cores": os.cpu_count(), "kind": "port",
-                "sample": f"{w.name}: one oracle run_solve (mode {mode}, all shifts, full tail) x{len(w.modes)} modes, "
-                          f"numpy/OpenBLAS on all {os.cpu_count()} host threads"}
-    except Exception as e:  # the baseline is reported, never required
-        return {"value": None, "unit": "s", "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
 
 
 if __name__ == "__main__":

@@ -95,6 +95,10 @@ sssvd_status sssvd_gpu_set_batch(sssvd_gpu_ctx* ctx, int max_shifts_in_flight);
 sssvd_status sssvd_gpu_nccl_unique_id(void* out128);
 sssvd_status sssvd_gpu_init_comm(sssvd_gpu_ctx* ctx, const void* unique_id128, int nranks, int rank);
 void sssvd_shard_range(int64_t h, int nranks, int rank, int64_t* begin, int64_t* end);
+/* The lower-triangle Gram tiles (kGramTile = 64 square, csrc/partition.h) rank `part` of `nparts`
+ * computes in the multi-GPU form_gram: writes up to `cap` (ti, tj) pairs into ij (tile-row, tile-col,
+ * ti >= tj) and returns their count (-1 for bad arguments). Host only; the same decode as the kernel. */
+int64_t sssvd_gram_tiles(int64_t n, int part, int nparts, int32_t* ij, int64_t cap);
 
 /* ---- operator ------------------------------------------------------------------------------ *
  * ProblemMatrix::from_dense (problem.hpp:20-25 auto-transpose when rows < cols, :56-58 NaN

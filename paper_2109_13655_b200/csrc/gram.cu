@@ -9,11 +9,12 @@
 // mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).
 #include "common.cuh"
 #include "kernels.h"
+#include "partition.h"
 
 namespace sssvd_gpu {
 
 namespace {
-constexpr int BM = 64, BK = 32, STAGES = 3, THREADS = 128;
+constexpr int BM = kGramTile, BK = 32, STAGES = 3, THREADS = 128;
 constexpr int LDS = BK + 4;  // 36 doubles (== 4 mod 16): conflict-free 8-byte fragment loads
 constexpr int TILE = BM * LDS;
 
@@ -41,10 +42,8 @@ gram_kernel(const double* __restrict__ A, int lda, int K, int n, double* __restr
   double* Qs = gsm + STAGES * TILE;
   // decode lower-triangle tile (ti >= tj) from the linear block index
   const long long t = (long long)blockIdx.x * nparts + part;
-  int ti = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-  while ((long long)(ti + 1) * (ti + 2) / 2 <= t) ++ti;
-  while ((long long)ti * (ti + 1) / 2 > t) --ti;
-  const int tj = (int)(t - (long long)ti * (ti + 1) / 2);
+  int ti, tj;
+  gram_tile_decode(t, &ti, &tj);
   const int i0 = ti * BM, j0 = tj * BM;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1;
@@ -106,8 +105,7 @@ gram_kernel(const double* __restrict__ A, int lda, int K, int n, double* __restr
 cudaError_t gram(const double* A, int lda, int K, int n, double* G, int ldg, int part, int nparts, cudaStream_t s) {
   const size_t smem = (size_t)2 * STAGES * TILE * sizeof(double);
   SSSVD_CUDA_TRY(set_kernel_smem((const void*)gram_kernel, smem, false));
-  const long long T = (n + BM - 1) / BM;
-  const long long tiles = T * (T + 1) / 2;
+  const long long tiles = gram_tile_total(n);
   const long long mine = (tiles - part + nparts - 1) / nparts;
   if (mine <= 0) return cudaSuccess;
   gram_kernel<<<(unsigned)mine, THREADS, smem, s>>>(A, lda, K, n, G, ldg, part, nparts);

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "host_mirror.h"
+#include "partition.h"
 #include "../../include/sssvd_gpu.h"
 
 namespace sssvd_gpu {
@@ -177,6 +178,21 @@ sssvd_status sssvd_moment_coefficients(int64_t h, const double* weights, const d
 
 void sssvd_shard_range(int64_t h, int nranks, int rank, int64_t* begin, int64_t* end) {
   shard_range(h, nranks, rank, begin, end);
+}
+
+int64_t sssvd_gram_tiles(int64_t n, int part, int nparts, int32_t* ij, int64_t cap) {
+  if (n <= 0 || nparts < 1 || part < 0 || part >= nparts) return -1;
+  const long long total = sssvd_gpu::gram_tile_total(n);
+  int64_t cnt = 0;
+  for (long long t = part; t < total; t += nparts, ++cnt) {
+    if (cnt < cap && ij) {
+      int ti, tj;
+      sssvd_gpu::gram_tile_decode(t, &ti, &tj);
+      ij[2 * cnt] = ti;
+      ij[2 * cnt + 1] = tj;
+    }
+  }
+  return cnt;
 }
 
 }  // extern "C"

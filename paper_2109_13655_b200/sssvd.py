@@ -112,7 +112,7 @@ class _Info(ctypes.Structure):
 
 EXPORTED_SYMBOLS = [
     "sssvd_default_config", "sssvd_gpu_create", "sssvd_gpu_destroy", "sssvd_gpu_last_error",
-    "sssvd_gpu_set_batch", "sssvd_gpu_nccl_unique_id", "sssvd_gpu_init_comm", "sssvd_shard_range",
+    "sssvd_gpu_set_batch", "sssvd_gpu_nccl_unique_id", "sssvd_gpu_init_comm", "sssvd_shard_range", "sssvd_gram_tiles",
     "sssvd_gpu_set_operator", "sssvd_gpu_set_operator_root", "sssvd_gpu_comm_size", "sssvd_gpu_form_gram", "sssvd_gpu_shifted_solve", "sssvd_gpu_moments",
     "sssvd_gpu_run_solve", "sssvd_result_info_get", "sssvd_result_copy", "sssvd_result_note",
     "sssvd_result_free", "sssvd_contour", "sssvd_random_start", "sssvd_validate_params",
@@ -151,6 +151,8 @@ def lib():
     L.sssvd_gpu_init_comm.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int]
     L.sssvd_shard_range.argtypes = [i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.sssvd_shard_range.restype = None
+    L.sssvd_gram_tiles.argtypes = [i64, ctypes.c_int, ctypes.c_int, dp, i64]
+    L.sssvd_gram_tiles.restype = i64
     L.sssvd_gpu_set_operator.argtypes = [vp, dp, i64, i64, i64, ip]
     L.sssvd_gpu_set_operator_root.argtypes = [vp, dp, i64, i64, i64, ip, ip]
     L.sssvd_gpu_comm_size.argtypes = [vp, ctypes.POINTER(ctypes.c_int)]
@@ -365,6 +367,17 @@ def shard_range(h: int, nranks: int, rank: int):
     b, e = ctypes.c_int64(), ctypes.c_int64()
     lib().sssvd_shard_range(h, nranks, rank, ctypes.byref(b), ctypes.byref(e))
     return b.value, e.value
+
+
+def gram_tiles(n: int, nranks: int, rank: int) -> np.ndarray:
+    """The (ti, tj) lower-triangle 64 x 64 tiles of G that `rank` forms in the multi-GPU form_gram
+    (the decode of csrc/partition.h, shared with the kernel)."""
+    cnt = lib().sssvd_gram_tiles(n, rank, nranks, None, 0)
+    if cnt < 0:
+        raise ValueError("gram_tiles: bad arguments")
+    out = np.zeros((max(cnt, 1), 2), dtype=np.int32)
+    lib().sssvd_gram_tiles(n, rank, nranks, _ptr(out), cnt)
+    return out[:cnt]
 
 
 # ----------------------------------------------------------------------------- device context

@@ -59,6 +59,69 @@ def worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
+def gram_worker(rank, world, port, q):
+    """form_gram sharded as on the GPU: this rank forms only the 64 x 64 lower-triangle tiles the
+    library assigns it (sssvd_gram_tiles, the kernel's own decode), zeros elsewhere; one all-reduce
+    (sum) assembles G, which must be bitwise A^T A with each tile written by exactly one rank."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2109_13655_b200 import sssvd
+    a = orc.random_matrix(300, 333, 9)
+    n = a.shape[1]
+    g = np.zeros((n, n))
+    owner = np.zeros((n, n), dtype=np.int64)
+    for ti, tj in sssvd.gram_tiles(n, world, rank):
+        ri, rj = slice(64 * ti, min(n, 64 * ti + 64)), slice(64 * tj, min(n, 64 * tj + 64))
+        g[ri, rj] = a[:, ri].T @ a[:, rj]
+        owner[ri, rj] += 1
+    t, o = torch.from_numpy(g), torch.from_numpy(owner)
+    dist.all_reduce(t)
+    dist.all_reduce(o)
+    if rank == 0:
+        q.put((t.numpy(), o.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_gram_tiles_allreduce(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=gram_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    g, owner = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    a = orc.random_matrix(300, 333, 9)
+    tile_lower = np.add.outer(np.arange(333) // 64, -(np.arange(333) // 64)) >= 0
+    assert np.all(owner[tile_lower] == 1) and np.all(owner[~tile_lower] == 0)
+    full = a.T @ a
+    assert np.allclose(g[tile_lower], full[tile_lower], rtol=0, atol=1e-12)
+    assert np.all(g[~tile_lower] == 0.0)
+
+
+def test_bench_gpus_flag_spawns_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself with 2 ranks (torch.distributed.run);
+    the reference arm runs on rank 0 only and reports the world size (CPU-only: config 1)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--config", "1", "--steps", "1", "--warmup", "3"], capture_output=True, text=True,
+                         timeout=600, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    assert lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference"
+    assert "rank 1" not in out.stdout
+
+
 @pytest.mark.parametrize("world", [2, 4])
 def test_sharded_moments_allreduce(world):
     ctx = mp.get_context("spawn")
