@@ -176,7 +176,8 @@ typedef enum {
   SSSVD_FIELD_RIGHT = 8,      /* double[cols*count] column-major */
   SSSVD_FIELD_BASIS_SV = 9,   /* double[retained_rank] Sigma_S1 */
   SSSVD_FIELD_BLOCKS = 10,    /* double[(M+1)*n_internal*L] moment blocks, column-major */
-  SSSVD_FIELD_Q = 11          /* double[retained_rank*count] column-major */
+  SSSVD_FIELD_Q = 11,         /* double[retained_rank*count] column-major */
+  SSSVD_FIELD_INVALID = 12    /* int32[count] TripletSet::invalid (naive route: theta <= 0) */
 } sssvd_field;
 
 sssvd_status sssvd_result_info_get(const sssvd_gpu_result* res, sssvd_result_info* info);

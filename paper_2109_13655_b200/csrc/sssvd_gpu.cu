@@ -253,7 +253,7 @@ struct sssvd_gpu_result {
   sssvd_result_info info{};
   std::vector<double> sigma, tau, estimated, exact, galerkin, basis_sv;
   PinnedArray left, right, blocks, q;
-  std::vector<int32_t> in_interval, spurious;
+  std::vector<int32_t> in_interval, spurious, invalid;
   std::string note;
 };
 
@@ -1366,6 +1366,7 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
     res->tau = d2h(tau_d, tcount, s);
     res->spurious.resize(tcount);
     for (int i = 0; i < tcount; ++i) res->spurious[i] = (res->tau[i] < info.spurious_threshold) || invalid[i];
+    res->invalid = invalid;
     tp.mark("exact + galerkin residuals");
     res->estimated.assign(norms.begin(), norms.begin() + tcount);
     for (int i = 0; i < tcount; ++i)
@@ -1956,6 +1957,7 @@ sssvd_status sssvd_result_copy(const sssvd_gpu_result* res, int field, void* dst
     case SSSVD_FIELD_BASIS_SV: cp(res->basis_sv); break;
     case SSSVD_FIELD_BLOCKS: cp(res->blocks); break;
     case SSSVD_FIELD_Q: cp(res->q); break;
+    case SSSVD_FIELD_INVALID: cp(res->invalid); break;
     default: return SSSVD_E_INVALID_ARGUMENT;
   }
   return SSSVD_OK;
