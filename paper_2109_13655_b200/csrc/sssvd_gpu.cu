@@ -1730,20 +1730,23 @@ __global__ void debug_diff_kernel(const unsigned long long* a, const unsigned lo
 }
 }  // namespace
 
-// debug: times the trailing-update GEMM C -= A B (complex, row-major, batched) on seeded data;
-// *mismatches_out counts the entries of a second run that differ bitwise from the first
-// (run-to-run determinism). variant must be 0 (the product kernel).
+// debug: times the trailing-update GEMM C -= A B (complex, row-major, batched) on seeded data.
+// variant 0: the product path (TMA kernel), 1: the cp.async kernel. *mismatches_out counts the
+// entries that differ bitwise from the cp.async kernel's result on the same inputs.
 sssvd_status sssvd_debug_zgemm(sssvd_gpu_ctx* ctx, int variant, int64_t m, int64_t n, int64_t k, int64_t batch,
                                int reps, double* ms_out, int64_t* mismatches_out) {
   return guarded(ctx, [&]() {
-    if (m < 1 || n < 1 || k < 1 || batch < 1 || reps < 1 || variant != 0)
+    if (m < 1 || n < 1 || k < 1 || batch < 1 || reps < 1 || variant < 0 || variant > 1)
       throw Status(SSSVD_E_INVALID_ARGUMENT, "debug_zgemm: bad arguments");
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
     const size_t na = (size_t)batch * m * k, nb = (size_t)batch * k * n, nc = (size_t)batch * m * n;
     double2 *A = nullptr, *B = nullptr, *C0 = nullptr, *C1 = nullptr, *C2 = nullptr;
     unsigned long long* cnt = nullptr;
-    auto release = [&]() { cudaFree(A); cudaFree(B); cudaFree(C0); cudaFree(C1); cudaFree(C2); cudaFree(cnt); };
+    auto release = [&]() {
+      zgemm_force_cpasync(false);
+      cudaFree(A); cudaFree(B); cudaFree(C0); cudaFree(C1); cudaFree(C2); cudaFree(cnt);
+    };
     try {
       CK(cudaMalloc(&A, na * sizeof(double2)));
       CK(cudaMalloc(&B, nb * sizeof(double2)));
@@ -1756,8 +1759,10 @@ sssvd_status sssvd_debug_zgemm(sssvd_gpu_ctx* ctx, int variant, int64_t m, int64
       debug_fill_kernel<<<1184, 256, 0, s>>>((double*)C0, 2 * (long long)nc, 3);
       CK(cudaMemcpyAsync(C1, C0, nc * sizeof(double2), cudaMemcpyDeviceToDevice, s));
       CK(cudaMemcpyAsync(C2, C0, nc * sizeof(double2), cudaMemcpyDeviceToDevice, s));
-      CK(zgemm_sub((int)m, (int)n, (int)k, A, (int)k, m * k, B, (int)n, k * n, C1, (int)n, m * n, (int)batch, s));
+      zgemm_force_cpasync(true);
       CK(zgemm_sub((int)m, (int)n, (int)k, A, (int)k, m * k, B, (int)n, k * n, C2, (int)n, m * n, (int)batch, s));
+      zgemm_force_cpasync(variant == 1);
+      CK(zgemm_sub((int)m, (int)n, (int)k, A, (int)k, m * k, B, (int)n, k * n, C1, (int)n, m * n, (int)batch, s));
       CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
       debug_diff_kernel<<<1184, 256, 0, s>>>((const unsigned long long*)C1, (const unsigned long long*)C2,
                                              2 * (long long)nc, cnt);

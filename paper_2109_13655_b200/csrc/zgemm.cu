@@ -12,6 +12,10 @@
 // Shared-memory row pitches are padded (A: 20, B: 66 double2) so every fragment load is one
 // conflict-free LDS.128 per quarter-warp.
 #include <algorithm>
+#include <cstring>
+#include <string>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <atomic>
 #include <map>
 #include <mutex>
@@ -378,6 +382,254 @@ zgemm_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long l
 
 size_t zgemm_sub_smem() { return (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double2); }
 
+
+// ----------------------------------------------------------------------------- TMA form
+// Persistent, warp-specialised form of C -= A B (the same DMMA chain per entry as zgemm_kernel,
+// so bitwise the same result): 4 consumer warps (32 x 32 warp tiles of a 64 x 64 CTA tile) and
+// one producer warp whose elected lane streams the K-stages with TMA (cp.async.bulk.tensor, SASS
+// UTMALDG) into a ring of TMA_STAGES stages guarded by full / empty mbarriers, so the consumers
+// never hit a CTA-wide barrier and the next tile's stages load under this tile's last k-steps
+// and epilogue. Two CTAs per SM: one CTA's epilogue (C read-modify-write) overlaps the other's
+// DMMA main loop. Tiles t = blockIdx.x + i gridDim.x over (shift, m-tile, n-tile).
+// Shared-memory layouts (dense, TMA writes them as is):
+//   A stage: 4 boxes (one per k-quad) of 64 rows x 4 complex (64 B rows, no swizzle): a DMMA A
+//            fragment (rows fr, fr+1 of a phase x 4 k) covers 128 contiguous bytes;
+//   B stage: 8 boxes of 16 k-rows x 8 complex (128 B rows, 128B swizzle: chunk ^= row % 8). Lane
+//            fr of a DMMA B fragment reads column x(fr) = 4 (fr & 1) + fr / 2 of its 8-column box,
+//            so the two columns of a phase sit in opposite halves of the swizzled row.
+constexpr int TMA_STAGES = 3, TMA_THREADS = 160;
+constexpr int TMA_A_BYTES = 64 * BK * 16, TMA_B_BYTES = BK * 64 * 16;
+constexpr int TMA_STAGE_BYTES = TMA_A_BYTES + TMA_B_BYTES;
+constexpr size_t TMA_SMEM = (size_t)TMA_STAGES * TMA_STAGE_BYTES + 1024 + 64;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int c0, int c1, int c2, void* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(void* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__global__ void __maxnreg__(200)
+zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int M, int N,
+                 int K, double2* C, int ldc, long long sC, int batch, unsigned long long* __restrict__ stamp,
+                 int stamp_cap) {
+  extern __shared__ unsigned char tsm_raw[];
+  // 1024-byte aligned ring (the 128B swizzle atom), derived from the shared array itself so the
+  // fragment loads stay LDS
+  unsigned char* base = tsm_raw + (((smem_u32(tsm_raw) + 1023u) & ~1023u) - smem_u32(tsm_raw));
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(base + TMA_STAGES * TMA_STAGE_BYTES);
+  unsigned long long* empty = full + TMA_STAGES;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (stamp && tid == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(stamp, t);
+  }
+  if (tid == 0) {
+    for (int s = 0; s < TMA_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);
+    }
+  }
+  __syncthreads();
+  const int tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
+  const int per = tm * tn, total = per * batch;
+  const int KT = (K + BK - 1) / BK;
+  if (warp == 4) {
+    // ---- producer: one elected lane issues every TMA of every stage of every tile of this CTA
+    if (lane == 0) {
+      int stage = 0;
+      unsigned phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int z = t / per, rem = t - z * per;
+        const int m0 = (rem / tn) * BM, n0 = (rem % tn) * BN;
+        for (int kt = 0; kt < KT; ++kt) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          mbar_expect_tx(&full[stage], TMA_STAGE_BYTES);
+          unsigned char* sa = base + stage * TMA_STAGE_BYTES;
+          unsigned char* sb = sa + TMA_A_BYTES;
+#pragma unroll
+          for (int q = 0; q < BK / 4; ++q) tma_load3(sa + q * (64 * 64), &mapA, 2 * (kt * BK + 4 * q), m0, z, &full[stage]);
+#pragma unroll
+          for (int bx = 0; bx < 8; ++bx) tma_load3(sb + bx * (BK * 128), &mapB, 2 * (n0 + 8 * bx), kt * BK, z, &full[stage]);
+          if (++stage == TMA_STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else {
+    // ---- consumers: warp (wm, wn) owns rows 32 wm.., columns 32 wn.. of each tile
+    const int wm = warp >> 1, wn = warp & 1;
+    const int fr = lane >> 2, fc = lane & 3;
+    const int xcol = 4 * (fr & 1) + (fr >> 1);   // this lane's B column inside an 8-column box
+    int stage = 0;
+    unsigned phase = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const int z = t / per, rem = t - z * per;
+      const int m0 = (rem / tn) * BM, n0 = (rem % tn) * BN;
+      double2* Cz = C + z * sC;
+      // pull this warp's C rows toward L2 while the main loop runs
+      for (int r = lane; r < 32; r += 32) {
+        const int row = m0 + wm * 32 + r;
+        if (row < M) {
+          const char* p = reinterpret_cast<const char*>(Cz + (size_t)row * ldc + n0 + wn * 32);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 128 * c));
+        }
+      }
+      double acc_re[4][4][2], acc_im[4][4][2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          acc_re[i][j][0] = acc_re[i][j][1] = 0.0;
+          acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
+        }
+      for (int kt = 0; kt < KT; ++kt) {
+        mbar_wait(&full[stage], phase);
+        const unsigned char* sa = base + stage * TMA_STAGE_BYTES;
+        const unsigned char* sb = sa + TMA_A_BYTES;
+#pragma unroll
+        for (int kq = 0; kq < BK / 4; ++kq) {
+          double2 a[4], b[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            a[i] = *reinterpret_cast<const double2*>(sa + kq * (64 * 64) + (wm * 32 + i * 8 + fr) * 64 + fc * 16);
+          const int krow = kq * 4 + fc;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            b[j] = *reinterpret_cast<const double2*>(sb + (wn * 4 + j) * (BK * 128) + krow * 128 +
+                                                     ((xcol ^ (krow & 7)) << 4));
+          double nai[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) nai[i] = -a[i].y;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma884(acc_re[i][j][0], acc_re[i][j][1], a[i].x, b[j].x);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma884(acc_im[i][j][0], acc_im[i][j][1], a[i].x, b[j].y);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma884(acc_re[i][j][0], acc_re[i][j][1], nai[i], b[j].y);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma884(acc_im[i][j][0], acc_im[i][j][1], a[i].y, b[j].x);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == TMA_STAGES) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+      // epilogue: accumulator (fr, 2 fc + e) of sub-tile j is tile column 8 (4 wn + j) + 4 e + fc
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = m0 + wm * 32 + i * 8 + fr;
+        if (r >= M) continue;
+        double2* crow = Cz + (size_t)r * ldc + n0;
+        double2 v[4][2];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int c = 8 * (4 * wn + j) + 4 * e + fc;
+            v[j][e] = n0 + c < N ? crow[c] : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int c = 8 * (4 * wn + j) + 4 * e + fc;
+            if (n0 + c < N) crow[c] = make_double2(v[j][e].x - acc_re[i][j][e], v[j][e].y - acc_im[i][j][e]);
+          }
+      }
+    }
+  }
+  if (stamp) {
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMax(stamp + stamp_cap, t);
+    }
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 3-D map over [batch][rows][2 cols] doubles of a row-major complex matrix (pitch ld complex,
+// batch stride sb complex): box = box_cols complex x box_rows rows x 1
+static bool encode_map(CUtensorMap* map, const double2* p, int rows, int cols, int ld, long long sb, int batch,
+                       int box_cols, int box_rows, bool swizzle128) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)2 * cols, (cuuint64_t)rows, (cuuint64_t)batch};
+  const cuuint64_t strides[2] = {(cuuint64_t)ld * 16, (cuuint64_t)std::max<long long>(sb, 1) * 16};
+  const cuuint32_t box[3] = {(cuuint32_t)(2 * box_cols), (cuuint32_t)box_rows, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double2*>(p), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// SSSVD_ZGEMM=cpasync selects the cp.async kernel for the trailing updates (read per call);
+// zgemm_force_cpasync (debug comparisons) overrides
+static int g_force_cpasync = 0;
+void zgemm_force_cpasync(bool on) { g_force_cpasync = on ? 1 : 0; }
+static bool tma_enabled() {
+  if (g_force_cpasync) return false;
+  const char* e = std::getenv("SSSVD_ZGEMM");
+  return !(e && std::string(e) == "cpasync");
+}
+
+static cudaError_t launch_tma(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B, int ldb,
+                              long long sB, double2* C, int ldc, long long sC, int batch, cudaStream_t stream,
+                              unsigned long long* stamp, bool* done) {
+  *done = false;
+  // the pitches and bases must satisfy TMA's 16-byte rules (always true for double2 buffers)
+  if (((uintptr_t)A & 15) || ((uintptr_t)B & 15)) return cudaSuccess;
+  if ((long long)batch > 1 && (sA <= 0 || sB <= 0)) return cudaSuccess;
+  CUtensorMap ma, mb;
+  if (!encode_map(&ma, A, M, K, lda, sA, batch, 4, 64, false)) return cudaSuccess;
+  if (!encode_map(&mb, B, K, N, ldb, sB, batch, 8, BK, true)) return cudaSuccess;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  SSSVD_CUDA_TRY(set_kernel_smem((const void*)zgemm_tma_kernel, TMA_SMEM, false));
+  const long long total = (long long)((M + BM - 1) / BM) * ((N + BN - 1) / BN) * batch;
+  const int grid = (int)std::min<long long>(total, 2LL * sms);
+  zgemm_tma_kernel<<<grid, TMA_THREADS, TMA_SMEM, stream>>>(ma, mb, M, N, K, C, ldc, sC, batch, stamp, g_prof.cap);
+  *done = true;
+  return cudaGetLastError();
+}
+
 // Per-device kernel attributes: cudaFuncSetAttribute applies to the current device only, so the
 // largest dynamic shared-memory size set so far is remembered per (kernel, device).
 cudaError_t set_kernel_smem(const void* fn, size_t bytes, bool nonportable_cluster) {
@@ -415,6 +667,11 @@ static cudaError_t launch(int M, int N, int K, const double2* A, int lda, long l
     g_prof.flops.push_back(8.0 * M * (double)N * K * batch);
   }
   note_launch();
+  if (!SET && !GATHER && tma_enabled()) {
+    bool done = false;
+    SSSVD_CUDA_TRY(launch_tma(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch, stream, stamp, &done));
+    if (done) return cudaSuccess;
+  }
   auto kern = zgemm_kernel<4, 4, SET, GATHER, 1>;
   SSSVD_CUDA_TRY(set_kernel_smem((const void*)kern, zgemm_sub_smem(), false));
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch);

@@ -227,3 +227,16 @@ def test_graph_capture_and_replay_are_bitwise_eager(dev):
     ref = orc.MomentAccumulator(orc.form_gram(orc.ProblemMatrix(a)), ro).accumulate(s0, 3).blocks
     for k in range(4):
         assert np.linalg.norm(runs[0][k] - ref[k]) / np.linalg.norm(ref[k]) <= 1e-10
+
+
+def test_high_moment_degree_chunks(dev):
+    """M = 40 > 32 register-resident accumulators: the moment kernel runs in degree chunks of 33
+    (any M with L M <= n is valid, moments.hpp:35-46); blocks match the oracle's power chain."""
+    a = constructed(160, 120, np.linspace(0.3, 1.6, 120), 71, 72)
+    rg, ro = rules(0.7, 1.1, 16, 0.1)
+    s0 = orc.random_start(120, 2, 42)
+    got = gpu_blocks(dev, a, rg, s0, 40)
+    ref = orc.MomentAccumulator(orc.form_gram(orc.ProblemMatrix(a)), ro).accumulate(s0, 40).blocks
+    assert len(got) == 41
+    for k in range(41):
+        assert np.linalg.norm(got[k] - ref[k]) <= 1e-10 * np.linalg.norm(ref[k]) + 1e-300
