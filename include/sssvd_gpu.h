@@ -227,8 +227,8 @@ sssvd_status sssvd_debug_thin_qr(sssvd_gpu_ctx* ctx, const double* a, int64_t m,
 sssvd_status sssvd_debug_svd_square(sssvd_gpu_ctx* ctx, const double* b, int64_t k, double* u_out, double* s_out,
                                     double* v_out);
 /* Debug: the trailing-update GEMM (C -= A B, complex, row-major, batched; zgemm.cu) on seeded device
- * data, timed over `reps` launches -> ms_out (mean per launch). variant 0 = the product path (the
- * TMA + mbarrier persistent kernel), 1 = the cp.async kernel; mismatches_out = entries of C that
+ * data, timed over `reps` launches -> ms_out (mean per launch). variant 0 = the cp.async kernel (the
+ * product default), 1 = the TMA + mbarrier persistent kernel; mismatches_out = entries of C that
  * differ BITWISE from the cp.async kernel's result on the same inputs. */
 sssvd_status sssvd_debug_zgemm(sssvd_gpu_ctx* ctx, int variant, int64_t m, int64_t n, int64_t k, int64_t batch,
                                int reps, double* ms_out, int64_t* mismatches_out);

@@ -44,8 +44,8 @@ cudaError_t pivot_floor(const double2* mats, int ld, long long stride, int n, co
 cudaError_t zgemm_sub(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B,
                       int ldb, long long sB, double2* C, int ldc, long long sC, int batch,
                       cudaStream_t stream);
-// debug: route zgemm_sub to the cp.async kernel instead of the TMA kernel (zgemm.cu)
-void zgemm_force_cpasync(bool on);
+// debug: route zgemm_sub to 1 = the cp.async kernel, 2 = the TMA kernel, 0 = the default (zgemm.cu)
+void zgemm_force(int kernel);
 // C = A B[brow[k], :] (row-gathered B), row-major complex, batched (zgemm.cu)
 cudaError_t zgemm_set_gather(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B,
                              int ldb, long long sB, const int* brow, int sR, double2* C, int ldc, long long sC,

@@ -722,7 +722,7 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
 // so every rank throws together instead of the healthy ranks waiting forever in a collective the
 // failed rank never reaches. The reference simply propagates the exception (parallel.hpp:44-50).
 static void agree_status(sssvd_gpu_ctx* ctx, int code, const std::string& msg) {
-  if (ctx->comm && ctx->nranks > 1) {
+  if (ctx->comm) {   // a 1-rank communicator runs the collective too (the tests' single-GPU check)
     int* d = ctx->scratch.as<int>(2048) + 2046;
     int h = code;
     CK(cudaMemcpyAsync(d, &h, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
@@ -1558,7 +1558,7 @@ sssvd_status sssvd_gpu_set_operator_root(sssvd_gpu_ctx* ctx, const double* a, in
                                          int64_t lda, int on_device, int root) {
   return guarded(ctx, [&]() {
     CK(cudaSetDevice(ctx->device));
-    if (!ctx->comm || ctx->nranks <= 1) {   // a single rank: plain upload
+    if (!ctx->comm) {   // no communicator: plain upload (a 1-rank communicator broadcasts to itself)
       int64_t m, n, ldp;
       bool tr;
       upload_operator(ctx, a, rows, cols, lda, on_device, &m, &n, &ldp, &tr);
@@ -1731,7 +1731,7 @@ __global__ void debug_diff_kernel(const unsigned long long* a, const unsigned lo
 }  // namespace
 
 // debug: times the trailing-update GEMM C -= A B (complex, row-major, batched) on seeded data.
-// variant 0: the product path (TMA kernel), 1: the cp.async kernel. *mismatches_out counts the
+// variant 0: the cp.async kernel (product default), 1: the TMA kernel. *mismatches_out counts the
 // entries that differ bitwise from the cp.async kernel's result on the same inputs.
 sssvd_status sssvd_debug_zgemm(sssvd_gpu_ctx* ctx, int variant, int64_t m, int64_t n, int64_t k, int64_t batch,
                                int reps, double* ms_out, int64_t* mismatches_out) {
@@ -1744,7 +1744,7 @@ sssvd_status sssvd_debug_zgemm(sssvd_gpu_ctx* ctx, int variant, int64_t m, int64
     double2 *A = nullptr, *B = nullptr, *C0 = nullptr, *C1 = nullptr, *C2 = nullptr;
     unsigned long long* cnt = nullptr;
     auto release = [&]() {
-      zgemm_force_cpasync(false);
+      zgemm_force(0);
       cudaFree(A); cudaFree(B); cudaFree(C0); cudaFree(C1); cudaFree(C2); cudaFree(cnt);
     };
     try {
@@ -1759,9 +1759,9 @@ sssvd_status sssvd_debug_zgemm(sssvd_gpu_ctx* ctx, int variant, int64_t m, int64
       debug_fill_kernel<<<1184, 256, 0, s>>>((double*)C0, 2 * (long long)nc, 3);
       CK(cudaMemcpyAsync(C1, C0, nc * sizeof(double2), cudaMemcpyDeviceToDevice, s));
       CK(cudaMemcpyAsync(C2, C0, nc * sizeof(double2), cudaMemcpyDeviceToDevice, s));
-      zgemm_force_cpasync(true);
+      zgemm_force(1);
       CK(zgemm_sub((int)m, (int)n, (int)k, A, (int)k, m * k, B, (int)n, k * n, C2, (int)n, m * n, (int)batch, s));
-      zgemm_force_cpasync(variant == 1);
+      zgemm_force(variant == 1 ? 2 : 1);
       CK(zgemm_sub((int)m, (int)n, (int)k, A, (int)k, m * k, B, (int)n, k * n, C1, (int)n, m * n, (int)batch, s));
       CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
       debug_diff_kernel<<<1184, 256, 0, s>>>((const unsigned long long*)C1, (const unsigned long long*)C2,

@@ -463,6 +463,7 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         }
       }
     }
+    __syncwarp();   // the producer warp reconverges before the closing barrier
   } else {
     // ---- consumers: warp (wm, wn) owns rows 32 wm.., columns 32 wn.. of each tile
     const int wm = warp >> 1, wn = warp & 1;
@@ -545,14 +546,14 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int c = 8 * (4 * wn + j) + 4 * e + fc;
-            v[j][e] = n0 + c < N ? crow[c] : make_double2(0.0, 0.0);
+            v[j][e] = n0 + c < N ? __ldcg(crow + c) : make_double2(0.0, 0.0);   // L2: never a stale L1 line
           }
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int c = 8 * (4 * wn + j) + 4 * e + fc;
-            if (n0 + c < N) crow[c] = make_double2(v[j][e].x - acc_re[i][j][e], v[j][e].y - acc_im[i][j][e]);
+            if (n0 + c < N) __stcg(crow + c, make_double2(v[j][e].x - acc_re[i][j][e], v[j][e].y - acc_im[i][j][e]));
           }
       }
     }
@@ -596,14 +597,15 @@ static bool encode_map(CUtensorMap* map, const double2* p, int rows, int cols, i
              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// SSSVD_ZGEMM=cpasync selects the cp.async kernel for the trailing updates (read per call);
-// zgemm_force_cpasync (debug comparisons) overrides
-static int g_force_cpasync = 0;
-void zgemm_force_cpasync(bool on) { g_force_cpasync = on ? 1 : 0; }
+// SSSVD_ZGEMM=tma selects the TMA kernel for the trailing updates (read per call; measured slower
+// than the cp.async kernel so far: config-5 phase 28.7 vs 23.2 s); zgemm_force (debug comparisons)
+// overrides: 1 = cp.async, 2 = TMA
+static int g_force = 0;
+void zgemm_force(int kernel) { g_force = kernel; }
 static bool tma_enabled() {
-  if (g_force_cpasync) return false;
+  if (g_force) return g_force == 2;
   const char* e = std::getenv("SSSVD_ZGEMM");
-  return !(e && std::string(e) == "cpasync");
+  return e && std::string(e) == "tma";
 }
 
 static cudaError_t launch_tma(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B, int ldb,

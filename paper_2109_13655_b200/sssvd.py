@@ -494,10 +494,10 @@ class Device:
         b = np.asfortranarray(b, dtype=np.float64)
         k, n = b.shape
         m = a.shape[1] if trans_a else a.shape[0]
-        lda = lda or a.shape[0]
-        ldb = ldb or b.shape[0]
-        ldc = ldc or m
-        ap = np.zeros((lda, a.shape[1]), order="F"); ap[:a.shape[0]] = a
+        lda = max(lda or a.shape[0], 1)
+        ldb = max(ldb or b.shape[0], 1)
+        ldc = max(ldc or m, 1)
+        ap = np.zeros((lda, max(a.shape[1], 1)), order="F"); ap[:a.shape[0], :a.shape[1]] = a
         bp = np.zeros((ldb, n), order="F"); bp[:k] = b
         cp = np.zeros((ldc, n), order="F")
         if c is not None:
@@ -516,7 +516,7 @@ class Device:
         k, n = b.shape
         m = a.shape[1] if trans_a else a.shape[0]
         out = np.zeros(max(m, 1) * n)
-        self.check(lib().sssvd_debug_dgemm(self.h, 1, int(trans_a), m, n, k, 1.0, _ptr(a), a.shape[0], _ptr(b),
+        self.check(lib().sssvd_debug_dgemm(self.h, 1, int(trans_a), m, n, k, 1.0, _ptr(a), max(a.shape[0], 1), _ptr(b),
                                            max(k, 1), 0.0, _ptr(d), _ptr(v), _ptr(out), m))
         return out[:n].copy()
 

@@ -62,8 +62,8 @@ int main(int argc, char** argv) {
 
   // an interval without spectrum: the filter annihilates the block -> empty (pipeline.hpp:142-156)
   g::RunConfig far = cfg;
-  far.interval_a = 50.0;
-  far.interval_b = 60.0;
+  far.interval_a = 5.0;
+  far.interval_b = 6.0;
   const g::RunResult empty = g::run_solve(dev, pm, far);
 
   // a shift exactly on the spectrum: ShiftedFactorization throws sssvd::NumericalError

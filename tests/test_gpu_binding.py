@@ -56,4 +56,7 @@ def test_cpp_binding_accumulate_and_run_solve(tmp_path):
     assert len(ns) == 40
     assert max(np.min(np.abs(sigma - s)) / s for s in sig[ns]) <= 1e-10
     assert max(exact[ns]) <= 1e-9 and max(gal[ns]) <= 1e-9
-    assert far_empty == 1 and caught == 1
+    # [5, 6] lies far above sigma_max = 1.195: the oracle's filter annihilates the block there too
+    far = orc.run_solve(am, orc.RunConfig(5.0, 6.0, params=orc.SsParams(block_size=L, moment_degree=M, quadrature_count=N)))
+    assert far.empty and far_empty == 1
+    assert caught == 1

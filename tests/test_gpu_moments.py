@@ -163,6 +163,37 @@ def test_nccl_single_rank_comm_path(dev):
         assert np.array_equal(ref[k], got[k])
 
 
+def test_nccl_single_rank_operator_broadcast_and_failure_agreement(dev):
+    """With a (1-rank) communicator: set_operator_root uploads on the root and broadcasts the padded
+    operator with ncclBroadcast (the multi-GPU upload), and run_solve through it is bitwise the plain
+    upload's; a shift on the spectrum goes through the failure agreement (one int all-reduce before
+    the moment all-reduce) and surfaces as NumericalError (shifted_solver.hpp:29-30)."""
+    from paper_2109_13655_b200 import sssvd
+    am, _, _, _ = orc.build_model(1, 400, 120, 7)
+    a = np.asfortranarray(am.dense)
+    cfg = sssvd.RunConfig(0.8, 1.2, params=sssvd.SsParams(block_size=8, moment_degree=4, quadrature_count=16))
+    d1 = sssvd.Device(0)
+    d1.set_operator(a)
+    ref = d1.run_solve(cfg)
+    d1.close()
+    d2 = sssvd.Device(0)
+    d2.init_comm(sssvd.Device.nccl_unique_id(), 1, 0)
+    assert d2.comm_size() == 1
+    d2.set_operator_root(a.ctypes.data, a.shape[0], a.shape[1], a.shape[0], on_device=False, root=0)
+    got = d2.run_solve(cfg)
+    assert np.array_equal(ref.triplets.sigma, got.triplets.sigma)
+    assert np.array_equal(ref.triplets.left, got.triplets.left) and np.array_equal(ref.exact, got.exact)
+    # G = diag(1, 4, ...) and a shift exactly at 4: the pivot floor trips on the (only) rank
+    diag = np.diag(np.arange(1.0, 9.0))
+    d2.set_operator(diag)
+    d2.form_gram(copy_out=False)
+    with pytest.raises(sssvd.NumericalError):
+        d2.check(sssvd.lib().sssvd_gpu_moments(
+            d2.h, 1, sssvd._ptr(np.array([4.0, 0.0])), sssvd._ptr(np.array([1.0, 0.0])),
+            sssvd._ptr(np.array([4.0, 0.0])), sssvd._ptr(np.ones(8)), 1, 1, 0, sssvd._ptr(np.empty(8))))
+    d2.close()
+
+
 def test_ell3_factor_cache_matches_oracle(dev):
     """ell > 1 with resident factors (moments.hpp:106-128): the refinement passes replay only the
     forward/back substitution of the new block; results must equal the oracle's to rounding."""

@@ -167,9 +167,9 @@ def test_gram_sharding_is_exact(dev):
 @pytest.mark.parametrize("m,n,k,batch", [(200, 136, 128, 3), (64, 64, 16, 1), (77, 35, 9, 2), (1000, 1016, 64, 2),
                                          (3968, 4000, 128, 2), (513, 129, 256, 1)])
 def test_zgemm_tma_bitwise_cpasync(dev, variant, m, n, k, batch):
-    """The TMA + mbarrier trailing-update GEMM (variant 0, the product path) issues the same DMMA
-    chain per entry of C as the cp.async kernel (variant 1): bitwise-equal C, ragged edges and
-    K not a multiple of 16 included (TMA zero-fills out-of-bounds boxes)."""
+    """The TMA + mbarrier trailing-update GEMM (variant 1) issues the same DMMA chain per entry of C
+    as the cp.async kernel (variant 0, the product default): bitwise-equal C, ragged edges and K
+    not a multiple of 16 included (TMA zero-fills out-of-bounds boxes)."""
     import ctypes
     from paper_2109_13655_b200 import sssvd
     ms, mism = ctypes.c_double(), ctypes.c_int64()
