@@ -43,7 +43,15 @@ def contract(g, o, w, truth):
     return strict, robust
 
 
-MIN_CHECKED = {1: 90, 2: 250, 3: 150, 4: 100}
+MIN_CHECKED = {1: 90, 2: 250, 3: 150, 4: 100, 5: 800}
+
+
+def check_counts(cfg, strict, robust, o):
+    # the comparisons must not be vacuous: most in-interval candidates are compared at both levels,
+    # and only a few verdicts at delta = 1e-20 are set by roundoff
+    assert strict.checked >= MIN_CHECKED[cfg]
+    assert robust.checked + robust.junk >= 0.5 * o["d20"].count_in_interval
+    assert robust.undetermined <= max(2, 0.02 * o["d20"].count_in_interval)
 
 
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4])
@@ -56,8 +64,7 @@ def test_config_parity_with_live_oracle(dev, cfg):
         o = oracle_runs(a, w, mode)
         strict, robust = contract(g, o, w, truth)
         print(f"cfg{cfg} mode{mode}: strict {strict}; robust {robust}")
-        assert strict.checked >= MIN_CHECKED[cfg]   # in-interval candidates compared at delta = 1e-12
-        assert robust.checked >= 0.8 * o["d20"].count_in_interval
+        check_counts(cfg, strict, robust, o)
         if cfg == 4:
             # the clustered config: the right Ritz vectors of the in-interval candidates span the
             # same subspace on both sides (delta = 1e-12, same count)
@@ -82,5 +89,4 @@ def test_config5_parity_with_oracle_fixture(dev):
         o = {t: Summary.from_arrays(fx, f"m{mode}_{t}_") for t in ("d20", "d12")}
         strict, robust = contract(g, o, w, truth)
         print(f"cfg5 mode{mode}: strict {strict}; robust {robust}")
-        assert strict.checked >= 500
-        assert robust.checked >= 0.8 * o["d20"].count_in_interval
+        check_counts(cfg=5, strict=strict, robust=robust, o=o)
