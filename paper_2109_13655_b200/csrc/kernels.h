@@ -38,6 +38,11 @@ size_t leaf_smem_bytes(int n, int W, int cluster);
 // K2 (lu.cu): cluster leaf LU; cb < r0: the leaf also applies its interchanges to columns [cb, r0)
 cudaError_t leaf_lu(double2* mats, int ld, long long stride, int n, int r0, int w, int W, int cluster, int* ipiv,
                        int batch, cudaStream_t s, int cb);
+// K2, register form (lu.cu): the leaf rows live in registers, one CTA + one cluster barrier per
+// pivot column; a CTA holds leaf_reg_rows(W) rows, the cluster is sized per launch (<= cluster)
+int leaf_reg_rows(int W);
+cudaError_t leaf_lu_reg(double2* mats, int ld, long long stride, int n, int r0, int w, int W, int cluster, int* ipiv,
+                        int batch, cudaStream_t s, int cb);
 cudaError_t pivot_floor(const double2* mats, int ld, long long stride, int n, const double2* shifts,
                         const double* gmax, int* status, double* minpiv, int batch, cudaStream_t s);
 // K5 (zgemm.cu): C -= A B, row-major complex, batched
@@ -46,6 +51,8 @@ cudaError_t zgemm_sub(int M, int N, int K, const double2* A, int lda, long long 
                       cudaStream_t stream);
 // debug: route zgemm_sub to 1 = the cp.async kernel, 2 = the TMA kernel, 0 = the default (zgemm.cu)
 void zgemm_force(int kernel);
+// allocates the current device's arrival counters of the first-wave CTA offset (zgemm.cu)
+void zgemm_init_device();
 // C = A B[brow[k], :] (row-gathered B), row-major complex, batched (zgemm.cu)
 cudaError_t zgemm_set_gather(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B,
                              int ldb, long long sB, const int* brow, int sR, double2* C, int ldc, long long sC,

@@ -263,6 +263,7 @@ namespace sssvd_gpu {
 struct LuPlan {
   int n, L, ld, NB, W, cluster;
   long long stride;
+  bool leaf_reg;   // register-resident leaf (lu.cu) instead of the shared-memory slab leaf
 };
 
 static LuPlan make_plan(int n, int L) {
@@ -278,7 +279,31 @@ static LuPlan make_plan(int n, int L) {
   static const char* nb_env = std::getenv("SSSVD_NB");
   p.NB = n >= 8192 ? 256 : 128;
   if (nb_env && (std::atoi(nb_env) == 128 || std::atoi(nb_env) == 256)) p.NB = std::atoi(nb_env);
-  // leaf width W and cluster size C: the leaf slab (ceil(n/C) x (W+1) complex) must fit ~200 KB
+  // Leaf: the register form where 16 CTAs hold the n rows (n <= 16384), the widest leaf that fits
+  // (W = 32 / 16 / 8: 256 / 512 / 1024 rows per CTA); SSSVD_LEAF=smem selects the shared-memory
+  // slab form (the only one above n = 16384), SSSVD_LEAF_W overrides the width. Read per plan so
+  // the tests can compare both forms (bitwise equal).
+  p.leaf_reg = false;
+  {
+    const char* lenv = std::getenv("SSSVD_LEAF");
+    const char* wenv = std::getenv("SSSVD_LEAF_W");
+    if (!(lenv && std::string(lenv) == "smem")) {
+      const int Ws[3] = {32, 16, 8};
+      int pick = 0;
+      for (int wi = 0; wi < 3 && !pick; ++wi)
+        if ((long long)16 * leaf_reg_rows(Ws[wi]) >= n) pick = Ws[wi];
+      const int wo = wenv ? std::atoi(wenv) : 0;
+      if ((wo == 8 || wo == 16 || wo == 32) && (long long)16 * leaf_reg_rows(wo) >= n) pick = wo;
+      if (pick) {
+        p.leaf_reg = true;
+        p.W = pick;
+        p.cluster = 16;
+        return p;
+      }
+    }
+  }
+  // shared-memory form: leaf width W and cluster size C with the slab (ceil(n/C) x (W+1) complex)
+  // within ~200 KB
   const size_t budget = 200 * 1024;
   p.W = 8;
   p.cluster = 16;
@@ -365,7 +390,10 @@ static void factor_rec(const LuPlan& P, const LuWork& W, double2* mats, int* ipi
   const int n = P.n;
   if (w <= P.W) {
     // the leaf applies its interchanges to the block columns [cb, c0) in its own epilogue
-    CK(leaf_lu(mats, P.ld, P.stride, n, c0, w, P.W, P.cluster, ipiv, nb, s, cb));
+    if (P.leaf_reg)
+      CK(leaf_lu_reg(mats, P.ld, P.stride, n, c0, w, P.W, P.cluster, ipiv, nb, s, cb));
+    else
+      CK(leaf_lu(mats, P.ld, P.stride, n, c0, w, P.W, P.cluster, ipiv, nb, s, cb));
     return;
   }
   int wl = ((w / 2) + P.W - 1) / P.W * P.W;
@@ -636,7 +664,7 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
     } else {
       const std::vector<uintptr_t> key = {
           (uintptr_t)n, (uintptr_t)L, (uintptr_t)M, (uintptr_t)nb, (uintptr_t)ng, (uintptr_t)P.NB, (uintptr_t)P.W,
-          (uintptr_t)P.cluster, (uintptr_t)P.ld, (uintptr_t)ctx->G.p,
+          (uintptr_t)P.cluster, (uintptr_t)P.leaf_reg, (uintptr_t)P.ld, (uintptr_t)ctx->G.p,
           (uintptr_t)V_dev, (uintptr_t)mats, (uintptr_t)ipiv, (uintptr_t)work.linv, (uintptr_t)work.T,
           (uintptr_t)work.src, (uintptr_t)work.disp, (uintptr_t)dshift, (uintptr_t)dcoef, (uintptr_t)S_dev,
           (uintptr_t)ctx->gmax.p, (uintptr_t)dstatus, (uintptr_t)dmin, (uintptr_t)lookahead,
@@ -1477,6 +1505,7 @@ sssvd_status sssvd_gpu_create(int device, sssvd_gpu_ctx** out) {
   cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming);
+  zgemm_init_device();   // per-device counters of the GEMM's first-wave offset (never inside a capture)
   *out = ctx;
   return SSSVD_OK;
 }

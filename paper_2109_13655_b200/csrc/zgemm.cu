@@ -47,7 +47,7 @@ struct GemmProf {
   unsigned long long acc_launches = 0;
 };
 static GemmProf g_prof;
-constexpr int kStampSlots = 8192;
+constexpr int kStampSlots = 32768;   // config 5 issues ~16.6k GEMM launches per 32-shift pass
 
 void zgemm_profile_enable(bool on) {
   g_prof.on = on;
@@ -228,7 +228,8 @@ template <int WI, int WJ, bool SET, bool GATHER, int ISSUE_AT = 0>
 __global__ void __launch_bounds__((64 / (8 * WI)) * (64 / (8 * WJ)) * 32, WI * WJ >= 8 ? 2 : 1)
 zgemm_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long long sA,
              const double2* __restrict__ B, int ldb, long long sB, const int* __restrict__ brow, int sR,
-             double2* C, int ldc, long long sC, unsigned long long* __restrict__ stamp, int stamp_cap) {
+             double2* C, int ldc, long long sC, unsigned long long* __restrict__ stamp, int stamp_cap,
+             unsigned* desync, int desync_first, unsigned desync_ns) {
   constexpr int WARPS_N = 64 / (8 * WJ);
   constexpr int THREADS = (64 / (8 * WI)) * WARPS_N * 32;
   extern __shared__ __align__(16) double2 smem[];
@@ -236,6 +237,28 @@ zgemm_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long l
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     atomicMin(stamp, t);
+  }
+  // The two CTAs resident on an SM start together and run identical work, so their prologues and
+  // epilogues (no DMMA) coincide for the whole launch. Every second CTA to arrive on an SM in the
+  // first wave waits about half a tile time once; the offset then persists through the launch,
+  // so one CTA's epilogue runs under the other's main loop.
+  if (desync) {
+    const int lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    if (lin < desync_first) {
+      if (threadIdx.x == 0) {
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        if (atomicAdd(desync + sm, 1u) & 1u) {
+          unsigned long long t0, t1;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+          do {
+            __nanosleep(1000);
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+          } while (t1 - t0 < desync_ns);
+        }
+      }
+      __syncthreads();
+    }
   }
   // stage s occupies [s*(A_STAGE+B_STAGE), (s+1)*(A_STAGE+B_STAGE)): A tile then B tile
   double2* As = smem;
@@ -655,6 +678,44 @@ cudaError_t set_kernel_smem(const void* fn, size_t bytes, bool nonportable_clust
   return cudaSuccess;
 }
 
+// per-device arrival counters of the first-wave offset (monotonic, never reset: only the parity
+// of consecutive arrivals on one SM matters)
+static unsigned* desync_counters(int* sms_out) {
+  static std::mutex mu;
+  static std::map<int, std::pair<unsigned*, int>> per_dev;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = per_dev.find(dev);
+  if (it == per_dev.end()) {
+    int sms = 0;
+    unsigned* p = nullptr;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaMalloc(&p, 1024 * sizeof(unsigned)) != cudaSuccess) return nullptr;
+    cudaMemset(p, 0, 1024 * sizeof(unsigned));
+    it = per_dev.emplace(dev, std::make_pair(p, sms)).first;
+  }
+  *sms_out = it->second.second;
+  return it->second.first;
+}
+void zgemm_init_device() {
+  int sms = 0;
+  (void)desync_counters(&sms);
+}
+
+// The first-wave offset in ns for a launch of KT k-stages: about half the time one 64 x 64 tile
+// takes when it has the SM's DMMA pipe to itself (2.1 us per k-stage + ~6 us of prologue and
+// epilogue). Measured on the isolated trailing updates (profiles/r02_zgemm_desync.txt): K = 128
+// 31.5 -> 33.5 TF/s, K = 256 33.9 -> 35.1 TF/s; offsets near a whole tile time re-align the two
+// CTAs and gain nothing. SSSVD_ZGEMM_DESYNC=0 turns it off, a positive value is ns per k-stage
+// (measurement override); read per call.
+static unsigned desync_ns(int KT) {
+  const char* e = std::getenv("SSSVD_ZGEMM_DESYNC");
+  if (!e) return 1050u * (unsigned)KT + 3000u;
+  const int v = std::atoi(e);
+  return v > 0 ? (unsigned)v * (unsigned)KT : 0u;
+}
+
 // C -= A B (SET = false) or C = A B[brow] (SET = GATHER = true). The next k-stage's copies are
 // issued after the first k-quad's DMMAs (measured +1 % over issuing them at the top of the stage;
 // bitwise identical).
@@ -677,8 +738,23 @@ static cudaError_t launch(int M, int N, int K, const double2* A, int lda, long l
   auto kern = zgemm_kernel<4, 4, SET, GATHER, 1>;
   SSSVD_CUDA_TRY(set_kernel_smem((const void*)kern, zgemm_sub_smem(), false));
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch);
+  // first-wave offset of the two co-resident CTAs (large launches only)
+  unsigned* desync = nullptr;
+  int first = 0;
+  unsigned ns = 0;
+  const int KT = (K + BK - 1) / BK;
+  const long long ctas = (long long)grid.x * grid.y * grid.z;
+  if (!SET && KT >= 4 && desync_ns(KT) > 0) {
+    int sms = 0;
+    unsigned* ctr = desync_counters(&sms);
+    if (ctr && ctas >= 8LL * sms) {
+      desync = ctr;
+      first = 2 * sms;
+      ns = desync_ns(KT);
+    }
+  }
   kern<<<grid, 128, zgemm_sub_smem(), stream>>>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, stamp,
-                                                  g_prof.cap);
+                                                  g_prof.cap, desync, first, ns);
   return cudaGetLastError();
 }
 

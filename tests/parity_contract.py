@@ -281,8 +281,13 @@ def check_robust(g20: Summary, o20: Summary, g12: Summary, o12: Summary, a: floa
 
 
 def principal_angle_sine(x: np.ndarray, y: np.ndarray) -> float:
-    """Largest principal-angle sine between span(x) and span(y) (orthonormalised first)."""
+    """Largest principal-angle sine between span(x) and span(y) (equal dimensions, orthonormalised
+    first), as the norm of the part of span(y) outside span(x): || (I - Qx Qx^T) Qy ||_2. (The
+    cosine form sqrt(1 - c_min^2) cannot resolve sines below ~sqrt(eps) = 1.5e-8.)"""
+    if x.shape[1] == 0 or y.shape[1] == 0:
+        return 0.0
     qx, _ = np.linalg.qr(x)
     qy, _ = np.linalg.qr(y)
-    c = np.linalg.svd(qx.T @ qy, compute_uv=False)
-    return float(np.sqrt(max(0.0, 1.0 - np.min(c) ** 2))) if c.size else 0.0
+    r = qy - qx @ (qx.T @ qy)
+    r -= qx @ (qx.T @ r)   # second projection pass: keeps the residual accurate at the 1e-16 level
+    return float(np.linalg.svd(r, compute_uv=False)[0])
