@@ -38,11 +38,6 @@ size_t leaf_smem_bytes(int n, int W, int cluster);
 // K2 (lu.cu): cluster leaf LU; cb < r0: the leaf also applies its interchanges to columns [cb, r0)
 cudaError_t leaf_lu(double2* mats, int ld, long long stride, int n, int r0, int w, int W, int cluster, int* ipiv,
                        int batch, cudaStream_t s, int cb);
-// K2, register form (lu.cu): the leaf rows live in registers, one CTA + one cluster barrier per
-// pivot column; a CTA holds leaf_reg_rows(W) rows, the cluster is sized per launch (<= cluster)
-int leaf_reg_rows(int W);
-cudaError_t leaf_lu_reg(double2* mats, int ld, long long stride, int n, int r0, int w, int W, int cluster, int* ipiv,
-                        int batch, cudaStream_t s, int cb);
 cudaError_t pivot_floor(const double2* mats, int ld, long long stride, int n, const double2* shifts,
                         const double* gmax, int* status, double* minpiv, int batch, cudaStream_t s);
 // K5 (zgemm.cu): C -= A B, row-major complex, batched

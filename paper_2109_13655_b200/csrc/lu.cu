@@ -15,7 +15,6 @@
 #include <algorithm>
 #include <cstdlib>
 #include <string>
-#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -615,312 +614,6 @@ leaf_lu_kernel(double2* mats, int ld, long long stride, int n, int r0, int w, in
       for (int e = 0; e < k; ++e)
         if (pos[e] != cont[e]) Mb[(size_t)pos[e] * ld + cb + c] = buf[(size_t)e * ncl + c];
     }
-  }
-}
-
-// ----------------------------------------------------------------------------- K2 leaf panel, register form
-// The same unblocked LU (bitwise: the same scale / rank-1 update per entry and the same pivot
-// choice, largest |.|^2 with ties to the smallest row), with the leaf kept in REGISTERS: thread t
-// of cluster CTA c owns rows my0 + t + k NT (k < RPT) of the leaf, all W columns of each. Per
-// pivot column there is ONE CTA barrier and ONE cluster barrier (the shared-memory form above
-// needs two CTA barriers and a cluster barrier, with warp 0 doing the exchange alone):
-//   1. warp argmax by redux.sync on the IEEE bit pattern (non-negative doubles order like their
-//      bits), warp leaders -> shared memory, __syncthreads, every warp reduces the leaders;
-//   2. the warp that owns the CTA's candidate row pushes the row's W values into EVERY cluster
-//      CTA's shared memory (st.shared::cluster), warp 0 pushes (score, row); the CTA that owns
-//      the diagonal row pushes that row likewise;
-//   3. cluster barrier (release / acquire);
-//   4. every warp picks the winner among the C candidates from its own shared memory, the
-//      owners of the diagonal and pivot rows exchange them in registers, and every thread
-//      scales / updates its rows and scores the next column.
-// The push buffers are double-buffered by column parity (a CTA can be at most one cluster barrier
-// ahead of the slowest one). The left-interchange epilogue is shared by all CTAs of the cluster
-// (each takes a slice of the columns [cb, r0)).
-__device__ __forceinline__ void st_dsmem_f64x2(unsigned addr, double2 v) {
-  asm volatile("st.shared::cluster.v2.f64 [%0], {%1,%2};" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
-}
-__device__ __forceinline__ void st_dsmem_f64(unsigned addr, double v) {
-  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
-}
-__device__ __forceinline__ void st_dsmem_s32(unsigned addr, int v) {
-  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
-// argmax over the warp of (score, row): score >= 0 or -1 (no candidate); ties -> smallest row
-__device__ __forceinline__ void warp_argmax(double& best, int& brow) {
-  const unsigned full = 0xffffffffu;
-  const unsigned hi = best >= 0.0 ? (unsigned)__double2hiint(best) + 1u : 0u;
-  const unsigned lo = (unsigned)__double2loint(best);
-  const unsigned mh = __reduce_max_sync(full, hi);
-  bool in = hi == mh;
-  const unsigned ml = __reduce_max_sync(full, in ? lo : 0u);
-  in = in && lo == ml;
-  const int mr = __reduce_min_sync(full, in ? brow : 0x7fffffff);
-  best = mh == 0u ? -1.0 : __hiloint2double((int)(mh - 1u), (int)ml);
-  brow = mh == 0u ? 0x7fffffff : mr;
-}
-
-template <int N, int I = 0, class F>
-__device__ __forceinline__ void static_for(F& f) {
-  if constexpr (I < N) {
-    f(std::integral_constant<int, I>{});
-    static_for<N, I + 1>(f);
-  }
-}
-
-constexpr int LEAF_CMAX = 16;
-constexpr int LEAF_EPI_BYTES = 24 * 1024;   // gather buffer of the left-interchange epilogue
-
-template <int W, int NT, int RPT>
-__global__ void __launch_bounds__(NT, 1)
-leaf_lu_reg_kernel(double2* mats, int ld, long long stride, int n, int r0, int w, int R, int* ipiv, int cb) {
-  constexpr int NW = NT / 32;
-  extern __shared__ __align__(16) unsigned char epi_raw[];
-  __shared__ __align__(16) double2 cand_vals[2][LEAF_CMAX][W];
-  __shared__ __align__(16) double2 diag_vals[2][W];
-  __shared__ double cand_score[2][LEAF_CMAX];
-  __shared__ int cand_row[2][LEAF_CMAX];
-  __shared__ double wred_s[2][NW];
-  __shared__ int wred_r[2][NW];
-  __shared__ int piv_s[W];
-
-  const int C = gridDim.x;
-  const int rank = (int)cluster_ctarank();
-  const int b = blockIdx.y;
-  double2* Mb = mats + b * stride;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int my0 = r0 + rank * R;
-  const int myn = max(0, min(R, n - my0));
-
-  double2 a[RPT][W];
-#pragma unroll
-  for (int k = 0; k < RPT; ++k) {
-    const int i = tid + k * NT;
-    const double2* row = Mb + (size_t)(my0 + i) * ld + r0;
-#pragma unroll
-    for (int c = 0; c < W; ++c) a[k][c] = (i < myn && c < w) ? row[c] : make_double2(0.0, 0.0);
-  }
-  double best = -1.0;
-  int brow = 0x7fffffff;
-#pragma unroll
-  for (int k = 0; k < RPT; ++k) {
-    const int i = tid + k * NT;
-    if (i < myn) {
-      const double s = cabs2(a[k][0]);
-      if (s > best) { best = s; brow = my0 + i; }
-    }
-  }
-
-  // the column loop is unrolled at compile time (every register-array index must be static)
-  auto column = [&](auto jc) {
-    constexpr int j = decltype(jc)::value;
-    if (j < w) {
-      const int d = r0 + j;
-      const int par = j & 1;
-      // ---- 1. CTA argmax of column j
-      warp_argmax(best, brow);
-      if (lane == 0) { wred_s[par][warp] = best; wred_r[par][warp] = brow; }
-      __syncthreads();
-      double cs = lane < NW ? wred_s[par][lane] : -1.0;
-      int cr = lane < NW ? wred_r[par][lane] : 0x7fffffff;
-      warp_argmax(cs, cr);
-      // ---- 2. push the candidate row, its (score, row) and the diagonal row to every CTA
-      if (cr != 0x7fffffff) {
-        const int oi = cr - my0;
-        const int ot = oi % NT, ok = oi / NT;
-        if (warp == (ot >> 5)) {
-          if (tid == ot) {
-#pragma unroll
-            for (int k = 0; k < RPT; ++k)
-              if (k == ok) {
-#pragma unroll
-                for (int c = 0; c < W; ++c) cand_vals[par][rank][c] = a[k][c];
-              }
-          }
-          __syncwarp();
-          for (int e = lane; e < C * W; e += 32) {
-            const int dst = e / W, c = e - dst * W;
-            if (dst != rank) st_dsmem_f64x2(dsmem_addr(&cand_vals[par][rank][c], dst), cand_vals[par][rank][c]);
-          }
-        }
-      }
-      if (warp == 0 && lane < C) {
-        st_dsmem_f64(dsmem_addr(&cand_score[par][rank], lane), cs);
-        st_dsmem_s32(dsmem_addr(&cand_row[par][rank], lane), cr);
-      }
-      {
-        const int rank_d = j / R;
-        if (rank == rank_d) {
-          const int di = j - rank_d * R;
-          const int dt = di % NT, dk = di / NT;
-          if (warp == (dt >> 5)) {
-            if (tid == dt) {
-#pragma unroll
-              for (int k = 0; k < RPT; ++k)
-                if (k == dk) {
-#pragma unroll
-                  for (int c = 0; c < W; ++c) diag_vals[par][c] = a[k][c];
-                }
-            }
-            __syncwarp();
-            for (int e = lane; e < C * W; e += 32) {
-              const int dst = e / W, c = e - dst * W;
-              if (dst != rank) st_dsmem_f64x2(dsmem_addr(&diag_vals[par][c], dst), diag_vals[par][c]);
-            }
-          }
-        }
-      }
-      // ---- 3. one cluster barrier per column
-      cluster_sync_all();
-      // ---- 4. winner, interchange in registers, scale + rank-1 update, score of column j+1
-      double s = lane < C ? cand_score[par][lane] : -1.0;
-      int r = lane < C ? cand_row[par][lane] : 0x7fffffff;
-      warp_argmax(s, r);
-      // the candidate rows are distinct, so the winner's CTA is the one whose candidate is row r
-      const unsigned whom = __ballot_sync(0xffffffffu, lane < C && cand_row[par][lane < C ? lane : 0] == r);
-      const int rk = __ffs(whom) - 1;
-      if (tid == 0) {
-        piv_s[j] = r;
-        if (rank == 0) ipiv[(size_t)b * n + d] = r;
-      }
-      const double2* uv = cand_vals[par][rk];
-      const double2* dv = diag_vals[par];
-#pragma unroll
-      for (int k = 0; k < RPT; ++k) {
-        const int g = my0 + tid + k * NT;
-        if (tid + k * NT < myn) {
-          if (g == d) {
-#pragma unroll
-            for (int c = 0; c < W; ++c) a[k][c] = uv[c];
-          } else if (g == r) {
-#pragma unroll
-            for (int c = 0; c < W; ++c) a[k][c] = dv[c];
-          }
-        }
-      }
-      const double2 u = uv[j];
-      const bool nz = cabs2(u) != 0.0;
-      const double2 inv = nz ? crecip(u) : make_double2(0.0, 0.0);
-      best = -1.0;
-      brow = 0x7fffffff;
-#pragma unroll
-      for (int k = 0; k < RPT; ++k) {
-        const int i = tid + k * NT;
-        if (i < myn && my0 + i > d) {
-          if (nz) {
-            const double2 l = cmul(a[k][j], inv);
-            a[k][j] = l;
-#pragma unroll
-            for (int c = j + 1; c < W; ++c) a[k][c] = cfms(a[k][c], l, uv[c]);
-          }
-          if (j + 1 < W && j + 1 < w) {
-            const double sc = cabs2(a[k][j + 1 < W ? j + 1 : j]);
-            if (sc > best) { best = sc; brow = my0 + i; }
-          }
-        }
-      }
-    }
-  };
-  static_for<W>(column);
-#pragma unroll
-  for (int k = 0; k < RPT; ++k) {
-    const int i = tid + k * NT;
-    if (i < myn) {
-      double2* row = Mb + (size_t)(my0 + i) * ld + r0;
-#pragma unroll
-      for (int c = 0; c < W; ++c)
-        if (c < w) row[c] = a[k][c];
-    }
-  }
-  // ---- epilogue: the leaf's interchanges applied to the block columns [cb, r0) on its left; every
-  // CTA of the cluster takes a slice of those columns (nobody else touches them meanwhile). The
-  // sequential swaps are folded into <= 2w (destination <- source) moves; a thread gathers every
-  // source of its column before scattering, so no load waits on a store.
-  if (cb < r0) {
-    __shared__ int pos[2 * W], cont[2 * W];
-    __shared__ int kmv;
-    __syncthreads();   // piv_s complete
-    if (warp == 0) {
-      int k = 0;
-      for (int j = 0; j < w; ++j) {
-        const int aa = r0 + j, q = piv_s[j];
-        int ia = -1, iq = -1;
-        for (int base = 0; base < k; base += 32) {
-          const int t = base + lane;
-          const int pv = t < k ? pos[t] : -1;
-          const unsigned ba = __ballot_sync(0xffffffffu, pv == aa);
-          const unsigned bq = __ballot_sync(0xffffffffu, pv == q);
-          if (ba && ia < 0) ia = base + __ffs(ba) - 1;
-          if (bq && iq < 0) iq = base + __ffs(bq) - 1;
-        }
-        if (ia < 0) {
-          if (lane == 0) { pos[k] = aa; cont[k] = aa; }
-          ia = k++;
-        }
-        if (q == aa) iq = ia;
-        if (iq < 0) {
-          if (lane == 0) { pos[k] = q; cont[k] = q; }
-          iq = k++;
-        }
-        __syncwarp();
-        if (lane == 0 && ia != iq) { const int t = cont[ia]; cont[ia] = cont[iq]; cont[iq] = t; }
-        __syncwarp();
-      }
-      if (lane == 0) kmv = k;
-    }
-    __syncthreads();
-    const int k = kmv, ncl = r0 - cb;
-    const int per = (ncl + C - 1) / C;
-    const int c_lo = cb + rank * per, c_hi = min(r0, c_lo + per);
-    double2* buf = reinterpret_cast<double2*>(epi_raw);
-    const int tact = min(NT, LEAF_EPI_BYTES / (int)sizeof(double2) / max(k, 1));   // threads per pass
-    if (tid < tact) {
-      for (int c = c_lo + tid; c < c_hi; c += tact) {
-        for (int e = 0; e < k; ++e) buf[(size_t)e * tact + tid] = Mb[(size_t)cont[e] * ld + c];
-        for (int e = 0; e < k; ++e)
-          if (pos[e] != cont[e]) Mb[(size_t)pos[e] * ld + c] = buf[(size_t)e * tact + tid];
-      }
-    }
-  }
-}
-
-template <int W, int NT, int RPT>
-static cudaError_t launch_leaf_reg(double2* mats, int ld, long long stride, int n, int r0, int w, int cluster,
-                                   int* ipiv, int batch, cudaStream_t s, int cb) {
-  const int m = n - r0;
-  // the smallest power-of-two cluster (up to the plan's) whose CTAs hold the m rows
-  int c = 1;
-  while (c < cluster && (long long)c * NT * RPT < m) c *= 2;
-  if ((long long)c * NT * RPT < m) return cudaErrorInvalidValue;
-  const int R = (m + c - 1) / c;
-  const size_t smem = cb < r0 ? LEAF_EPI_BYTES : 0;
-  SSSVD_CUDA_TRY(set_kernel_smem((const void*)leaf_lu_reg_kernel<W, NT, RPT>, LEAF_EPI_BYTES, true));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(c, batch, 1);
-  cfg.blockDim = dim3(NT, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = c;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  note_launch();
-  return cudaLaunchKernelEx(&cfg, leaf_lu_reg_kernel<W, NT, RPT>, mats, ld, stride, n, r0, w, R, ipiv, cb);
-}
-
-// rows one CTA of the register leaf holds, per leaf width
-int leaf_reg_rows(int W) { return W == 32 ? 256 : W == 16 ? 512 : W == 8 ? 1024 : 0; }
-
-cudaError_t leaf_lu_reg(double2* mats, int ld, long long stride, int n, int r0, int w, int W, int cluster, int* ipiv,
-                        int batch, cudaStream_t s, int cb) {
-  if (cb > r0 || cluster > LEAF_CMAX) return cudaErrorInvalidValue;
-  switch (W) {
-    case 8: return launch_leaf_reg<8, 512, 2>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s, cb);
-    case 16: return launch_leaf_reg<16, 512, 1>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s, cb);
-    case 32: return launch_leaf_reg<32, 256, 1>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s, cb);
-    default: return cudaErrorInvalidValue;
   }
 }
 

@@ -154,7 +154,7 @@ struct sssvd_gpu_ctx {
   bool has_gram = false;
   DBuf A, G, gmax, mats, ipiv, shifts, coef, S, V, status, minpiv, scratch;
   DBuf t0, t1, t2, t7, gwork;
-  DBuf lw_linv, lw_T, lw_src, lw_disp, lw2_linv, lw2_T, lw2_src, lw2_disp, jscr, jperm, jq, jr, jj, qy, qt, qw;
+  DBuf lw_linv, lw_T, lw_src, lw_disp, lw2_linv, lw2_T, lw2_src, lw2_disp, jscr, jperm, jq, jr, jj, qy, qt, qw, ts_tmp, ts_rs, ts_r;
   // factor cache (moments.hpp:106-116): the last pass left shifts [fact_jb, fact_je) factored in
   // one resident batch of `mats`, so a later pass with the same operator/shifts/L only replays the
   // forward elimination of its new right-hand side and the back substitution
@@ -263,7 +263,6 @@ namespace sssvd_gpu {
 struct LuPlan {
   int n, L, ld, NB, W, cluster;
   long long stride;
-  bool leaf_reg;   // register-resident leaf (lu.cu) instead of the shared-memory slab leaf
 };
 
 static LuPlan make_plan(int n, int L) {
@@ -279,31 +278,7 @@ static LuPlan make_plan(int n, int L) {
   static const char* nb_env = std::getenv("SSSVD_NB");
   p.NB = n >= 8192 ? 256 : 128;
   if (nb_env && (std::atoi(nb_env) == 128 || std::atoi(nb_env) == 256)) p.NB = std::atoi(nb_env);
-  // Leaf: the register form where 16 CTAs hold the n rows (n <= 16384), the widest leaf that fits
-  // (W = 32 / 16 / 8: 256 / 512 / 1024 rows per CTA); SSSVD_LEAF=smem selects the shared-memory
-  // slab form (the only one above n = 16384), SSSVD_LEAF_W overrides the width. Read per plan so
-  // the tests can compare both forms (bitwise equal).
-  p.leaf_reg = false;
-  {
-    const char* lenv = std::getenv("SSSVD_LEAF");
-    const char* wenv = std::getenv("SSSVD_LEAF_W");
-    if (!(lenv && std::string(lenv) == "smem")) {
-      const int Ws[3] = {32, 16, 8};
-      int pick = 0;
-      for (int wi = 0; wi < 3 && !pick; ++wi)
-        if ((long long)16 * leaf_reg_rows(Ws[wi]) >= n) pick = Ws[wi];
-      const int wo = wenv ? std::atoi(wenv) : 0;
-      if ((wo == 8 || wo == 16 || wo == 32) && (long long)16 * leaf_reg_rows(wo) >= n) pick = wo;
-      if (pick) {
-        p.leaf_reg = true;
-        p.W = pick;
-        p.cluster = 16;
-        return p;
-      }
-    }
-  }
-  // shared-memory form: leaf width W and cluster size C with the slab (ceil(n/C) x (W+1) complex)
-  // within ~200 KB
+  // leaf width W and cluster size C: the leaf slab (ceil(n/C) x (W+1) complex) must fit ~200 KB
   const size_t budget = 200 * 1024;
   p.W = 8;
   p.cluster = 16;
@@ -327,8 +302,8 @@ static LuPlan make_plan(int n, int L) {
   if (!found) throw Status(SSSVD_E_LENGTH, "operator too large for the on-chip leaf panel");
   {
     // measurement overrides: leaf width / cluster size (used only if the slab fits)
-    static const char* wenv = std::getenv("SSSVD_LEAF_W");
-    static const char* cenv = std::getenv("SSSVD_LEAF_C");
+    const char* wenv = std::getenv("SSSVD_LEAF_W");
+    const char* cenv = std::getenv("SSSVD_LEAF_C");
     const int w = wenv ? std::atoi(wenv) : p.W, c = cenv ? std::atoi(cenv) : p.cluster;
     if ((w == 8 || w == 16 || w == 32) && (c == 1 || c == 2 || c == 4 || c == 8 || c == 16) &&
         leaf_smem_bytes(n, w, c) <= budget) {
@@ -390,10 +365,7 @@ static void factor_rec(const LuPlan& P, const LuWork& W, double2* mats, int* ipi
   const int n = P.n;
   if (w <= P.W) {
     // the leaf applies its interchanges to the block columns [cb, c0) in its own epilogue
-    if (P.leaf_reg)
-      CK(leaf_lu_reg(mats, P.ld, P.stride, n, c0, w, P.W, P.cluster, ipiv, nb, s, cb));
-    else
-      CK(leaf_lu(mats, P.ld, P.stride, n, c0, w, P.W, P.cluster, ipiv, nb, s, cb));
+    CK(leaf_lu(mats, P.ld, P.stride, n, c0, w, P.W, P.cluster, ipiv, nb, s, cb));
     return;
   }
   int wl = ((w / 2) + P.W - 1) / P.W * P.W;
@@ -664,7 +636,7 @@ static void moment_pass(sssvd_gpu_ctx* ctx, const std::vector<std::complex<doubl
     } else {
       const std::vector<uintptr_t> key = {
           (uintptr_t)n, (uintptr_t)L, (uintptr_t)M, (uintptr_t)nb, (uintptr_t)ng, (uintptr_t)P.NB, (uintptr_t)P.W,
-          (uintptr_t)P.cluster, (uintptr_t)P.leaf_reg, (uintptr_t)P.ld, (uintptr_t)ctx->G.p,
+          (uintptr_t)P.cluster, (uintptr_t)P.ld, (uintptr_t)ctx->G.p,
           (uintptr_t)V_dev, (uintptr_t)mats, (uintptr_t)ipiv, (uintptr_t)work.linv, (uintptr_t)work.T,
           (uintptr_t)work.src, (uintptr_t)work.disp, (uintptr_t)dshift, (uintptr_t)dcoef, (uintptr_t)S_dev,
           (uintptr_t)ctx->gmax.p, (uintptr_t)dstatus, (uintptr_t)dmin, (uintptr_t)lookahead,
@@ -899,7 +871,7 @@ static bool qr_plan(int m, int* w_out, bool* reg_out) {
   return true;
 }
 
-static void thin_qr(sssvd_gpu_ctx* ctx, double* A, int m, int k, double* R) {
+static void thin_qr_oneshot(sssvd_gpu_ctx* ctx, double* A, int m, int k, double* R) {
   // hand-written blocked Householder QR (householder_qr.cu), two levels: cluster panels of w
   // columns, whose updates stay inside an outer block of NBO columns; the outer block's reflectors
   // are merged into one compact-WY factor (T from G = Y^T Y, larft) and applied to the trailing
@@ -968,6 +940,52 @@ static void thin_qr(sssvd_gpu_ctx* ctx, double* A, int m, int k, double* R) {
     dgemm(ctx, true, kb, nq, mb, 1.0, Yb, m, A + (size_t)jb * m + jb, m, 0.0, Wt, kb);
     dgemm(ctx, false, kb, nq, kb, 1.0, Tuse, ldt, Wt, kb, 0.0, W2, kb);
     dgemm(ctx, false, mb, nq, kb, -1.0, Yb, m, W2, kb, 1.0, A + (size_t)jb * m + jb, m);
+  }
+}
+
+// Rows per chunk of the tall-skinny QR below: the tallest panel the register kernel holds (w = 8).
+static constexpr int kQrChunkRows = 32768;
+
+// thin QR of any height. Up to kQrChunkRows rows the blocked Householder QR above factors the
+// matrix in one shot (R agrees with LAPACK / Eigen to rounding, signs included). Taller matrices
+// (the reference's HouseholderQR has no row limit: moments.hpp:195-198, extract.hpp:46-52) go
+// through one level of TSQR: each row chunk A_i = Q_i R_i, the stacked R_i (p k x k) = Q_s R, and
+// Q's rows of chunk i = Q_i Q_s[i k : (i+1) k, :]. Q R = A and Q^T Q = I hold to the same 1e-15
+// level; R can differ from the one-shot factor in the signs of its rows (Q's columns flip with
+// them), which no consumer of the tail depends on (|R_ii| for the rank flag, the SVD of R, and the
+// products Q U_R / Q p are invariant).
+static void thin_qr(sssvd_gpu_ctx* ctx, double* A, int m, int k, double* R) {
+  if (m <= kQrChunkRows) {
+    thin_qr_oneshot(ctx, A, m, k, R);
+    return;
+  }
+  cudaStream_t s = ctx->stream;
+  const int p = (m + kQrChunkRows - 1) / kQrChunkRows;
+  const int mc = (m + p - 1) / p;   // rows per chunk (the last one may be shorter)
+  if (m - (p - 1) * mc < k)
+    throw Status(SSSVD_E_LENGTH, "thin_qr: more columns than rows in a row chunk of the tall-skinny QR");
+  double* tmp = ctx->ts_tmp.as<double>((size_t)mc * k);
+  double* Rs = ctx->ts_rs.as<double>((size_t)p * k * k);
+  double* Ri = ctx->ts_r.as<double>((size_t)k * k);
+  const int ldrs = p * k;
+  for (int i = 0; i < p; ++i) {
+    const int o = i * mc, mi = std::min(mc, m - o);
+    CK(cudaMemcpy2DAsync(tmp, sizeof(double) * mi, A + o, sizeof(double) * m, sizeof(double) * mi, k,
+                         cudaMemcpyDeviceToDevice, s));
+    thin_qr_oneshot(ctx, tmp, mi, k, Ri);
+    CK(cudaMemcpy2DAsync(Rs + (size_t)i * k, sizeof(double) * ldrs, Ri, sizeof(double) * k, sizeof(double) * k, k,
+                         cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpy2DAsync(A + o, sizeof(double) * m, tmp, sizeof(double) * mi, sizeof(double) * mi, k,
+                         cudaMemcpyDeviceToDevice, s));
+  }
+  // Rs <- Q_s: one shot (above kQrChunkRows stacked rows the shared-memory panel takes over, up to
+  // ~368k rows, i.e. m ~ 1.4 M rows at k = 8192)
+  thin_qr_oneshot(ctx, Rs, ldrs, k, R);
+  for (int i = 0; i < p; ++i) {
+    const int o = i * mc, mi = std::min(mc, m - o);
+    CK(cudaMemcpy2DAsync(tmp, sizeof(double) * mi, A + o, sizeof(double) * m, sizeof(double) * mi, k,
+                         cudaMemcpyDeviceToDevice, s));
+    dgemm(ctx, false, mi, k, k, 1.0, tmp, mi, Rs + (size_t)i * k, ldrs, 0.0, A + o, m);
   }
 }
 
@@ -1081,14 +1099,6 @@ static void run_solve_impl(sssvd_gpu_ctx* ctx, const sssvd_config& cfg, sssvd_gp
   const int64_t n = ctx->n, m = ctx->m;
   if (n <= 0) throw Status(SSSVD_E_INVALID_ARGUMENT, "no operator set");
   validate_params(cfg.params, n);
-  {
-    // the tail's Householder panels keep a panel's rows on chip: project_qr factors m rows and
-    // low_rank n rows; refuse up front instead of after the shifted-solve phase
-    int w;
-    bool reg;
-    if (!qr_plan((int)m, &w, &reg) || !qr_plan((int)n, &w, &reg))
-      throw Status(SSSVD_E_LENGTH, "run_solve: operator too tall for the on-chip QR panel of the extraction step");
-  }
   CopyFence copy_fence{ctx->cstream};   // every return path waits for the result copies
   const bool use_exp = cfg.mode == SSSVD_MODE_SS_SVD_NT || cfg.mode == SSSVD_MODE_NAIVE_NT;
   const bool naive = cfg.mode == SSSVD_MODE_NAIVE || cfg.mode == SSSVD_MODE_NAIVE_NT;
@@ -1517,7 +1527,7 @@ void sssvd_gpu_destroy(sssvd_gpu_ctx* ctx) {
   DBuf* bufs[] = {&ctx->A, &ctx->G, &ctx->gmax, &ctx->mats, &ctx->ipiv, &ctx->shifts, &ctx->coef, &ctx->S, &ctx->V,
                   &ctx->status, &ctx->minpiv, &ctx->scratch, &ctx->t0, &ctx->t1, &ctx->t2, &ctx->t7, &ctx->gwork,
                   &ctx->lw_linv, &ctx->lw_T, &ctx->lw_src, &ctx->lw_disp, &ctx->lw2_linv, &ctx->lw2_T, &ctx->lw2_src, &ctx->lw2_disp, &ctx->jscr, &ctx->jperm, &ctx->jq, &ctx->jr, &ctx->jj,
-                  &ctx->qy, &ctx->qt, &ctx->qw};
+                  &ctx->qy, &ctx->qt, &ctx->qw, &ctx->ts_tmp, &ctx->ts_rs, &ctx->ts_r};
   for (DBuf* b : bufs) b->release();
   for (auto& b : ctx->tail) b.release();
   if (ctx->comm) nccl().CommDestroy(ctx->comm);

@@ -243,29 +243,6 @@ def test_lookahead_schedule_is_bitwise_plain_schedule(dev, monkeypatch):
         assert np.linalg.norm(look[-1][k] - ref[k]) / np.linalg.norm(ref[k]) <= 1e-10
 
 
-@pytest.mark.parametrize("n,width", [(700, 0), (700, 8), (700, 16), (1500, 32), (2500, 16), (4300, 0), (4300, 8)])
-def test_register_leaf_is_bitwise_slab_leaf(dev, monkeypatch, n, width):
-    """The register-resident leaf LU (one CTA barrier + one cluster barrier per pivot column,
-    candidate rows pushed over DSMEM) performs the same arithmetic with the same pivot choices as
-    the shared-memory slab leaf, so the moments agree bit for bit: every leaf width, ragged panel
-    widths, multi-CTA clusters (n = 4300 > 4096 rows: W = 16 by default) and the oracle."""
-    a = constructed(n + 200, n, np.linspace(0.05, 1.5, n), 31, 32)
-    rg, ro = rules(0.6, 0.9, 8, 0.1)
-    s0 = orc.random_start(n, 8, 42)
-    monkeypatch.setenv("SSSVD_LEAF", "smem")
-    slab = gpu_blocks(dev, a, rg, s0, 2)
-    monkeypatch.delenv("SSSVD_LEAF")
-    if width:
-        monkeypatch.setenv("SSSVD_LEAF_W", str(width))
-    reg = [gpu_blocks(dev, a, rg, s0, 2) for _ in range(3)]   # eager, captured, replayed
-    for r in reg:
-        for k in range(3):
-            assert np.array_equal(slab[k], r[k])
-    ref = orc.MomentAccumulator(orc.form_gram(orc.ProblemMatrix(a)), ro).accumulate(s0, 2).blocks
-    for k in range(3):
-        assert np.linalg.norm(reg[-1][k] - ref[k]) / np.linalg.norm(ref[k]) <= 1e-10
-
-
 def test_graph_capture_and_replay_are_bitwise_eager(dev):
     """The shifted-solve pass runs eagerly on its first sighting, is captured into a CUDA graph on
     the second and replayed afterwards: all three must give the same moments bit for bit, and match

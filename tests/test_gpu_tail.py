@@ -31,6 +31,22 @@ def test_thin_qr_matches_lapack(dev, m, k):
     assert np.linalg.norm(r - r_ref) <= 1e-13 * np.linalg.norm(r_ref)
 
 
+@pytest.mark.parametrize("m,k", [(70000, 48), (400000, 12), (33000, 700)])
+def test_thin_qr_tall_tsqr(dev, m, k):
+    """Above 32768 rows thin_qr runs one level of TSQR (the reference's HouseholderQR has no row
+    limit; 60000 x 784 is the paper's MNIST shape): Q R = A, Q^T Q = I, R upper triangular and equal
+    to LAPACK's up to the signs of its rows."""
+    rng = np.random.default_rng(m + k)
+    a = rng.standard_normal((m, k))
+    q, r = dev.thin_qr(a)
+    _, r_ref = np.linalg.qr(a)
+    assert np.linalg.norm(q @ r - a) <= 1e-14 * np.linalg.norm(a) * np.sqrt(k)
+    assert np.linalg.norm(q.T @ q - np.eye(k)) <= 1e-14 * np.sqrt(m * k)
+    assert np.allclose(np.tril(r, -1), 0.0)
+    sg = np.sign(np.diag(r)) * np.sign(np.diag(r_ref))
+    assert np.linalg.norm(sg[:, None] * r - r_ref) <= 1e-13 * np.linalg.norm(r_ref)
+
+
 def test_thin_qr_graded_and_rank_deficient(dev):
     a = graded(1500, 256, 3)
     a[:, 100] = a[:, 7]          # exact duplicate column
