@@ -271,10 +271,17 @@ def main():
             time.sleep(0.05)
         time.sleep(0.2)
         barrier()
+        # BENCH_PROFILER_RANGE=1 (launch-list captures: ncu --profile-from-start off): the capture
+        # holds exactly the timed steps. A number printed by a run under ncu is never a bench value.
+        prof_range = os.environ.get("BENCH_PROFILER_RANGE") == "1"
+        if prof_range:
+            torch.cuda.profiler.start()
         for i in range(args.steps):
             res = step(evs[i])
             phases.append(res)
         barrier()
+        if prof_range:
+            torch.cuda.profiler.stop()
     launches = sssvd.launch_count() - launches0
     gemm_ms, gemm_flops, gemm_launches = sssvd.profile_gemm_collect()
     sssvd.profile_gemm(False)

@@ -63,6 +63,36 @@ def test_naive_and_two_sided_share_blocks(dev):
     assert nv.count_nonspurious_in_interval == two.count_nonspurious_in_interval
 
 
+@pytest.mark.parametrize("nt", [False, True])
+def test_naive_route_matches_oracle(dev, nt):
+    """The naive / naive-NT route (extract.hpp:108-139: Rayleigh-Ritz on U_S1^T (A^T A) U_S1 by a
+    symmetric eigendecomposition) against the oracle's naive_eigen_route on the same seeded model:
+    same counts and verdicts, found sigma within 1e-10, vectors up to sign."""
+    from paper_2109_13655_b200 import sssvd
+    a, _, sigma, _ = orc.build_model(1, 400, 120, 7)
+    lo, hi = 0.8, 1.2
+    prm = dict(block_size=12, moment_degree=4, quadrature_count=32, seed=42)
+    res = sssvd.run_solve(a.dense, sssvd.RunConfig(lo, hi, mode=sssvd.SolveMode.NaiveNT if nt else sssvd.SolveMode.Naive,
+                                                   params=sssvd.SsParams(**prm)), dev)
+    ref = orc.run_solve(a, orc.RunConfig(lo, hi, mode=orc.NAIVE_NT if nt else orc.NAIVE, params=orc.SsParams(**prm)))
+    assert res.count_in_interval == ref.count_in_interval
+    assert res.count_nonspurious_in_interval == ref.count_nonspurious_in_interval
+    expected = int(np.sum((sigma >= lo) & (sigma <= hi)))
+    assert res.count_nonspurious_in_interval == expected
+    oi = [i for i in range(ref.triplets.count()) if ref.triplets.in_interval[i] and not ref.verdict.spurious[i]]
+    gi = ns_idx(res)
+    assert len(gi) == len(oi)
+    for j, i in zip(gi, oi):                                          # both ascending in sigma
+        so = ref.triplets.sigma[i]
+        assert abs(res.triplets.sigma[j] - so) <= 1e-10 * so
+        for gv, ov in ((res.triplets.right[:, j], ref.triplets.right[:, i]),
+                       (res.triplets.left[:, j], ref.triplets.left[:, i])):
+            # the model's singular values are 0.01 apart: sin(angle) <= residual / gap on either side
+            bound = max(1e-8, 10.0 * (res.exact[j] + ref.residuals.exact[i]) / 0.01)
+            assert min(np.linalg.norm(gv - ov), np.linalg.norm(gv + ov)) <= bound
+        assert res.exact[j] <= max(1e-9, 2 * ref.residuals.exact[i])
+
+
 def test_wide_input_orientation(dev):
     from paper_2109_13655_b200 import sssvd
     m, n = 30, 70
