@@ -447,7 +447,7 @@ cudaError_t trsm_upper_blocks(double2* mats, int ld, long long stride, int r0, i
 // Warp 0 publishes the CTA candidate and the diagonal row straight from the slab, reduces the C
 // candidates over DSMEM, fetches the pivot row (and, in the winning CTA, the old diagonal row),
 // and performs the interchange in the slab.
-template <int W, int NT, int V>
+template <int W, int NT>
 __global__ void __launch_bounds__(NT, 1)
 leaf_lu_kernel(double2* mats, int ld, long long stride, int n, int r0, int w, int R, int* ipiv, int cb) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
@@ -552,19 +552,8 @@ leaf_lu_kernel(double2* mats, int ld, long long stride, int n, int r0, int w, in
       if (nz) {
         const double2 l = cmul(row[j], inv);
         row[j] = l;
-        if (V == 0) {
 #pragma unroll 4
-          for (int c = j + 1; c < W; ++c) row[c] = cfms(row[c], l, urow[c]);
-        } else {
-          // every column of the leaf in flight at once (loads, then the products, then the stores)
-          double2 t[W];
-#pragma unroll
-          for (int c = 0; c < W; ++c)
-            if (c > j) t[c] = cfms(row[c], l, urow[c]);
-#pragma unroll
-          for (int c = 0; c < W; ++c)
-            if (c > j) row[c] = t[c];
-        }
+        for (int c = j + 1; c < W; ++c) row[c] = cfms(row[c], l, urow[c]);
       }
       if (j + 1 < w) {
         const double sc = cabs2(row[j + 1]);
@@ -628,7 +617,7 @@ leaf_lu_kernel(double2* mats, int ld, long long stride, int n, int r0, int w, in
   }
 }
 
-template <int W, int NT, int V>
+template <int W, int NT>
 static cudaError_t launch_leaf(double2* mats, int ld, long long stride, int n, int r0, int w, int cluster,
                                   int* ipiv, int batch, cudaStream_t s, int cb) {
   const int m = n - r0;
@@ -636,7 +625,7 @@ static cudaError_t launch_leaf(double2* mats, int ld, long long stride, int n, i
   // the slab, or the fused left-swap epilogue's move list + gather buffer if that is larger
   const size_t smem = std::max((size_t)R * (W + 1) * sizeof(double2),
                                cb < r0 ? 1024 + (size_t)2 * W * (r0 - cb) * sizeof(double2) : (size_t)0);
-  SSSVD_CUDA_TRY(set_kernel_smem((const void*)leaf_lu_kernel<W, NT, V>, smem, true));
+  SSSVD_CUDA_TRY(set_kernel_smem((const void*)leaf_lu_kernel<W, NT>, smem, true));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cluster, batch, 1);
   cfg.blockDim = dim3(NT, 1, 1);
@@ -650,24 +639,16 @@ static cudaError_t launch_leaf(double2* mats, int ld, long long stride, int n, i
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   note_launch();
-  return cudaLaunchKernelEx(&cfg, leaf_lu_kernel<W, NT, V>, mats, ld, stride, n, r0, w, R, ipiv, cb);
+  return cudaLaunchKernelEx(&cfg, leaf_lu_kernel<W, NT>, mats, ld, stride, n, r0, w, R, ipiv, cb);
 }
 
 cudaError_t leaf_lu(double2* mats, int ld, long long stride, int n, int r0, int w, int W, int cluster, int* ipiv,
                        int batch, cudaStream_t s, int cb) {
   if (cb > r0) return cudaErrorInvalidValue;
-  const char* venv = std::getenv("SSSVD_LEAF_V");
-  const int v = venv ? std::atoi(venv) : 0;
   switch (W) {
-    case 8:
-      return v ? launch_leaf<8, 512, 1>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s, cb)
-               : launch_leaf<8, 512, 0>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s, cb);
-    case 16:
-      return v ? launch_leaf<16, 512, 1>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s, cb)
-               : launch_leaf<16, 512, 0>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s, cb);
-    case 32:
-      return v ? launch_leaf<32, 256, 1>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s, cb)
-               : launch_leaf<32, 256, 0>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s, cb);
+    case 8: return launch_leaf<8, 512>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s, cb);
+    case 16: return launch_leaf<16, 512>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s, cb);
+    case 32: return launch_leaf<32, 256>(mats, ld, stride, n, r0, w, cluster, ipiv, batch, s, cb);
     default: return cudaErrorInvalidValue;
   }
 }
