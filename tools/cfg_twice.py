@@ -7,7 +7,8 @@ c = int(sys.argv[1])
 w = workloads.CONFIGS[c]
 a, _ = workloads.make_operator(c)
 dev = sssvd.Device(0)
-for it in range(3):
+iters = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+for it in range(iters):
     for mode in w.modes:
         cfg = sssvd.RunConfig(w.a, w.b, mode=mode, params=sssvd.SsParams(block_size=w.L, moment_degree=w.M, quadrature_count=w.N), gram_cap=1 << 30)
         t0 = time.time(); r = sssvd.run_solve(a, cfg, dev); wall = time.time() - t0

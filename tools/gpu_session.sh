@@ -1,10 +1,12 @@
+# The evidence run of a round on one B200 (gpurun -- bash tools/gpu_session.sh): GPU tests, smoke, the bench
+# line of every config, the reference arm, and the ncu launch list of the bench command (timed step only).
 set -x
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.max.sm,power.limit --format=csv > gpurun_out/s1_gpu.txt
-python -m pytest tests -m gpu -q -x --durations=15 > gpurun_out/s1_tests.log 2>&1; echo "rc=$?" >> gpurun_out/s1_tests.log
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/s1_smoke.log 2>&1; echo "rc=$?" >> gpurun_out/s1_smoke.log
-python bench.py > gpurun_out/s1_bench_cfg5.jsonl 2> gpurun_out/s1_bench_cfg5.err; echo "rc=$?" >> gpurun_out/s1_bench_cfg5.err
-python bench.py --config 2 --steps 10 > gpurun_out/s1_bench_cfg2.jsonl 2> gpurun_out/s1_bench_cfg2.err
-python bench.py --config 1 --steps 10 --no-cpu-baseline > gpurun_out/s1_bench_cfg1.jsonl 2> gpurun_out/s1_bench_cfg1.err
-python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/s1_ref_cfg5.jsonl 2> gpurun_out/s1_ref_cfg5.err
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/s1_launches_cfg2.csv python tools/profile_once.py 2 0 > gpurun_out/s1_ncu_cfg2.log 2>&1
+python -m pytest tests -m gpu -q --durations=6 > gpurun_out/ev_tests.log 2>&1; echo "rc=$?" >> gpurun_out/ev_tests.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/ev_smoke.log 2>&1; echo "rc=$?" >> gpurun_out/ev_smoke.log
+python bench.py > gpurun_out/ev_bench_cfg5.jsonl 2> gpurun_out/ev_bench_cfg5.err; echo "rc=$?" >> gpurun_out/ev_bench_cfg5.err
+python bench.py --impl reference > gpurun_out/ev_ref_cfg5.jsonl 2> gpurun_out/ev_ref_cfg5.err
+for c in 1 2 3 4; do
+  python bench.py --config $c --steps 5 --no-cpu-baseline > gpurun_out/ev_bench_cfg$c.jsonl 2> gpurun_out/ev_bench_cfg$c.err
+done
+BENCH_PROFILER_RANGE=1 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/ev_launches_bench_cfg5.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ev_ncu_bench5.log 2>&1; echo "rc=$?" >> gpurun_out/ev_ncu_bench5.log
