@@ -12,6 +12,7 @@
 // Shared-memory row pitches are padded (A: 20, B: 66 double2) so every fragment load is one
 // conflict-free LDS.128 per quarter-warp.
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <cuda.h>
@@ -88,6 +89,15 @@ void zgemm_stamp_harvest(const std::vector<double>& flops) {
     if (en[i] == 0 || st[i] == ~0ull) continue;   // empty launch
     iv.emplace_back(st[i], en[i]);
     f += flops[i];
+  }
+  // SSSVD_GEMM_DUMP=<path>: append every launch of the pass as "start_ns end_ns flops" (tools/gemm_timeline.py)
+  if (const char* dump = std::getenv("SSSVD_GEMM_DUMP")) {
+    if (FILE* fp = std::fopen(dump, "a")) {
+      std::fprintf(fp, "# pass %zu launches\n", cnt);
+      for (size_t i = 0; i < cnt; ++i)
+        if (en[i] != 0 && st[i] != ~0ull) std::fprintf(fp, "%llu %llu %.0f\n", st[i], en[i], flops[i]);
+      std::fclose(fp);
+    }
   }
   std::sort(iv.begin(), iv.end());
   double t = 0;
