@@ -93,6 +93,31 @@ def test_naive_route_matches_oracle(dev, nt):
         assert res.exact[j] <= max(1e-9, 2 * ref.residuals.exact[i])
 
 
+def test_tall_operator_goes_through_tsqr(dev):
+    """m = 70000 rows: project_qr's thin QR (extract.hpp:46-52) runs one level of TSQR above 32768
+    rows. Same counts as the oracle, sigma within 1e-10, left / right vectors up to sign within the
+    residual / gap bound, Galerkin residual at roundoff."""
+    from paper_2109_13655_b200 import sssvd
+    a, _, sigma, _ = orc.build_model(1, 70000, 48, 7)
+    lo, hi = 0.2, 0.33
+    prm = dict(block_size=8, moment_degree=3, quadrature_count=16, seed=42)
+    res = sssvd.run_solve(a.dense, sssvd.RunConfig(lo, hi, params=sssvd.SsParams(**prm)), dev)
+    ref = orc.run_solve(a, orc.RunConfig(lo, hi, params=orc.SsParams(**prm)))
+    expected = int(np.sum((sigma >= lo) & (sigma <= hi)))
+    assert res.count_nonspurious_in_interval == ref.count_nonspurious_in_interval == expected
+    gi = ns_idx(res)
+    oi = [i for i in range(ref.triplets.count()) if ref.triplets.in_interval[i] and not ref.verdict.spurious[i]]
+    for j, i in zip(gi, oi):
+        so = ref.triplets.sigma[i]
+        assert abs(res.triplets.sigma[j] - so) <= 1e-10 * so
+        bound = max(1e-8, 10.0 * (res.exact[j] + ref.residuals.exact[i]) / 0.01)   # sigma spacing 0.01
+        for gv, ov in ((res.triplets.right[:, j], ref.triplets.right[:, i]),
+                       (res.triplets.left[:, j], ref.triplets.left[:, i])):
+            assert min(np.linalg.norm(gv - ov), np.linalg.norm(gv + ov)) <= bound
+        assert res.galerkin[j] <= 1e-12
+        assert np.linalg.norm(res.triplets.left[:, j]) == pytest.approx(1.0, abs=1e-12)
+
+
 def test_wide_input_orientation(dev):
     from paper_2109_13655_b200 import sssvd
     m, n = 30, 70

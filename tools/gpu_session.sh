@@ -9,4 +9,5 @@ python bench.py --impl reference > gpurun_out/ev_ref_cfg5.jsonl 2> gpurun_out/ev
 for c in 1 2 3 4; do
   python bench.py --config $c --steps 5 --no-cpu-baseline > gpurun_out/ev_bench_cfg$c.jsonl 2> gpurun_out/ev_bench_cfg$c.err
 done
-BENCH_PROFILER_RANGE=1 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/ev_launches_bench_cfg5.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ev_ncu_bench5.log 2>&1; echo "rc=$?" >> gpurun_out/ev_ncu_bench5.log
+BENCH_PROFILER_RANGE=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/ev_launches_bench_cfg5.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ev_ncu_bench5.log 2>&1; echo "rc=$?" >> gpurun_out/ev_ncu_bench5.log
+python -m pytest tests/test_gpu_parity_configs.py -m gpu -q -s > gpurun_out/ev_parity_reports.log 2>&1; echo "rc=$?" >> gpurun_out/ev_parity_reports.log
