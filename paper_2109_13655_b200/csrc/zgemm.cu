@@ -239,7 +239,7 @@ __global__ void __launch_bounds__((64 / (8 * WI)) * (64 / (8 * WJ)) * 32, WI * W
 zgemm_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long long sA,
              const double2* __restrict__ B, int ldb, long long sB, const int* __restrict__ brow, int sR,
              double2* C, int ldc, long long sC, unsigned long long* __restrict__ stamp, int stamp_cap,
-             unsigned* desync, int desync_first, unsigned desync_ns) {
+             unsigned* desync, int desync_first, unsigned desync_ns, int group_m) {
   constexpr int WARPS_N = 64 / (8 * WJ);
   constexpr int THREADS = (64 / (8 * WI)) * WARPS_N * 32;
   extern __shared__ __align__(16) double2 smem[];
@@ -281,7 +281,10 @@ zgemm_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long l
   // from L2 meanwhile (ncu: 15.3 GB read for 8.7 GB algorithmic). Instead consecutive CTAs walk
   // down GROUP_M m-tiles of one n-tile before moving to the next n-tile, so a B tile is reused
   // GROUP_M times back to back and the group's A rows (GROUP_M x 256 KB at K = 256) stay in L2.
-  constexpr int GROUP_M = 32;
+  // The host picks GROUP_M = 32 when one shift's B operand would not stay in L2 beside the C
+  // stream, else 1 (the plain order: measured 2 % faster on the config-2 shapes, whose A and B
+  // fit L2 together).
+  const int GROUP_M = group_m;
   int tile_m, tile_n;
   {
     const int tiles_n = gridDim.x, tiles_m = gridDim.y;
@@ -786,8 +789,9 @@ static cudaError_t launch(int M, int N, int K, const double2* A, int lda, long l
       ns = desync_ns(KT);
     }
   }
+  const int group_m = (double)K * N * sizeof(double2) > 24e6 ? 32 : 1;
   kern<<<grid, 128, zgemm_sub_smem(), stream>>>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, stamp,
-                                                  g_prof.cap, desync, first, ns);
+                                                  g_prof.cap, desync, first, ns, group_m);
   return cudaGetLastError();
 }
 
