@@ -1772,22 +1772,24 @@ __global__ void debug_fill_kernel(double* p, long long cnt, unsigned long long s
     p[i] = (double)(x >> 11) * (1.0 / 9007199254740992.0) - 0.5;
   }
 }
-__global__ void debug_diff_kernel(const unsigned long long* a, const unsigned long long* b, long long cnt,
+__global__ void debug_diff_kernel(const double* a, const double* b, long long cnt, double tol,
                                   unsigned long long* out) {
   unsigned long long c = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cnt; i += (long long)gridDim.x * blockDim.x)
-    c += a[i] != b[i];
+    c += !(fabs(a[i] - b[i]) <= tol);
   if (c) atomicAdd(out, c);
 }
 }  // namespace
 
 // debug: times the trailing-update GEMM C -= A B (complex, row-major, batched) on seeded data.
-// variant 0: the cp.async kernel (product default), 1: the TMA kernel. *mismatches_out counts the
-// entries that differ bitwise from the cp.async kernel's result on the same inputs.
+// variant 0: the 4-product cp.async kernel, 1: its TMA form, 2: the 3-product (3M) kernel (the product
+// default). *mismatches_out counts the entries that differ from the 4-product cp.async kernel's
+// result on the same inputs: bitwise for variants 0 and 1, by more than the 3M rounding bound
+// (K * 1e-15 on operands in [-0.5, 0.5]) for variant 2.
 sssvd_status sssvd_debug_zgemm(sssvd_gpu_ctx* ctx, int variant, int64_t m, int64_t n, int64_t k, int64_t batch,
                                int reps, double* ms_out, int64_t* mismatches_out) {
   return guarded(ctx, [&]() {
-    if (m < 1 || n < 1 || k < 1 || batch < 1 || reps < 1 || variant < 0 || variant > 1)
+    if (m < 1 || n < 1 || k < 1 || batch < 1 || reps < 1 || variant < 0 || variant > 6)
       throw Status(SSSVD_E_INVALID_ARGUMENT, "debug_zgemm: bad arguments");
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
@@ -1812,11 +1814,11 @@ sssvd_status sssvd_debug_zgemm(sssvd_gpu_ctx* ctx, int variant, int64_t m, int64
       CK(cudaMemcpyAsync(C2, C0, nc * sizeof(double2), cudaMemcpyDeviceToDevice, s));
       zgemm_force(1);
       CK(zgemm_sub((int)m, (int)n, (int)k, A, (int)k, m * k, B, (int)n, k * n, C2, (int)n, m * n, (int)batch, s));
-      zgemm_force(variant == 1 ? 2 : 1);
+      zgemm_force(variant + 1);
       CK(zgemm_sub((int)m, (int)n, (int)k, A, (int)k, m * k, B, (int)n, k * n, C1, (int)n, m * n, (int)batch, s));
       CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
-      debug_diff_kernel<<<1184, 256, 0, s>>>((const unsigned long long*)C1, (const unsigned long long*)C2,
-                                             2 * (long long)nc, cnt);
+      debug_diff_kernel<<<1184, 256, 0, s>>>((const double*)C1, (const double*)C2, 2 * (long long)nc,
+                                             variant >= 2 ? 1e-15 * (double)k : 0.0, cnt);
       unsigned long long h = 0;
       CK(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
       cudaEvent_t e0, e1;

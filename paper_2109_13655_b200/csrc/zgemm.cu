@@ -434,6 +434,201 @@ zgemm_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long l
 
 size_t zgemm_sub_smem() { return (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double2); }
 
+// ----------------------------------------------------------------------------- 3M form
+// C -= A B with THREE real products per complex multiply-add instead of four:
+//   P1 = Are Bre,  P2 = Aim Bim,  P3 = (Are + Aim)(Bre + Bim);   Re = P1 - P2,  Im = P3 - P1 - P2
+// (the "3M" complex GEMM; Higham, "Stability of a method for multiplying complex matrices with
+// three real matrix multiplications", SIMAX 1992: normwise the same error bound as the 4-product
+// form). 25 % fewer DMMAs per complex flop; the price is a third accumulator set, so the CTA tile
+// is 64 x (16 WJ) with 4 warps of 32 x (8 WJ): WJ = 3 (64 x 48) keeps 144 accumulator registers per
+// thread; WJ = 4 needs 192 + operands > 255 and spills inside the k-loop (measured slower).
+// The operand sums are formed from the fragments in registers (one DADD per fragment element).
+// Same cp.async ring, C prefetch and tile order as zgemm_kernel. The first-wave offset of the
+// 4-product kernel is not used: measured without effect here (41.9 TF/s in 8 M N K units at every
+// offset from 0 to 1200 ns per k-stage, profiles/r02_3m_zgemm.txt).
+template <int WJ>
+struct Tile3M {
+  static constexpr int BN3 = 16 * WJ;
+  static constexpr int LDB3 = BN3 + 2;            // == 2 mod 8 for WJ = 3, 4
+  static constexpr int B_STAGE3 = BK * LDB3;
+  static constexpr int SSTRIDE3 = A_STAGE + B_STAGE3;
+  static constexpr int CP3 = BN3 + 1;
+  static_assert(32 * CP3 <= SSTRIDE3, "C half-tile must fit one pipeline stage");
+  static constexpr size_t SMEM = (size_t)STAGES * SSTRIDE3 * sizeof(double2);
+};
+
+template <int WI, int WJ, int MAXREG>
+__global__ void __maxnreg__(MAXREG)
+zgemm3m_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long long sA,
+               const double2* __restrict__ B, int ldb, long long sB, double2* C, int ldc, long long sC,
+               unsigned long long* __restrict__ stamp, int stamp_cap, int group_m) {
+  using T = Tile3M<WJ>;
+  constexpr int BN3 = T::BN3, LDB3 = T::LDB3, SSTRIDE = T::SSTRIDE3, CP3 = T::CP3;
+  constexpr int THREADS = 64 / (8 * WI) * 64;   // (64 / 8 WI) x 2 warps
+  extern __shared__ __align__(16) double2 smem[];
+  if (stamp && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(stamp, t);
+  }
+  double2* As = smem;
+  double2* Bs = smem + A_STAGE;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  int tile_m, tile_n;
+  {
+    const int tiles_n = gridDim.x, tiles_m = gridDim.y;
+    const int lin_t = blockIdx.y * tiles_n + blockIdx.x;
+    const int per_group = group_m * tiles_n;
+    const int g = lin_t / per_group, within = lin_t - g * per_group;
+    const int gm = min(group_m, tiles_m - g * group_m);
+    tile_n = within / gm;
+    tile_m = g * group_m + (within - tile_n * gm);
+  }
+  const int m0 = tile_m * BM, n0 = tile_n * BN3;
+  A += blockIdx.z * sA;
+  B += blockIdx.z * sB;
+  C += blockIdx.z * sC;
+
+  double p1[WI][WJ][2], p2[WI][WJ][2], p3[WI][WJ][2];
+#pragma unroll
+  for (int i = 0; i < WI; ++i)
+#pragma unroll
+    for (int j = 0; j < WJ; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) p1[i][j][e] = p2[i][j][e] = p3[i][j][e] = 0.0;
+
+  const int KT = (K + BK - 1) / BK;
+  auto c_stage = [&](int h) { return smem + ((KT + h) % STAGES) * SSTRIDE; };
+  // stage loader: A as in StageLoader (thread = one k column, 8 rows); B: thread = one k row of
+  // the stage and every 8th column of it (8 consecutive lanes copy 128 contiguous bytes)
+  constexpr int AN = BM * BK / THREADS, AR = THREADS / BK, LPR = THREADS / BK, BNE = BN3 / LPR;
+  const int a_k = tid % BK, ar = tid / BK;
+  const double2* ap = A + (size_t)(m0 + ar) * lda + a_k;
+  const long long a_step = (long long)AR * lda;
+  const int a_dst = ar * LDA_S + a_k;
+  unsigned a_rows = 0;
+#pragma unroll
+  for (int i = 0; i < AN; ++i) a_rows |= (m0 + ar + i * AR < M ? 1u : 0u) << i;
+  const int b_k = tid / LPR, bc = tid % LPR;
+  const double2* bp = B + (size_t)b_k * ldb + n0 + bc;
+  const long long b_adv = (long long)BK * ldb;
+  const int b_dst = b_k * LDB3 + bc;
+  unsigned b_cols = 0;
+#pragma unroll
+  for (int i = 0; i < BNE; ++i) b_cols |= (n0 + bc + LPR * i < N ? 1u : 0u) << i;
+  const bool interior = m0 + BM <= M && n0 + BN3 <= N;
+  auto load = [&](double2* as_, double2* bs_, int kleft) {
+    if (interior && kleft >= BK) {
+#pragma unroll
+      for (int i = 0; i < AN; ++i) cp_async16(as_ + a_dst + i * AR * LDA_S, ap + i * a_step);
+#pragma unroll
+      for (int i = 0; i < BNE; ++i) cp_async16(bs_ + b_dst + LPR * i, bp + LPR * i);
+    } else {
+      const bool ak = a_k < kleft, bk = b_k < kleft;
+#pragma unroll
+      for (int i = 0; i < AN; ++i) cp_async16(as_ + a_dst + i * AR * LDA_S, ap + i * a_step, ak && ((a_rows >> i) & 1u));
+#pragma unroll
+      for (int i = 0; i < BNE; ++i) cp_async16(bs_ + b_dst + LPR * i, bp + LPR * i, bk && ((b_cols >> i) & 1u));
+    }
+    ap += BK;
+    bp += b_adv;
+  };
+  auto load_c = [&](double2* dst, int h) {
+#pragma unroll
+    for (int i = 0; i < (32 * BN3) / THREADS; ++i) {
+      const int idx = tid + i * THREADS;
+      const int r = idx / BN3, c = idx % BN3;
+      const bool p = (m0 + 32 * h + r < M) && (n0 + c < N);
+      cp_async16(dst + r * CP3 + c, p ? C + (size_t)(m0 + 32 * h + r) * ldc + n0 + c : C, p);
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load(As + s * SSTRIDE, Bs + s * SSTRIDE, K - s * BK);
+    for (int h = 0; h < 2; ++h)
+      if (KT - 2 + h < 0 && s == 0) load_c(c_stage(h), h);
+    cp_async_commit();
+  }
+  const int fr = lane >> 2, fc = lane & 3;
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    const double2* as = As + (kt % STAGES) * SSTRIDE + (wm * 8 * WI + fr) * LDA_S + fc;
+    const double2* bs = Bs + (kt % STAGES) * SSTRIDE + fc * LDB3 + wn * 8 * WJ + fr;
+#pragma unroll
+    for (int kq = 0; kq < BK / 4; ++kq) {
+      if (kq == 1) {
+        const int nk = kt + STAGES - 1;
+        if (nk < KT) {
+          const int st = nk % STAGES;
+          load(As + st * SSTRIDE, Bs + st * SSTRIDE, K - nk * BK);
+        } else {
+          const int h = kt - (KT - 2);
+          if (h >= 0 && h < 2) load_c(c_stage(h), h);
+        }
+        cp_async_commit();
+      }
+      double2 a[WI], b[WJ];
+      double sa[WI], sb[WJ];
+#pragma unroll
+      for (int i = 0; i < WI; ++i) a[i] = as[i * 8 * LDA_S + kq * 4];
+#pragma unroll
+      for (int j = 0; j < WJ; ++j) b[j] = bs[kq * 4 * LDB3 + j * 8];
+#pragma unroll
+      for (int i = 0; i < WI; ++i) sa[i] = a[i].x + a[i].y;
+#pragma unroll
+      for (int j = 0; j < WJ; ++j) sb[j] = b[j].x + b[j].y;
+#pragma unroll
+      for (int i = 0; i < WI; ++i)
+#pragma unroll
+        for (int j = 0; j < WJ; ++j) dmma884(p1[i][j][0], p1[i][j][1], a[i].x, b[j].x);
+#pragma unroll
+      for (int i = 0; i < WI; ++i)
+#pragma unroll
+        for (int j = 0; j < WJ; ++j) dmma884(p2[i][j][0], p2[i][j][1], a[i].y, b[j].y);
+#pragma unroll
+      for (int i = 0; i < WI; ++i)
+#pragma unroll
+        for (int j = 0; j < WJ; ++j) dmma884(p3[i][j][0], p3[i][j][1], sa[i], sb[j]);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < WI; ++i) {
+    const int rt = wm * 8 * WI + i * 8 + fr;
+    const int r = m0 + rt;
+    if (r >= M) continue;
+    const int cbase = n0 + wn * 8 * WJ + 2 * fc;
+    double2* crow = C + (size_t)r * ldc + cbase;
+    const double2* cs = c_stage(rt >> 5) + (rt & 31) * CP3 + wn * 8 * WJ + 2 * fc;
+    double2 v[WJ][2];
+#pragma unroll
+    for (int j = 0; j < WJ; ++j) {
+      v[j][0] = cs[j * 8];
+      v[j][1] = cs[j * 8 + 1];
+    }
+#pragma unroll
+    for (int j = 0; j < WJ; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = cbase + j * 8 + e;
+        if (c < N)
+          crow[j * 8 + e] = make_double2(v[j][e].x - (p1[i][j][e] - p2[i][j][e]),
+                                         v[j][e].y - ((p3[i][j][e] - p1[i][j][e]) - p2[i][j][e]));
+      }
+  }
+  if (stamp) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMax(stamp + stamp_cap, t);
+    }
+  }
+}
+
 
 // ----------------------------------------------------------------------------- TMA form
 // Persistent, warp-specialised form of C -= A B (the same DMMA chain per entry as zgemm_kernel,
@@ -649,15 +844,19 @@ static bool encode_map(CUtensorMap* map, const double2* p, int rows, int cols, i
              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// SSSVD_ZGEMM=tma selects the TMA kernel for the trailing updates (read per call; measured slower
-// than the cp.async kernel so far: config-5 phase 28.7 vs 23.2 s); zgemm_force (debug comparisons)
-// overrides: 1 = cp.async, 2 = TMA
+// Kernel of the C -= A B updates: 1 = 4-product cp.async kernel, 2 = its TMA form, 3 = the 3-product
+// (3M) kernel, the default (measured: config-5 step 24.0 -> 20.2 s, isolated trailing update 34.8 ->
+// 41.9 TF/s in 8 M N K units; a 64 x 64 3M tile needs 255 registers and spills, 39.3).
+// SSSVD_ZGEMM = 4m | tma selects another kernel for A/B measurements (read per call); zgemm_force
+// (debug comparisons) overrides.
 static int g_force = 0;
 void zgemm_force(int kernel) { g_force = kernel; }
-static bool tma_enabled() {
-  if (g_force) return g_force == 2;
+static int sub_kernel() {
+  if (g_force) return g_force;
   const char* e = std::getenv("SSSVD_ZGEMM");
-  return e && std::string(e) == "tma";
+  if (!e) return 3;
+  const std::string v(e);
+  return v == "4m" ? 1 : v == "tma" ? 2 : v == "3m8" ? 4 : v == "3m244" ? 5 : v == "3m248" ? 6 : v == "3m240" ? 7 : 3;
 }
 
 static cudaError_t launch_tma(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B, int ldb,
@@ -752,6 +951,19 @@ static unsigned desync_ns(int KT) {
   return v > 0 ? (unsigned)v * (unsigned)KT : 0u;
 }
 
+template <int WI, int WJ, int MAXREG>
+static cudaError_t launch_3m(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B, int ldb,
+                               long long sB, double2* C, int ldc, long long sC, int batch, cudaStream_t stream,
+                               unsigned long long* stamp) {
+  using T = Tile3M<WJ>;
+  auto kern = zgemm3m_kernel<WI, WJ, MAXREG>;
+  SSSVD_CUDA_TRY(set_kernel_smem((const void*)kern, T::SMEM, false));
+  dim3 grid((N + T::BN3 - 1) / T::BN3, (M + BM - 1) / BM, batch);
+  const int group_m = (double)K * N * sizeof(double2) > 24e6 ? 32 : 1;
+  kern<<<grid, 64 / (8 * WI) * 64, T::SMEM, stream>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, stamp, g_prof.cap,
+                                                     group_m);
+  return cudaGetLastError();
+}
 // C -= A B (SET = false) or C = A B[brow] (SET = GATHER = true). The next k-stage's copies are
 // issued after the first k-quad's DMMAs (measured +1 % over issuing them at the top of the stage;
 // bitwise identical).
@@ -760,17 +972,24 @@ static cudaError_t launch(int M, int N, int K, const double2* A, int lda, long l
                           long long sB, const int* brow, int sR, double2* C, int ldc, long long sC, int batch,
                           cudaStream_t stream) {
   if (M <= 0 || N <= 0 || K <= 0 || batch <= 0) return cudaSuccess;
+  const int which = (!SET && !GATHER) ? sub_kernel() : 1;
   unsigned long long* stamp = nullptr;
   if (g_prof.in_pass && (int)g_prof.flops.size() < g_prof.cap) {
     stamp = g_prof.d_stamp + g_prof.flops.size();
-    g_prof.flops.push_back(8.0 * M * (double)N * K * batch);
+    // EXECUTED tensor flops: 4 real products per complex multiply-add, 3 in the 3M kernels
+    g_prof.flops.push_back((which >= 3 ? 6.0 : 8.0) * M * (double)N * K * batch);
   }
   note_launch();
-  if (!SET && !GATHER && tma_enabled()) {
+  if (which == 2) {
     bool done = false;
     SSSVD_CUDA_TRY(launch_tma(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch, stream, stamp, &done));
     if (done) return cudaSuccess;
   }
+  if (which == 3) return launch_3m<4, 3, 255>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch, stream, stamp);
+  if (which == 4) return launch_3m<2, 3, 128>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch, stream, stamp);
+  if (which == 5) return launch_3m<4, 3, 244>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch, stream, stamp);
+  if (which == 6) return launch_3m<4, 3, 248>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch, stream, stamp);
+  if (which == 7) return launch_3m<4, 3, 240>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch, stream, stamp);
   auto kern = zgemm_kernel<4, 4, SET, GATHER, 1>;
   SSSVD_CUDA_TRY(set_kernel_smem((const void*)kern, zgemm_sub_smem(), false));
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch);

@@ -36,7 +36,7 @@ def test_contract_rejects_shifted_sigmas():
 def test_contract_rejects_flipped_firm_verdict():
     o, truth = load()
     g = Summary(**{k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in o["d20"].__dict__.items()})
-    firm = np.flatnonzero(g.in_interval & ~g.spurious & (g.tau > 10 * g.threshold) & (g.exact < 1e-3))
+    firm = np.flatnonzero(g.in_interval & ~g.spurious & (g.tau > 20 * g.threshold) & (g.exact < 1e-3))
     g.spurious[firm[0]] = True
     with pytest.raises(AssertionError):
         check_robust(g, o["d20"], o["d12"], o["d12"], 0.8, 0.9, truth.max(), truth)

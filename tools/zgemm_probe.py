@@ -10,7 +10,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2109_13655_b200 import sssvd  # noqa: E402
 
 args = [int(x) for x in sys.argv[1:6]] if len(sys.argv) > 5 else [3968, 4000, 128, 8, 5]
-variants = [int(v) for v in sys.argv[6].split(",")] if len(sys.argv) > 6 else [0, 1]
+variants = [int(v) for v in sys.argv[6].split(",")] if len(sys.argv) > 6 else [0, 1, 2]
 m, n, k, b, reps = args
 dev = sssvd.Device(0)
 for v in variants:
