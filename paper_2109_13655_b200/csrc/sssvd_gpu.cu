@@ -1789,7 +1789,7 @@ __global__ void debug_diff_kernel(const double* a, const double* b, long long cn
 sssvd_status sssvd_debug_zgemm(sssvd_gpu_ctx* ctx, int variant, int64_t m, int64_t n, int64_t k, int64_t batch,
                                int reps, double* ms_out, int64_t* mismatches_out) {
   return guarded(ctx, [&]() {
-    if (m < 1 || n < 1 || k < 1 || batch < 1 || reps < 1 || variant < 0 || variant > 6)
+    if (m < 1 || n < 1 || k < 1 || batch < 1 || reps < 1 || variant < 0 || variant > 2)
       throw Status(SSSVD_E_INVALID_ARGUMENT, "debug_zgemm: bad arguments");
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;

@@ -443,9 +443,7 @@ size_t zgemm_sub_smem() { return (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(d
 // is 64 x (16 WJ) with 4 warps of 32 x (8 WJ): WJ = 3 (64 x 48) keeps 144 accumulator registers per
 // thread; WJ = 4 needs 192 + operands > 255 and spills inside the k-loop (measured slower).
 // The operand sums are formed from the fragments in registers (one DADD per fragment element).
-// Same cp.async ring, C prefetch and tile order as zgemm_kernel. The first-wave offset of the
-// 4-product kernel is not used: measured without effect here (41.9 TF/s in 8 M N K units at every
-// offset from 0 to 1200 ns per k-stage, profiles/r02_3m_zgemm.txt).
+// Same cp.async ring, C prefetch, tile order and first-wave offset as zgemm_kernel.
 template <int WJ>
 struct Tile3M {
   static constexpr int BN3 = 16 * WJ;
@@ -457,19 +455,38 @@ struct Tile3M {
   static constexpr size_t SMEM = (size_t)STAGES * SSTRIDE3 * sizeof(double2);
 };
 
-template <int WI, int WJ, int MAXREG>
-__global__ void __maxnreg__(MAXREG)
+template <int WJ>
+__global__ void __launch_bounds__(128, 2)
 zgemm3m_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long long sA,
                const double2* __restrict__ B, int ldb, long long sB, double2* C, int ldc, long long sC,
-               unsigned long long* __restrict__ stamp, int stamp_cap, int group_m) {
+               unsigned long long* __restrict__ stamp, int stamp_cap, unsigned* desync, int desync_first,
+               unsigned desync_ns, int group_m) {
   using T = Tile3M<WJ>;
   constexpr int BN3 = T::BN3, LDB3 = T::LDB3, SSTRIDE = T::SSTRIDE3, CP3 = T::CP3;
-  constexpr int THREADS = 64 / (8 * WI) * 64;   // (64 / 8 WI) x 2 warps
+  constexpr int THREADS = 128, WI = 4;
   extern __shared__ __align__(16) double2 smem[];
   if (stamp && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     atomicMin(stamp, t);
+  }
+  if (desync) {
+    const int lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    if (lin < desync_first) {
+      if (threadIdx.x == 0) {
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        if (atomicAdd(desync + sm, 1u) & 1u) {
+          unsigned long long t0, t1;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+          do {
+            __nanosleep(1000);
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+          } while (t1 - t0 < desync_ns);
+        }
+      }
+      __syncthreads();
+    }
   }
   double2* As = smem;
   double2* Bs = smem + A_STAGE;
@@ -502,7 +519,7 @@ zgemm3m_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long
   auto c_stage = [&](int h) { return smem + ((KT + h) % STAGES) * SSTRIDE; };
   // stage loader: A as in StageLoader (thread = one k column, 8 rows); B: thread = one k row of
   // the stage and every 8th column of it (8 consecutive lanes copy 128 contiguous bytes)
-  constexpr int AN = BM * BK / THREADS, AR = THREADS / BK, LPR = THREADS / BK, BNE = BN3 / LPR;
+  constexpr int AN = BM * BK / THREADS, AR = THREADS / BK, BNE = BN3 / 8;
   const int a_k = tid % BK, ar = tid / BK;
   const double2* ap = A + (size_t)(m0 + ar) * lda + a_k;
   const long long a_step = (long long)AR * lda;
@@ -510,26 +527,26 @@ zgemm3m_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long
   unsigned a_rows = 0;
 #pragma unroll
   for (int i = 0; i < AN; ++i) a_rows |= (m0 + ar + i * AR < M ? 1u : 0u) << i;
-  const int b_k = tid / LPR, bc = tid % LPR;
+  const int b_k = tid >> 3, bc = tid & 7;
   const double2* bp = B + (size_t)b_k * ldb + n0 + bc;
   const long long b_adv = (long long)BK * ldb;
   const int b_dst = b_k * LDB3 + bc;
   unsigned b_cols = 0;
 #pragma unroll
-  for (int i = 0; i < BNE; ++i) b_cols |= (n0 + bc + LPR * i < N ? 1u : 0u) << i;
+  for (int i = 0; i < BNE; ++i) b_cols |= (n0 + bc + 8 * i < N ? 1u : 0u) << i;
   const bool interior = m0 + BM <= M && n0 + BN3 <= N;
   auto load = [&](double2* as_, double2* bs_, int kleft) {
     if (interior && kleft >= BK) {
 #pragma unroll
       for (int i = 0; i < AN; ++i) cp_async16(as_ + a_dst + i * AR * LDA_S, ap + i * a_step);
 #pragma unroll
-      for (int i = 0; i < BNE; ++i) cp_async16(bs_ + b_dst + LPR * i, bp + LPR * i);
+      for (int i = 0; i < BNE; ++i) cp_async16(bs_ + b_dst + 8 * i, bp + 8 * i);
     } else {
       const bool ak = a_k < kleft, bk = b_k < kleft;
 #pragma unroll
       for (int i = 0; i < AN; ++i) cp_async16(as_ + a_dst + i * AR * LDA_S, ap + i * a_step, ak && ((a_rows >> i) & 1u));
 #pragma unroll
-      for (int i = 0; i < BNE; ++i) cp_async16(bs_ + b_dst + LPR * i, bp + LPR * i, bk && ((b_cols >> i) & 1u));
+      for (int i = 0; i < BNE; ++i) cp_async16(bs_ + b_dst + 8 * i, bp + 8 * i, bk && ((b_cols >> i) & 1u));
     }
     ap += BK;
     bp += b_adv;
@@ -554,7 +571,7 @@ zgemm3m_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long
   for (int kt = 0; kt < KT; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
-    const double2* as = As + (kt % STAGES) * SSTRIDE + (wm * 8 * WI + fr) * LDA_S + fc;
+    const double2* as = As + (kt % STAGES) * SSTRIDE + (wm * 32 + fr) * LDA_S + fc;
     const double2* bs = Bs + (kt % STAGES) * SSTRIDE + fc * LDB3 + wn * 8 * WJ + fr;
 #pragma unroll
     for (int kq = 0; kq < BK / 4; ++kq) {
@@ -597,7 +614,7 @@ zgemm3m_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < WI; ++i) {
-    const int rt = wm * 8 * WI + i * 8 + fr;
+    const int rt = wm * 32 + i * 8 + fr;
     const int r = m0 + rt;
     if (r >= M) continue;
     const int cbase = n0 + wn * 8 * WJ + 2 * fc;
@@ -628,7 +645,6 @@ zgemm3m_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long
     }
   }
 }
-
 
 // ----------------------------------------------------------------------------- TMA form
 // Persistent, warp-specialised form of C -= A B (the same DMMA chain per entry as zgemm_kernel,
@@ -846,7 +862,9 @@ static bool encode_map(CUtensorMap* map, const double2* p, int rows, int cols, i
 
 // Kernel of the C -= A B updates: 1 = 4-product cp.async kernel, 2 = its TMA form, 3 = the 3-product
 // (3M) kernel, the default (measured: config-5 step 24.0 -> 20.2 s, isolated trailing update 34.8 ->
-// 41.9 TF/s in 8 M N K units; a 64 x 64 3M tile needs 255 registers and spills, 39.3).
+// 41.9 TF/s in 8 M N K units). Forms of the 3M kernel measured slower and not kept
+// (profiles/r02_3m_zgemm.txt): 64 x 64 tiles (255 registers, spills: 39.3), 8 warps of 16 x 24
+// (40.5), a multi-tile CTA with cross-tile stage prefetch and a global-memory C epilogue (40.7).
 // SSSVD_ZGEMM = 4m | tma selects another kernel for A/B measurements (read per call); zgemm_force
 // (debug comparisons) overrides.
 static int g_force = 0;
@@ -856,7 +874,7 @@ static int sub_kernel() {
   const char* e = std::getenv("SSSVD_ZGEMM");
   if (!e) return 3;
   const std::string v(e);
-  return v == "4m" ? 1 : v == "tma" ? 2 : v == "3m8" ? 4 : v == "3m244" ? 5 : v == "3m248" ? 6 : v == "3m240" ? 7 : 3;
+  return v == "4m" ? 1 : v == "tma" ? 2 : 3;
 }
 
 static cudaError_t launch_tma(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B, int ldb,
@@ -951,19 +969,36 @@ static unsigned desync_ns(int KT) {
   return v > 0 ? (unsigned)v * (unsigned)KT : 0u;
 }
 
-template <int WI, int WJ, int MAXREG>
+template <int WJ>
 static cudaError_t launch_3m(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B, int ldb,
-                               long long sB, double2* C, int ldc, long long sC, int batch, cudaStream_t stream,
-                               unsigned long long* stamp) {
+                             long long sB, double2* C, int ldc, long long sC, int batch, cudaStream_t stream,
+                             unsigned long long* stamp) {
   using T = Tile3M<WJ>;
-  auto kern = zgemm3m_kernel<WI, WJ, MAXREG>;
+  auto kern = zgemm3m_kernel<WJ>;
   SSSVD_CUDA_TRY(set_kernel_smem((const void*)kern, T::SMEM, false));
   dim3 grid((N + T::BN3 - 1) / T::BN3, (M + BM - 1) / BM, batch);
+  // first-wave offset as in the 4-product launcher (measured neutral on this kernel: 41.88-41.90
+  // TF/s at every offset from 0 to 1200 ns per k-stage, profiles/r02_3m_zgemm.txt)
+  unsigned* desync = nullptr;
+  int first = 0;
+  unsigned ns = 0;
+  const int KT = (K + BK - 1) / BK;
+  const long long ctas = (long long)grid.x * grid.y * grid.z;
+  if (KT >= 4 && desync_ns(KT) > 0) {
+    int sms = 0;
+    unsigned* ctr = desync_counters(&sms);
+    if (ctr && ctas >= desync_min_waves() * 2LL * sms) {
+      desync = ctr;
+      first = 2 * sms;
+      ns = desync_ns(KT) * (3 * WJ) / 16;   // a tile's DMMA time relative to the 64 x 64 4-product tile
+    }
+  }
   const int group_m = (double)K * N * sizeof(double2) > 24e6 ? 32 : 1;
-  kern<<<grid, 64 / (8 * WI) * 64, T::SMEM, stream>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, stamp, g_prof.cap,
-                                                     group_m);
+  kern<<<grid, 128, T::SMEM, stream>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, stamp, g_prof.cap, desync, first,
+                                       ns, group_m);
   return cudaGetLastError();
 }
+
 // C -= A B (SET = false) or C = A B[brow] (SET = GATHER = true). The next k-stage's copies are
 // issued after the first k-quad's DMMAs (measured +1 % over issuing them at the top of the stage;
 // bitwise identical).
@@ -985,11 +1020,7 @@ static cudaError_t launch(int M, int N, int K, const double2* A, int lda, long l
     SSSVD_CUDA_TRY(launch_tma(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch, stream, stamp, &done));
     if (done) return cudaSuccess;
   }
-  if (which == 3) return launch_3m<4, 3, 255>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch, stream, stamp);
-  if (which == 4) return launch_3m<2, 3, 128>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch, stream, stamp);
-  if (which == 5) return launch_3m<4, 3, 244>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch, stream, stamp);
-  if (which == 6) return launch_3m<4, 3, 248>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch, stream, stamp);
-  if (which == 7) return launch_3m<4, 3, 240>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch, stream, stamp);
+  if (which == 3) return launch_3m<3>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch, stream, stamp);
   auto kern = zgemm_kernel<4, 4, SET, GATHER, 1>;
   SSSVD_CUDA_TRY(set_kernel_smem((const void*)kern, zgemm_sub_smem(), false));
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch);
