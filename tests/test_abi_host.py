@@ -42,8 +42,13 @@ def test_sass_uses_fp64_tensor_cores():
     sass = os.popen(f"/usr/local/cuda/bin/cuobjdump -sass {so} 2>/dev/null").read()
     funcs = sass.split("Function : ")
     zg = [f for f in funcs if "zgemm_kernel" in f[:60]]
+    z3 = [f for f in funcs if "zgemm3m_kernel" in f[:60]]
+    tm = [f for f in funcs if "zgemm_tma_kernel" in f[:60]]
     gr = [f for f in funcs if f.startswith("_ZN9sssvd_gpu11gram_kernel")]
-    assert zg and "DMMA.8x8x4" in zg[0]        # trailing update on the FP64 tensor pipe
+    assert z3 and z3[0].count("DMMA.8x8x4") >= 144   # 3M trailing update: 36 DMMAs per k-quad, 4 k-quads per stage
+    assert "LDGSTS" in z3[0] and "LDL" not in z3[0]  # cp.async staging, no register spill
+    assert zg and "DMMA.8x8x4" in zg[0]        # 4-product kernel (gather-GEMM, A/B comparator)
+    assert tm and "UTMALDG" in tm[0]           # its TMA form
     assert gr and "DMMA.8x8x4" in gr[0]        # Gram on the FP64 tensor pipe
 
 

@@ -61,6 +61,30 @@ def test_moments_match_oracle(dev, m, n, L, M, N, exp):
         assert err <= 1e-10, (k, err)
 
 
+def test_three_product_update_matches_four_product(monkeypatch):
+    """The LU's trailing updates use the 3-product (3M) complex GEMM by default; SSSVD_ZGEMM=4m
+    selects the 4-product kernel. Both paths' moment blocks agree with each other to roundoff times
+    the conditioning of the shifted solves, and each is as close to the oracle as the other
+    (profiles/r02_3m_sensitivity.txt has the full-size configs)."""
+    from paper_2109_13655_b200 import sssvd
+    m, n, L, M, N = 2000, 1000, 16, 8, 32
+    a = constructed(m, n, np.linspace(0.01, 1.0, n), 11, 12)
+    rg, ro = rules(0.45, 0.55, N, 0.1, True)
+    s0 = orc.random_start(n, L, 42)
+    ref = orc.MomentAccumulator(orc.form_gram(orc.ProblemMatrix(a), 1 << 30), ro).accumulate(s0, M).blocks
+    out = {}
+    for kernel in ("3m", "4m"):
+        monkeypatch.setenv("SSSVD_ZGEMM", kernel)
+        out[kernel] = gpu_blocks(sssvd.Device(0), a, rg, s0, M)   # a fresh context: no captured pass is replayed
+    monkeypatch.delenv("SSSVD_ZGEMM")
+    e3 = max(np.linalg.norm(out["3m"][k] - ref[k]) / np.linalg.norm(ref[k]) for k in range(M + 1))
+    e4 = max(np.linalg.norm(out["4m"][k] - ref[k]) / np.linalg.norm(ref[k]) for k in range(M + 1))
+    d34 = max(np.linalg.norm(out["3m"][k] - out["4m"][k]) / np.linalg.norm(ref[k]) for k in range(M + 1))
+    assert d34 > 0                       # the two kernels really are different arithmetic
+    assert e3 <= 1e-10 and e4 <= 1e-10 and d34 <= 1e-10
+    assert e3 <= 5 * e4 + 1e-13, (e3, e4)   # 3M is not measurably further from the oracle
+
+
 def test_batching_does_not_change_result(dev):
     """test_moments.cpp:205-215 (worker count) -> shifts-in-flight count: bitwise identical."""
     a = orc.random_matrix(300, 160, 91)
