@@ -211,10 +211,12 @@ sssvd_status sssvd_filter_profile(double a, double b, int64_t count, double aspe
 /* Instrumentation: number of kernels this library launched so far (process-wide), and live
  * CUDA-event timing of the dominant kernel (the DMMA trailing update) while enabled: `ms` is the
  * GEMM-busy time (union of the launch intervals; the shift groups overlap their GEMMs), `flops`
- * the algorithmic flops of those launches. */
+ * the EXECUTED tensor flops of those launches (6 M N K for a 3-product complex update, 8 M N K for a
+ * 4-product one); collect2 also returns the same work in the conventional 8 M N K unit. */
 uint64_t sssvd_gpu_launch_count(void);
 void sssvd_gpu_profile_gemm(int enable);
 void sssvd_gpu_profile_gemm_collect(double* ms, double* flops, uint64_t* launches);
+void sssvd_gpu_profile_gemm_collect2(double* ms, double* executed_flops, double* algorithmic_flops, uint64_t* launches);
 /* Debug: tile share `part` of `nparts` of form_gram (the multi-GPU Gram sharding), zeros
  * elsewhere; n x n column-major. */
 sssvd_status sssvd_debug_gram_part(sssvd_gpu_ctx* ctx, int part, int nparts, double* g_out);

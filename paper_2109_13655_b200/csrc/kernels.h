@@ -17,7 +17,7 @@ void note_launch(unsigned long long count = 1);
 unsigned long long launch_count();
 void unnote_launch(unsigned long long count);   // captured into a graph, not executed
 void zgemm_profile_enable(bool on);
-void zgemm_profile_collect(double* ms, double* flops, unsigned long long* launches);
+void zgemm_profile_collect(double* ms, double* flops, double* algorithmic, unsigned long long* launches);
 // GEMM stamps of one shifted-solve pass (zgemm.cu): begin resets the slots (stream-ordered, so it
 // is captured with a graph), end returns the per-slot flops, harvest folds a finished pass in
 cudaError_t zgemm_stamp_pass_begin(cudaStream_t s);

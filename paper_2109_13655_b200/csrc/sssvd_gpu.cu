@@ -1492,10 +1492,14 @@ extern "C" {
 
 uint64_t sssvd_gpu_launch_count(void) { return launch_count(); }
 void sssvd_gpu_profile_gemm(int enable) { zgemm_profile_enable(enable != 0); }
+void sssvd_gpu_profile_gemm_collect2(double* ms, double* executed_flops, double* algorithmic_flops, uint64_t* launches) {
+  unsigned long long n = 0;
+  zgemm_profile_collect(ms, executed_flops, algorithmic_flops, &n);
+  *launches = n;
+}
 void sssvd_gpu_profile_gemm_collect(double* ms, double* flops, uint64_t* launches) {
-  unsigned long long l = 0;
-  zgemm_profile_collect(ms, flops, &l);
-  *launches = l;
+  double alg = 0;
+  sssvd_gpu_profile_gemm_collect2(ms, flops, &alg, launches);
 }
 
 const char* sssvd_build_info(void) {

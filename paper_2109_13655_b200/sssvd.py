@@ -117,7 +117,7 @@ EXPORTED_SYMBOLS = [
     "sssvd_gpu_run_solve", "sssvd_result_info_get", "sssvd_result_copy", "sssvd_result_note",
     "sssvd_result_free", "sssvd_contour", "sssvd_random_start", "sssvd_validate_params",
     "sssvd_moment_coefficients", "sssvd_build_info", "sssvd_gpu_launch_count", "sssvd_gpu_profile_gemm",
-    "sssvd_gpu_profile_gemm_collect", "sssvd_debug_gram_part",
+    "sssvd_gpu_profile_gemm_collect", "sssvd_gpu_profile_gemm_collect2", "sssvd_debug_gram_part",
     "sssvd_gpu_set_operator_csc", "sssvd_mm_read", "sssvd_mm_info_get", "sssvd_mm_values", "sssvd_mm_colptr",
     "sssvd_mm_rowind", "sssvd_mm_free", "sssvd_mm_write", "sssvd_host_last_error", "sssvd_build_model",
     "sssvd_filter_profile", "sssvd_debug_thin_qr", "sssvd_debug_svd_square", "sssvd_debug_zgemm",
@@ -198,6 +198,9 @@ def lib():
     L.sssvd_gpu_profile_gemm_collect.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                                  ctypes.POINTER(ctypes.c_uint64)]
     L.sssvd_gpu_profile_gemm_collect.restype = None
+    L.sssvd_gpu_profile_gemm_collect2.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                                  ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]
+    L.sssvd_gpu_profile_gemm_collect2.restype = None
     _lib = L
     return L
 
@@ -357,10 +360,16 @@ def profile_gemm(enable: bool):
 
 
 def profile_gemm_collect():
-    """(total ms, algorithmic flops, launches) of the DMMA trailing-update kernel since enable."""
-    ms, fl, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_uint64()
-    lib().sssvd_gpu_profile_gemm_collect(ctypes.byref(ms), ctypes.byref(fl), ctypes.byref(n))
-    return ms.value, fl.value, int(n.value)
+    """(GEMM-busy ms, executed tensor flops, launches) of the DMMA GEMMs since enable."""
+    ms, fl, _, n = profile_gemm_collect2()
+    return ms, fl, n
+
+
+def profile_gemm_collect2():
+    """(GEMM-busy ms, executed tensor flops, the same work in 8 M N K units, launches) since enable."""
+    ms, fl, alg, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_uint64()
+    lib().sssvd_gpu_profile_gemm_collect2(ctypes.byref(ms), ctypes.byref(fl), ctypes.byref(alg), ctypes.byref(n))
+    return ms.value, fl.value, alg.value, int(n.value)
 
 
 def shard_range(h: int, nranks: int, rank: int):
