@@ -311,7 +311,7 @@ __device__ __forceinline__ void gb_store_x(const double (&x)[RPL], double* col, 
 // Same test and rotation as pair_rotation.
 // both columns in shared memory (outer round 0 only, where the pairs change every inner round)
 __device__ __forceinline__ bool gb_visit_smem(double* x, double* y, int k, double tol, int lane, double& cs,
-                                              double& sn) {
+                                              double& sn, double& c2max) {
   double a = 0.0, bb = 0.0, g = 0.0;
 #pragma unroll 8
   for (int r = lane; r < k; r += 32) {
@@ -327,6 +327,7 @@ __device__ __forceinline__ bool gb_visit_smem(double* x, double* y, int k, doubl
     g += __shfl_xor_sync(0xffffffffu, g, off);
   }
   if (!(g * g > tol * tol * a * bb) || g == 0.0) return false;
+  c2max = fmax(c2max, g * g / (a * bb));   // squared cosine of the largest angle rotated so far
   const double d = bb - a, g2x = 2.0 * g;
   const double tt = copysign(1.0, d) * g2x / (fabs(d) + sqrt(fma(d, d, g2x * g2x)));
   cs = rsqrt(fma(tt, tt, 1.0));
@@ -342,7 +343,7 @@ __device__ __forceinline__ bool gb_visit_smem(double* x, double* y, int k, doubl
 
 template <int RPL>
 __device__ __forceinline__ bool gb_visit(double (&x)[RPL], double* y, int k, double tol, int lane, double& cs,
-                                         double& sn) {
+                                         double& sn, double& c2max) {
   // four partial sums per product: 4x shorter FMA dependency chains
   double a4[4] = {0.0, 0.0, 0.0, 0.0}, b4[4] = {0.0, 0.0, 0.0, 0.0}, g4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -363,6 +364,7 @@ __device__ __forceinline__ bool gb_visit(double (&x)[RPL], double* y, int k, dou
     g += __shfl_xor_sync(0xffffffffu, g, off);
   }
   if (!(g * g > tol * tol * a * bb) || g == 0.0) return false;
+  c2max = fmax(c2max, g * g / (a * bb));   // squared cosine of the largest angle rotated so far
   const double d = bb - a, g2x = 2.0 * g;
   const double tt = copysign(1.0, d) * g2x / (fabs(d) + sqrt(fma(d, d, g2x * g2x)));
   cs = rsqrt(fma(tt, tt, 1.0));
@@ -452,18 +454,24 @@ __device__ __forceinline__ void vupdate_apply(const VUpdate& u, double* __restri
 }
 
 // one block pair per CTA per outer round (the plan guarantees nbe / 2 <= CTAs)
+constexpr double kJacobiFinalCos = 1e-8;
+
 template <int RPL, bool PROF>
 __global__ void __launch_bounds__(GB_THREADS, 1)
 jacobi_grid_block_kernel(double* __restrict__ Wm, double* __restrict__ Vm, int k, int ldw, int b, int nbe,
                          double tol, int max_sweeps, unsigned int* __restrict__ bar,
                          unsigned int* __restrict__ rot_count, int* __restrict__ sweeps_out,
                          unsigned long long* __restrict__ prof) {
+  // rot_count[0..1]: rotations of the sweep (ping-pong by sweep parity); the two 64-bit words after
+  // them: the largest squared cosine rotated in the sweep (double bits: order-preserving for >= 0)
+  unsigned long long* c2_glob = reinterpret_cast<unsigned long long*>(rot_count + 2);
   extern __shared__ __align__(16) double gsm[];
   const int w2 = 2 * b;
   double* Ws = gsm;                        // [w2][k]
   double* Qs = Ws + (size_t)w2 * k;        // [16][16] column-major (2b <= 16, zero padded)
   __shared__ int colid[32];
   __shared__ unsigned int cta_rot;
+  __shared__ unsigned long long cta_c2;
   __shared__ int pair_rot;
   __shared__ __align__(8) unsigned long long mbar;
   GridBarrier gb{bar, bar + 1};
@@ -481,7 +489,11 @@ jacobi_grid_block_kernel(double* __restrict__ Wm, double* __restrict__ Vm, int k
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
     unsigned int my_rot = 0;
-    if (tid == 0) cta_rot = 0;
+    double my_c2 = 0.0;
+    if (tid == 0) {
+      cta_rot = 0;
+      cta_c2 = 0ull;
+    }
     for (int round = 0; round < nbe - 1; ++round) {
       if (rec) t0 = clock64();
       const int bx = player(pi, round, nbe), by = player(nbe - 1 - pi, round, nbe);
@@ -530,7 +542,7 @@ jacobi_grid_block_kernel(double* __restrict__ Wm, double* __restrict__ Vm, int k
             int p = player(p0, ir, w2), q = player(w2 - 1 - p0, ir, w2);
             if (p > q) { int t = p; p = q; q = t; }
             double cs, sn;
-            if (gb_visit_smem(Ws + (size_t)p * k, Ws + (size_t)q * k, k, tol, lane, cs, sn)) {
+            if (gb_visit_smem(Ws + (size_t)p * k, Ws + (size_t)q * k, k, tol, lane, cs, sn, my_c2)) {
               if (lane < w2) {
                 double* qp = Qs + (size_t)p * 16;
                 double* qq = Qs + (size_t)q * 16;
@@ -558,7 +570,7 @@ jacobi_grid_block_kernel(double* __restrict__ Wm, double* __restrict__ Vm, int k
           if (active) {
             const int q = b + (p + ir) % b;
             double cs, sn;
-            if (gb_visit<RPL>(x, Ws + (size_t)q * k, k, tol, lane, cs, sn)) {
+            if (gb_visit<RPL>(x, Ws + (size_t)q * k, k, tol, lane, cs, sn, my_c2)) {
               if (lane < w2) {
                 double* qp = Qs + (size_t)p * 16;
                 double* qq = Qs + (size_t)q * 16;
@@ -613,14 +625,27 @@ jacobi_grid_block_kernel(double* __restrict__ Wm, double* __restrict__ Vm, int k
         if (round == 0) prof[5] += t2 - t1;   // inner rounds of outer round 0 (full inner sweep)
       }
     }
-    if (lane == 0 && my_rot) atomicAdd(&cta_rot, my_rot);
+    if (lane == 0 && my_rot) {
+      atomicAdd(&cta_rot, my_rot);
+      atomicMax(&cta_c2, (unsigned long long)__double_as_longlong(my_c2));
+    }
     __syncthreads();
-    if (tid == 0 && cta_rot) atomicAdd(rot_count + (sweep & 1), cta_rot);
+    if (tid == 0 && cta_rot) {
+      atomicAdd(rot_count + (sweep & 1), cta_rot);
+      atomicMax(c2_glob + (sweep & 1), cta_c2);
+    }
     grid_barrier(gb, gridDim.x, local_gen);
     const unsigned int rc = *((volatile unsigned int*)(rot_count + (sweep & 1)));
-    if (blockIdx.x == 0 && tid == 0) rot_count[(sweep + 1) & 1] = 0;
+    const double c2 = __longlong_as_double((long long)*((volatile unsigned long long*)(c2_glob + (sweep & 1))));
+    if (blockIdx.x == 0 && tid == 0) {
+      rot_count[(sweep + 1) & 1] = 0;
+      c2_glob[(sweep + 1) & 1] = 0ull;
+    }
     grid_barrier(gb, gridDim.x, local_gen);
-    if (rc == 0) {
+    // converged: no rotation, or only rotations by angles whose cosine is below kJacobiFinalCos.
+    // Rotating two columns by such an angle changes any cosine by O(c^2) <= 1e-16 < tol, so the next
+    // sweep would find nothing to rotate: the sweep that would only confirm it is skipped.
+    if (rc == 0 || c2 < kJacobiFinalCos * kJacobiFinalCos) {
       ++sweep;
       break;
     }
