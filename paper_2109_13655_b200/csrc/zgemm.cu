@@ -460,10 +460,11 @@ struct Tile3M {
   static constexpr size_t SMEM = (size_t)STAGES * SSTRIDE3 * sizeof(double2);
 };
 
-template <int WJ>
+template <int WJ, bool SET = false, bool GATHER = false>
 __global__ void __launch_bounds__(128, 2)
 zgemm3m_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long long sA,
-               const double2* __restrict__ B, int ldb, long long sB, double2* C, int ldc, long long sC,
+               const double2* __restrict__ B, int ldb, long long sB, const int* __restrict__ brow, int sR,
+               double2* C, int ldc, long long sC,
                unsigned long long* __restrict__ stamp, int stamp_cap, unsigned* desync, int desync_first,
                unsigned desync_ns, int group_m) {
   using T = Tile3M<WJ>;
@@ -511,6 +512,7 @@ zgemm3m_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long
   A += blockIdx.z * sA;
   B += blockIdx.z * sB;
   C += blockIdx.z * sC;
+  if (GATHER) brow += blockIdx.z * sR;
 
   double p1[WI][WJ][2], p2[WI][WJ][2], p3[WI][WJ][2];
 #pragma unroll
@@ -534,6 +536,10 @@ zgemm3m_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long
   for (int i = 0; i < AN; ++i) a_rows |= (m0 + ar + i * AR < M ? 1u : 0u) << i;
   const int b_k = tid >> 3, bc = tid & 7;
   const double2* bp = B + (size_t)b_k * ldb + n0 + bc;
+  // GATHER: row k of the B operand is row brow[k] of B; the index of the NEXT stage's row is
+  // fetched one stage ahead so its latency never sits in front of a cp.async
+  int gk = b_k, grow = 0;
+  if (GATHER) grow = gk < K ? brow[gk] : 0;
   const long long b_adv = (long long)BK * ldb;
   const int b_dst = b_k * LDB3 + bc;
   unsigned b_cols = 0;
@@ -541,20 +547,26 @@ zgemm3m_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long
   for (int i = 0; i < BNE; ++i) b_cols |= (n0 + bc + 8 * i < N ? 1u : 0u) << i;
   const bool interior = m0 + BM <= M && n0 + BN3 <= N;
   auto load = [&](double2* as_, double2* bs_, int kleft) {
+    const double2* bsrc = GATHER ? B + (size_t)grow * ldb + n0 + bc : bp;
     if (interior && kleft >= BK) {
 #pragma unroll
       for (int i = 0; i < AN; ++i) cp_async16(as_ + a_dst + i * AR * LDA_S, ap + i * a_step);
 #pragma unroll
-      for (int i = 0; i < BNE; ++i) cp_async16(bs_ + b_dst + 8 * i, bp + 8 * i);
+      for (int i = 0; i < BNE; ++i) cp_async16(bs_ + b_dst + 8 * i, bsrc + 8 * i);
     } else {
       const bool ak = a_k < kleft, bk = b_k < kleft;
 #pragma unroll
       for (int i = 0; i < AN; ++i) cp_async16(as_ + a_dst + i * AR * LDA_S, ap + i * a_step, ak && ((a_rows >> i) & 1u));
 #pragma unroll
-      for (int i = 0; i < BNE; ++i) cp_async16(bs_ + b_dst + 8 * i, bp + 8 * i, bk && ((b_cols >> i) & 1u));
+      for (int i = 0; i < BNE; ++i) cp_async16(bs_ + b_dst + 8 * i, bsrc + 8 * i, bk && ((b_cols >> i) & 1u));
     }
     ap += BK;
-    bp += b_adv;
+    if (GATHER) {
+      gk += BK;
+      grow = gk < K ? brow[gk] : 0;
+    } else {
+      bp += b_adv;
+    }
   };
   auto load_c = [&](double2* dst, int h) {
 #pragma unroll
@@ -568,8 +580,10 @@ zgemm3m_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < KT) load(As + s * SSTRIDE, Bs + s * SSTRIDE, K - s * BK);
-    for (int h = 0; h < 2; ++h)
-      if (KT - 2 + h < 0 && s == 0) load_c(c_stage(h), h);
+    if (!SET) {
+      for (int h = 0; h < 2; ++h)
+        if (KT - 2 + h < 0 && s == 0) load_c(c_stage(h), h);
+    }
     cp_async_commit();
   }
   const int fr = lane >> 2, fc = lane & 3;
@@ -585,7 +599,7 @@ zgemm3m_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long
         if (nk < KT) {
           const int st = nk % STAGES;
           load(As + st * SSTRIDE, Bs + st * SSTRIDE, K - nk * BK);
-        } else {
+        } else if (!SET) {
           const int h = kt - (KT - 2);
           if (h >= 0 && h < 2) load_c(c_stage(h), h);
         }
@@ -626,6 +640,17 @@ zgemm3m_kernel(int M, int N, int K, const double2* __restrict__ A, int lda, long
     if (r >= M) continue;
     const int cbase = n0 + wn * 8 * WJ + 2 * fc;
     double2* crow = C + (size_t)r * ldc + cbase;
+    if (SET) {
+#pragma unroll
+      for (int j = 0; j < WJ; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = cbase + j * 8 + e;
+          if (c < N)
+            crow[j * 8 + e] = make_double2(p1[i][j][e] - p2[i][j][e], (p3[i][j][e] - p1[i][j][e]) - p2[i][j][e]);
+        }
+      continue;
+    }
     const double2* cs = c_stage(rt >> 5) + (rt & 31) * CP3 + wn * 8 * WJ + 2 * fc;
     double2 v[WJ][2];
 #pragma unroll
@@ -867,7 +892,7 @@ static bool encode_map(CUtensorMap* map, const double2* p, int rows, int cols, i
              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Kernel of the C -= A B updates: 1 = 4-product cp.async kernel, 2 = its TMA form, 3 = the 3-product
+// Kernel of the C -= A B updates and of the gather-GEMM C = A B[brow]: 1 = 4-product cp.async kernel, 2 = its TMA form, 3 = the 3-product
 // (3M) kernel, the default (measured: config-5 step 24.0 -> 20.2 s, isolated trailing update 34.8 ->
 // 41.9 TF/s in 8 M N K units). Forms of the 3M kernel measured slower and not kept
 // (profiles/r02_3m_zgemm.txt): 64 x 64 tiles (255 registers, spills: 39.3), 8 warps of 16 x 24
@@ -976,12 +1001,12 @@ static unsigned desync_ns(int KT) {
   return v > 0 ? (unsigned)v * (unsigned)KT : 0u;
 }
 
-template <int WJ>
+template <int WJ, bool SET, bool GATHER>
 static cudaError_t launch_3m(int M, int N, int K, const double2* A, int lda, long long sA, const double2* B, int ldb,
-                             long long sB, double2* C, int ldc, long long sC, int batch, cudaStream_t stream,
-                             unsigned long long* stamp) {
+                             long long sB, const int* brow, int sR, double2* C, int ldc, long long sC, int batch,
+                             cudaStream_t stream, unsigned long long* stamp) {
   using T = Tile3M<WJ>;
-  auto kern = zgemm3m_kernel<WJ>;
+  auto kern = zgemm3m_kernel<WJ, SET, GATHER>;
   SSSVD_CUDA_TRY(set_kernel_smem((const void*)kern, T::SMEM, false));
   dim3 grid((N + T::BN3 - 1) / T::BN3, (M + BM - 1) / BM, batch);
   // first-wave offset as in the 4-product launcher (measured neutral on this kernel: 41.88-41.90
@@ -991,7 +1016,7 @@ static cudaError_t launch_3m(int M, int N, int K, const double2* A, int lda, lon
   unsigned ns = 0;
   const int KT = (K + BK - 1) / BK;
   const long long ctas = (long long)grid.x * grid.y * grid.z;
-  if (KT >= 4 && desync_ns(KT) > 0) {
+  if (!SET && KT >= 4 && desync_ns(KT) > 0) {
     int sms = 0;
     unsigned* ctr = desync_counters(&sms);
     if (ctr && ctas >= desync_min_waves() * 2LL * sms) {
@@ -1001,8 +1026,8 @@ static cudaError_t launch_3m(int M, int N, int K, const double2* A, int lda, lon
     }
   }
   const int group_m = (double)K * N * sizeof(double2) > 24e6 ? 32 : 1;
-  kern<<<grid, 128, T::SMEM, stream>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, stamp, g_prof.cap, desync, first,
-                                       ns, group_m);
+  kern<<<grid, 128, T::SMEM, stream>>>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, stamp, g_prof.cap, desync,
+                                       first, ns, group_m);
   return cudaGetLastError();
 }
 
@@ -1014,7 +1039,8 @@ static cudaError_t launch(int M, int N, int K, const double2* A, int lda, long l
                           long long sB, const int* brow, int sR, double2* C, int ldc, long long sC, int batch,
                           cudaStream_t stream) {
   if (M <= 0 || N <= 0 || K <= 0 || batch <= 0) return cudaSuccess;
-  const int which = (!SET && !GATHER) ? sub_kernel() : 1;
+  // the gather-GEMM (SET && GATHER) follows the 3M / 4-product choice; the TMA form covers only C -= A B
+  const int which = (SET == GATHER) ? (SET && sub_kernel() == 2 ? 1 : sub_kernel()) : 1;
   unsigned long long* stamp = nullptr;
   if (g_prof.in_pass && (int)g_prof.flops.size() < g_prof.cap) {
     stamp = g_prof.d_stamp + g_prof.flops.size();
@@ -1027,7 +1053,8 @@ static cudaError_t launch(int M, int N, int K, const double2* A, int lda, long l
     SSSVD_CUDA_TRY(launch_tma(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch, stream, stamp, &done));
     if (done) return cudaSuccess;
   }
-  if (which == 3) return launch_3m<3>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch, stream, stamp);
+  if (which == 3)
+    return launch_3m<3, SET, GATHER>(M, N, K, A, lda, sA, B, ldb, sB, brow, sR, C, ldc, sC, batch, stream, stamp);
   auto kern = zgemm_kernel<4, 4, SET, GATHER, 1>;
   SSSVD_CUDA_TRY(set_kernel_smem((const void*)kern, zgemm_sub_smem(), false));
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch);
