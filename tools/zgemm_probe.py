@@ -1,5 +1,6 @@
-"""Times the trailing-update GEMM on one shape through sssvd_debug_zgemm (variant 0 = cp.async
-kernel, 1 = TMA kernel) and reports TF/s and the bitwise check; under ncu it is the capture target.
+"""Times the trailing-update GEMM on one shape through sssvd_debug_zgemm (variant 0 = 4-product
+cp.async kernel, 1 = its TMA form, 2 = the 3-product (3M) kernel, the library default) and reports
+TF/s in 8 M N K units and the check against variant 0; under ncu it is the capture target.
     python tools/zgemm_probe.py [M N K batch reps variants]"""
 import ctypes
 import json
